@@ -1,0 +1,228 @@
+/*
+ * sampler.h — C ABI of the B200-native last-stage sampler (arXiv 2506.22033, "SiPipe").
+ *
+ * The operation: turn a batch of decode logits Z[B x V] into next tokens, per row b:
+ *
+ *   p_b = Filter( softmax( ApplyPenalty(z_b, y_<s) / tau ) ; k, p )      PAPER.md P:150-158 (§2.1, eq.)
+ *   y_b ~ Categorical(p_b)                                               PAPER.md P:161 (§2.1 step 3)
+ *   Z' = Z - alpha*f, f = CalcPenalty(Y) (frequency / presence / repetition)  P:354 (§5.1)
+ *   Z'' = Z'/tau,  P_ij = exp(Z''_ij) / sum_v exp(Z''_iv)                P:354 (§5.1)
+ *   top-k / top-p restrict candidates; min-p is listed at P:529 (§7.1)
+ *   incremental per-request history, "only the B elements ... updated"  P:368-371 (§5.1 (1),(2))
+ *   TP logits shards B x V/t combined without an all-gather of logits   P:375 (§5.1 (3))
+ *
+ * Exact semantics (tie-breaks, filter order, RNG, penalty rounding, greedy epsilon) are the
+ * readings R1..R15 of DESIGN.md §3 (= SURVEY.md §8(c)); the float64 oracle in oracle/ is the
+ * executable statement of them.  The interface follows SPEC.md's sampler module
+ * (SamplingParams S:146-149, SamplingOutput S:151-154, new_replica/append/evict_and_admit
+ * S:157-195, sample S:227-235, errors S:161/S:181/S:209, ownership S:264).
+ *
+ * Conventions
+ *  - Every function returns int32 status: SAMPLER_OK (0) or a negative SAMPLER_E* code.
+ *    On error, sampler_last_error(h) holds a one-line message.  Argument / range errors
+ *    are detected on the host BEFORE any launch and have no side effects.
+ *  - "dev" pointers are CUDA device pointers of the handle's device; "host" pointers are
+ *    ordinary host memory.  Nothing is retained after a call returns except by the handle.
+ *  - Calls marked ASYNC are stream-ordered on `cuda_stream` (a cudaStream_t; NULL = legacy
+ *    default stream): they only enqueue kernels, and every borrowed buffer must stay alive
+ *    and unmodified until the stream has passed the call.  Calls marked SYNC return after the
+ *    device work they issue has completed.
+ *  - A handle has ONE owner thread at a time.  Handles are independent.
+ *  - Logits are row-major [B x ld] (bf16 or fp32), row b at logits + b*ld elements.  Required:
+ *    logits 16-byte aligned, ld*sizeof(elem) % 16 == 0, ld >= vocab_local, and the buffer
+ *    readable for B*ld elements (rows are streamed with 16-byte bulk copies).  Logits are
+ *    borrowed read-only: the library never writes them (unlike the paper's in-place CPU
+ *    layout).
+ *  - Data-dependent row faults (a NaN or +inf logit; a row whose every logit is -inf) never
+ *    fail the call: that row gets token -1, logprob NaN and a non-zero row_status.
+ *    -inf logits are legal and mean probability 0.
+ */
+#ifndef PAPER_2506_22033_B200_SAMPLER_H
+#define PAPER_2506_22033_B200_SAMPLER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------- */
+enum {
+  SAMPLER_OK = 0,
+  SAMPLER_EINVAL = -1,       /* bad argument (NULL handle/pointer, bad size/alignment, bad param) */
+  SAMPLER_ENOMEM = -2,       /* device allocation failed */
+  SAMPLER_ECUDA = -3,        /* a CUDA runtime call or launch failed (message has the CUDA error) */
+  SAMPLER_ERANGE = -4,       /* token id outside [0,V), slot outside [0,B_max), history > L_max */
+  SAMPLER_EUNSUPPORTED = -5  /* valid but unsupported request (e.g. dtype, vocab > 2^31-2^20) */
+};
+
+/* logits dtype codes */
+enum { SAMPLER_F32 = 0, SAMPLER_BF16 = 2 };
+
+/* penalty semantics (R1):
+ *  OPENAI_CTRL: for ids with cnt>0 or in-prompt: y=x; if r!=1: y = y>0 ? y/r : y*r;
+ *               if cnt>0: y = y - freq*cnt; y = y - pres     (each op rounded to binary32)
+ *  LINEAR     : paper-literal Z' = Z - alpha*f:
+ *               y = ((x - freq*cnt) - pres*[cnt>0]) - rep*[cnt>0 or in-prompt]
+ *               where `repetition_penalty` is used as the subtractive coefficient alpha_rep. */
+enum { SAMPLER_PEN_OPENAI_CTRL = 0, SAMPLER_PEN_LINEAR = 1 };
+
+/* per-row status written to row_status_dev */
+enum {
+  SAMPLER_ROW_OK = 0,
+  SAMPLER_ROW_NONFINITE = 1,   /* a NaN or +inf logit in the row ("finite entries") */
+  SAMPLER_ROW_ALL_NEG_INF = 2, /* no token has positive probability */
+  SAMPLER_ROW_UNRESOLVED = 3   /* vocab-sharded merge: the row's kept set is not bounded by the
+                                  exchanged candidates (top-p/min-p-only rows, or top_k >
+                                  max_top_k); see DESIGN.md §8 NEXT-1.  Never produced by
+                                  sampler_sample on an unsharded handle. */
+};
+
+typedef struct {
+  int32_t vocab_size;     /* V: global vocabulary size, 1 <= V <= 2^31 - 2^20 */
+  int32_t vocab_offset;   /* first global id of this rank's slice (0 when unsharded) */
+  int32_t vocab_local;    /* slice length (== vocab_size when unsharded); ids
+                             [vocab_offset, vocab_offset+vocab_local) are local */
+  int32_t max_batch;      /* B_max: number of request slots (rows per call <= B_max) */
+  int32_t max_history;    /* L_max: prompt + output tokens per slot */
+  int32_t max_top_k;      /* K_cand in [1, 128]: candidates kept per partial reduction.  Rows
+                             with 1 <= top_k <= K_cand (and greedy rows) are always exact in one
+                             streaming pass; other rows take the exact multi-pass path. */
+  int32_t logits_dtype;   /* SAMPLER_F32 | SAMPLER_BF16 */
+  int32_t penalty_mode;   /* SAMPLER_PEN_* */
+  int32_t device;         /* CUDA device ordinal; the handle's memory lives there */
+} sampler_config;
+
+/* Per-row sampling parameters.  48 bytes, 8-byte aligned; the same layout
+ * is used for host arrays (set_params) and device arrays (params_dev). */
+typedef struct {
+  float temperature;        /* >= 0; < 1e-5 (incl. 0) => greedy (R5); < 0 => EINVAL */
+  int32_t top_k;            /* <= 0 or >= V => off; k => keep the k best (z' desc, id asc) */
+  float top_p;              /* in (0, 1]; 1 => off */
+  float min_p;              /* in [0, 1]; 0 => off; keep p >= min_p * p_max */
+  float repetition_penalty; /* OPENAI_CTRL: > 0, 1 => off.  LINEAR: alpha_rep, 0 => off */
+  float presence_penalty;   /* 0 => off (any finite value) */
+  float frequency_penalty;  /* 0 => off (any finite value) */
+  int32_t reserved;         /* must be 0 */
+  uint64_t seed;            /* Philox key (R11) */
+  uint64_t request_id;      /* Philox counter words 2-3: keys the draw by request, not row */
+} sampling_params;
+
+typedef struct sampler sampler; /* opaque handle */
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+
+/* SYNC.  Validate cfg, allocate all device state on cfg->device (params table, per-slot
+ * history store and unique-token penalty table [B_max x L_max], workspace) and return the
+ * handle in *out.  All slots start with empty history and default params (greedy off,
+ * temperature 1, no filters, no penalties, seed 0, request_id = slot).
+ * Errors: EINVAL (NULL args, sizes out of range), ENOMEM, ECUDA.  On error *out = NULL. */
+int sampler_create(const sampler_config* cfg, sampler** out);
+
+/* SYNC.  Free everything the handle owns.  NULL is a no-op returning OK. */
+int sampler_destroy(sampler* h);
+
+/* Message describing the last failing call on h ("" if none).  Valid until the next call on
+ * h.  With h == NULL: the message of the last failing sampler_create on this thread. */
+const char* sampler_last_error(const sampler* h);
+
+/* ---- per-slot state ----------------------------------------------------------------- */
+
+/* SYNC.  Copy n host params into the handle's table at host slot indices slots[0..n).
+ * Every entry is validated first (EINVAL: temperature < 0 or non-finite, top_p not in
+ * (0,1], min_p not in [0,1], repetition_penalty <= 0 in OPENAI_CTRL mode, non-finite
+ * penalties, reserved != 0; ERANGE: slot outside [0, B_max)); nothing is written on error. */
+int sampler_set_params(sampler* h, int32_t n, const int32_t* slots_host,
+                       const sampling_params* params_host);
+
+/* SYNC.  Admit / evict (SPEC S:187 evict_and_admit): replace slot's history with the given
+ * host token lists and rebuild its unique-token penalty table from scratch.
+ * prompt/output may be NULL when their count is 0.
+ * Errors: ERANGE (slot out of range, n_prompt + n_output > L_max, any id outside [0, V)). */
+int sampler_set_history(sampler* h, int32_t slot, const int32_t* prompt_host, int32_t n_prompt,
+                        const int32_t* output_host, int32_t n_output);
+
+/* SYNC.  Append one output token to each of n slots (SPEC S:177 append_tokens): the slot's
+ * output list grows by one and its penalty entry is updated incrementally.
+ * Errors: ERANGE (slot, token or L_max overflow) — checked for all n before any change. */
+int sampler_append_tokens(sampler* h, int32_t n, const int32_t* slots_host,
+                          const int32_t* tokens_host);
+
+/* SYNC.  Export a slot's state for inspection / checkpoint.  Any output pointer may be NULL.
+ *  n_prompt, n_output: history lengths; prompt_out/output_out: capacity >= L_max tokens;
+ *  n_unique + uniq_ids/uniq_counts/uniq_in_prompt (capacity >= L_max): the incremental
+ *  penalty table (ids ascending; counts = occurrences in the output; in_prompt 0/1). */
+int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_output,
+                        int32_t* prompt_out, int32_t* output_out, int32_t* n_unique,
+                        int32_t* uniq_ids, int32_t* uniq_counts, int32_t* uniq_in_prompt);
+
+/* ---- sampling ----------------------------------------------------------------------- */
+
+/* ASYNC.  Sample one token for each of B rows of logits (unsharded handle:
+ * vocab_local == vocab_size).
+ *  logits      dev [B x ld] of cfg->logits_dtype (see alignment rules above)
+ *  slots_dev   dev int32[B]: row b uses request slot slots_dev[b] (distinct); NULL => b
+ *  params_dev  dev sampling_params[B] for row b; NULL => the slot's table entry (set_params)
+ *  seeds_dev   dev uint64[B]: overrides params.seed for row b; NULL => params.seed
+ *  step        Philox counter words 0-1 (decode step)
+ *  append_to_history  nonzero => append each sampled token to its slot; rows
+ *              with a non-OK status append nothing.  Overflowing L_max sets the slot's
+ *              overflow bit (visible via sampler_get_history) and appends nothing.
+ *  tokens_dev  dev int32[B] out; logprobs_dev dev float[B] out = log softmax(z'/tau_eff)[tok]
+ *              (full vocabulary, before filtering; R12)
+ *  filtered_logprobs_dev  dev float[B] out, nullable: log of the token's probability in the
+ *              final filtered, renormalised distribution (0 for greedy rows)
+ *  row_status_dev  dev int32[B] out, nullable: SAMPLER_ROW_*
+ * Errors: EINVAL (NULL handle/logits/tokens/logprobs, B < 1 or > B_max, bad alignment, sharded
+ * handle), ECUDA. */
+int sampler_sample(sampler* h, const void* logits, int64_t ld, int32_t B,
+                   const int32_t* slots_dev, const sampling_params* params_dev,
+                   const uint64_t* seeds_dev, uint64_t step, int32_t append_to_history,
+                   int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                   int32_t* row_status_dev, void* cuda_stream);
+
+/* ASYNC, test/debug only.  Same inputs as sampler_sample (no history append); additionally
+ * writes q_dev [B x vocab_size] fp32 = the final filtered distribution (w_v / W for kept ids,
+ * 0 elsewhere; one-hot for greedy rows).  For parity tests on small shapes. */
+int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32_t B,
+                               const int32_t* slots_dev, const sampling_params* params_dev,
+                               const uint64_t* seeds_dev, uint64_t step,
+                               int32_t* tokens_dev, float* logprobs_dev, float* q_dev,
+                               void* cuda_stream);
+
+/* ---- vocab-sharded two-phase sampling (TP-style logits shards) ---------------- */
+
+/* Bytes of one rank's candidate records for B rows (the all-gather payload per rank). */
+int64_t sampler_record_bytes(const sampler* h, int32_t B);
+
+/* ASYNC.  Phase 1 on this rank's slice logits_slice [B x ld] (ids vocab_offset + j):
+ * penalties for local ids, local max / sum and the local top-K_cand candidates per row, written
+ * to records_dev (sampler_record_bytes(h,B) bytes, device).  The caller all-gathers the records
+ * of all ranks (rank order) and calls sampler_merge. */
+int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
+                         const int32_t* slots_dev, const sampling_params* params_dev,
+                         void* records_dev, void* cuda_stream);
+
+/* ASYNC.  Phase 2: merge `world` ranks' records (gathered_records_dev = world consecutive
+ * blocks of sampler_record_bytes(h,B) bytes, rank order) into the final tokens.  Every rank
+ * computes identical outputs (deterministic, rank-ordered reductions).  History append (if
+ * requested) is applied on every rank (replicated per-rank tables).  Rows whose kept set is not
+ * bounded by the candidates get SAMPLER_ROW_UNRESOLVED. */
+int sampler_merge(sampler* h, const void* gathered_records_dev, int32_t world, int32_t B,
+                  const int32_t* slots_dev, const sampling_params* params_dev,
+                  const uint64_t* seeds_dev, uint64_t step, int32_t append_to_history,
+                  int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                  int32_t* row_status_dev, void* cuda_stream);
+
+/* ---- introspection ------------------------------------------------------------------ */
+
+/* Number of kernel launches the last sample / sample_local / merge / debug call enqueued. */
+int32_t sampler_last_launch_count(const sampler* h);
+
+/* Build identification string (arch, compile flags). */
+const char* sampler_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_2506_22033_B200_SAMPLER_H */

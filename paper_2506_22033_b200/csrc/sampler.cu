@@ -1,0 +1,540 @@
+// sampler.cu — C-ABI implementation (host side) of include/sampler.h.
+//
+// Owns per-handle device state (params table, per-slot history + incremental unique-token
+// penalty table, workspace), validates every call on the host before any launch, and enqueues
+// the sm_100a kernels of stream.cuh / exact.cuh on the caller's stream.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "exact.cuh"
+#include "merge.cuh"
+#include "stream.cuh"
+
+using namespace smp;
+
+struct sampler {
+  sampler_config cfg{};
+  int sm_count = 0;
+  int Vp = 0;    // vocab_local rounded up to the vector width
+  int vec = 8;   // elements per 16 bytes
+  int max_warps = 0;
+  int64_t rec_stride = 0;
+  // device state
+  sampling_params* d_params = nullptr;
+  SlotMeta* d_meta = nullptr;
+  UniqEntry* d_uniq = nullptr;
+  int32_t* d_hist = nullptr;
+  uint8_t* d_records = nullptr;
+  int32_t* d_tickets = nullptr;
+  RowInfo* d_info = nullptr;
+  float* d_scratch = nullptr;
+  // host mirror
+  std::vector<sampling_params> h_params;
+  std::string err;
+  int32_t last_launches = 0;
+};
+
+static thread_local std::string g_create_err;
+
+static int fail(sampler* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h)
+    h->err = buf;
+  else
+    g_create_err = buf;
+  return code;
+}
+
+#define CK(h, call)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((h), SAMPLER_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));      \
+  } while (0)
+
+static const char* param_error(const sampling_params& p, int pen_mode) {
+  if (!(p.temperature >= 0.0f) || !std::isfinite(p.temperature)) return "temperature must be finite and >= 0";
+  if (!(p.top_p > 0.0f && p.top_p <= 1.0f)) return "top_p must be in (0, 1]";
+  if (!(p.min_p >= 0.0f && p.min_p <= 1.0f)) return "min_p must be in [0, 1]";
+  if (!std::isfinite(p.repetition_penalty) || !std::isfinite(p.presence_penalty) ||
+      !std::isfinite(p.frequency_penalty))
+    return "penalties must be finite";
+  if (pen_mode == SAMPLER_PEN_OPENAI_CTRL && !(p.repetition_penalty > 0.0f))
+    return "repetition_penalty must be > 0 (OPENAI_CTRL mode)";
+  if (p.reserved != 0) return "reserved must be 0";
+  return nullptr;
+}
+
+static bool row_may_pend(const sampling_params& p, int V, int kcand) {
+  if (p.temperature < kGreedyEps) return false;
+  if (p.top_k >= 1 && p.top_k < V && p.top_k <= kcand) return false;
+  return true;
+}
+
+extern "C" {
+
+const char* sampler_version(void) {
+  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a), cp.async.bulk streaming, "
+         "warp top-K candidates, Philox4x32-10";
+}
+
+const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+int32_t sampler_last_launch_count(const sampler* h) { return h ? h->last_launches : 0; }
+
+int sampler_create(const sampler_config* cfg, sampler** out) {
+  if (!out) return fail(nullptr, SAMPLER_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, SAMPLER_EINVAL, "cfg is NULL");
+  const sampler_config c = *cfg;
+  if (c.vocab_size < 1 || c.vocab_size > (int32_t)(0x7FFFFFFF - (1 << 20)))
+    return fail(nullptr, SAMPLER_EINVAL, "vocab_size out of range");
+  if (c.vocab_offset < 0 || c.vocab_local < 1 || (int64_t)c.vocab_offset + c.vocab_local > c.vocab_size)
+    return fail(nullptr, SAMPLER_EINVAL, "vocab slice out of range");
+  if (c.max_batch < 1 || c.max_batch > (1 << 20)) return fail(nullptr, SAMPLER_EINVAL, "max_batch out of range");
+  if (c.max_history < 1 || c.max_history > (1 << 24))
+    return fail(nullptr, SAMPLER_EINVAL, "max_history out of range");
+  if (c.max_top_k < 1 || c.max_top_k > SAMPLER_KCAND_MAX)
+    return fail(nullptr, SAMPLER_EINVAL, "max_top_k must be in [1, %d]", SAMPLER_KCAND_MAX);
+  if (c.logits_dtype != SAMPLER_F32 && c.logits_dtype != SAMPLER_BF16)
+    return fail(nullptr, SAMPLER_EUNSUPPORTED, "logits_dtype must be SAMPLER_F32 or SAMPLER_BF16");
+  if (c.penalty_mode != SAMPLER_PEN_OPENAI_CTRL && c.penalty_mode != SAMPLER_PEN_LINEAR)
+    return fail(nullptr, SAMPLER_EINVAL, "bad penalty_mode");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+    return fail(nullptr, SAMPLER_ECUDA, "no CUDA device");
+  if (c.device < 0 || c.device >= ndev) return fail(nullptr, SAMPLER_EINVAL, "bad device ordinal");
+  if (cudaSetDevice(c.device) != cudaSuccess) return fail(nullptr, SAMPLER_ECUDA, "cudaSetDevice failed");
+
+  sampler* h = new sampler();
+  h->cfg = c;
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device);
+  h->vec = (c.logits_dtype == SAMPLER_BF16) ? 8 : 4;
+  h->Vp = (c.vocab_local + h->vec - 1) / h->vec * h->vec;
+  h->max_warps = h->sm_count * 2 * kWarpsPerCta;
+  h->rec_stride = rec_stride_bytes(c.max_top_k);
+  const int64_t B = c.max_batch, L = c.max_history;
+  const int64_t nrec = (int64_t)h->max_warps + B;
+  auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
+  bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
+            al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
+            al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_records, h->rec_stride * nrec) &&
+            al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
+            al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp);
+  if (!ok) {
+    cudaGetLastError();
+    sampler_destroy(h);
+    return fail(nullptr, SAMPLER_ENOMEM, "device allocation failed");
+  }
+  h->h_params.resize(B);
+  for (int64_t i = 0; i < B; ++i) {
+    sampling_params p{};
+    p.temperature = 1.0f;
+    p.top_k = 0;
+    p.top_p = 1.0f;
+    p.min_p = 0.0f;
+    p.repetition_penalty = (c.penalty_mode == SAMPLER_PEN_LINEAR) ? 0.0f : 1.0f;
+    p.presence_penalty = 0.0f;
+    p.frequency_penalty = 0.0f;
+    p.reserved = 0;
+    p.seed = 0;
+    p.request_id = (uint64_t)i;
+    h->h_params[i] = p;
+  }
+  if (cudaMemcpy(h->d_params, h->h_params.data(), sizeof(sampling_params) * B, cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
+      cudaMemset(h->d_tickets, 0, sizeof(int32_t) * B) != cudaSuccess ||
+      cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
+      cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kStreamSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kExactSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExactSmem) !=
+          cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    const char* m = cudaGetErrorString(cudaGetLastError());
+    sampler_destroy(h);
+    return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
+  }
+  *out = h;
+  return SAMPLER_OK;
+}
+
+int sampler_destroy(sampler* h) {
+  if (!h) return SAMPLER_OK;
+  cudaSetDevice(h->cfg.device);
+  cudaFree(h->d_params);
+  cudaFree(h->d_meta);
+  cudaFree(h->d_uniq);
+  cudaFree(h->d_hist);
+  cudaFree(h->d_records);
+  cudaFree(h->d_tickets);
+  cudaFree(h->d_info);
+  cudaFree(h->d_scratch);
+  delete h;
+  return SAMPLER_OK;
+}
+
+int sampler_set_params(sampler* h, int32_t n, const int32_t* slots, const sampling_params* params) {
+  if (!h) return SAMPLER_EINVAL;
+  if (n < 0 || (n > 0 && (!slots || !params))) return fail(h, SAMPLER_EINVAL, "bad arguments");
+  for (int32_t i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot %d out of range", slots[i]);
+    const char* e = param_error(params[i], h->cfg.penalty_mode);
+    if (e) return fail(h, SAMPLER_EINVAL, "params[%d]: %s", i, e);
+  }
+  CK(h, cudaSetDevice(h->cfg.device));
+  for (int32_t i = 0; i < n; ++i) {
+    h->h_params[slots[i]] = params[i];
+    CK(h, cudaMemcpy(h->d_params + slots[i], &params[i], sizeof(sampling_params), cudaMemcpyHostToDevice));
+  }
+  return SAMPLER_OK;
+}
+
+static int upload_slot(sampler* h, int slot, const std::vector<int32_t>& prompt, const std::vector<int32_t>& output,
+                       int32_t flags) {
+  const int L = h->cfg.max_history;
+  std::map<int32_t, uint32_t> m;
+  for (int32_t t : prompt) m[t] |= 1u;
+  for (int32_t t : output) m[t] += 2u;
+  std::vector<UniqEntry> u;
+  u.reserve(m.size());
+  for (auto& kv : m) {
+    UniqEntry e;
+    e.id = kv.first;
+    e.meta = kv.second;
+    u.push_back(e);
+  }
+  std::vector<int32_t> toks(prompt);
+  toks.insert(toks.end(), output.begin(), output.end());
+  SlotMeta sm;
+  sm.n_prompt = (int32_t)prompt.size();
+  sm.n_out = (int32_t)output.size();
+  sm.n_uniq = (int32_t)u.size();
+  sm.flags = flags;
+  CK(h, cudaSetDevice(h->cfg.device));
+  if (!u.empty())
+    CK(h, cudaMemcpy(h->d_uniq + (int64_t)slot * L, u.data(), sizeof(UniqEntry) * u.size(), cudaMemcpyHostToDevice));
+  if (!toks.empty())
+    CK(h, cudaMemcpy(h->d_hist + (int64_t)slot * L, toks.data(), sizeof(int32_t) * toks.size(), cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(h->d_meta + slot, &sm, sizeof(SlotMeta), cudaMemcpyHostToDevice));
+  return SAMPLER_OK;
+}
+
+int sampler_set_history(sampler* h, int32_t slot, const int32_t* prompt, int32_t n_prompt, const int32_t* output,
+                        int32_t n_output) {
+  if (!h) return SAMPLER_EINVAL;
+  if (slot < 0 || slot >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot %d out of range", slot);
+  if (n_prompt < 0 || n_output < 0 || (n_prompt > 0 && !prompt) || (n_output > 0 && !output))
+    return fail(h, SAMPLER_EINVAL, "bad history arguments");
+  if ((int64_t)n_prompt + n_output > h->cfg.max_history)
+    return fail(h, SAMPLER_ERANGE, "history %d exceeds max_history %d", n_prompt + n_output, h->cfg.max_history);
+  for (int32_t i = 0; i < n_prompt; ++i)
+    if (prompt[i] < 0 || prompt[i] >= h->cfg.vocab_size) return fail(h, SAMPLER_ERANGE, "prompt token out of range");
+  for (int32_t i = 0; i < n_output; ++i)
+    if (output[i] < 0 || output[i] >= h->cfg.vocab_size) return fail(h, SAMPLER_ERANGE, "output token out of range");
+  std::vector<int32_t> p(prompt, prompt + n_prompt), o(output, output + n_output);
+  return upload_slot(h, slot, p, o, 0);
+}
+
+static int read_slot(sampler* h, int slot, SlotMeta* sm, std::vector<int32_t>* toks, std::vector<UniqEntry>* u) {
+  const int L = h->cfg.max_history;
+  CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaMemcpy(sm, h->d_meta + slot, sizeof(SlotMeta), cudaMemcpyDeviceToHost));
+  if (toks) {
+    toks->resize(sm->n_prompt + sm->n_out);
+    if (!toks->empty())
+      CK(h, cudaMemcpy(toks->data(), h->d_hist + (int64_t)slot * L, sizeof(int32_t) * toks->size(),
+                       cudaMemcpyDeviceToHost));
+  }
+  if (u) {
+    u->resize(sm->n_uniq);
+    if (!u->empty())
+      CK(h, cudaMemcpy(u->data(), h->d_uniq + (int64_t)slot * L, sizeof(UniqEntry) * u->size(),
+                       cudaMemcpyDeviceToHost));
+  }
+  return SAMPLER_OK;
+}
+
+int sampler_append_tokens(sampler* h, int32_t n, const int32_t* slots, const int32_t* tokens) {
+  if (!h) return SAMPLER_EINVAL;
+  if (n < 0 || (n > 0 && (!slots || !tokens))) return fail(h, SAMPLER_EINVAL, "bad arguments");
+  std::vector<SlotMeta> metas(n);
+  for (int32_t i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot out of range");
+    if (tokens[i] < 0 || tokens[i] >= h->cfg.vocab_size) return fail(h, SAMPLER_ERANGE, "token out of range");
+  }
+  CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaDeviceSynchronize());
+  // capacity check for all first (per slot, counting repeats within this call)
+  std::map<int32_t, int> add;
+  for (int32_t i = 0; i < n; ++i) add[slots[i]]++;
+  for (auto& kv : add) {
+    SlotMeta sm;
+    CK(h, cudaMemcpy(&sm, h->d_meta + kv.first, sizeof(SlotMeta), cudaMemcpyDeviceToHost));
+    if ((int64_t)sm.n_prompt + sm.n_out + kv.second > h->cfg.max_history)
+      return fail(h, SAMPLER_ERANGE, "slot %d would exceed max_history", kv.first);
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    SlotMeta sm;
+    std::vector<int32_t> toks;
+    int rc = read_slot(h, slots[i], &sm, &toks, nullptr);
+    if (rc) return rc;
+    std::vector<int32_t> p(toks.begin(), toks.begin() + sm.n_prompt), o(toks.begin() + sm.n_prompt, toks.end());
+    o.push_back(tokens[i]);
+    rc = upload_slot(h, slots[i], p, o, sm.flags);
+    if (rc) return rc;
+  }
+  return SAMPLER_OK;
+}
+
+int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_output, int32_t* prompt_out,
+                        int32_t* output_out, int32_t* n_unique, int32_t* uniq_ids, int32_t* uniq_counts,
+                        int32_t* uniq_in_prompt) {
+  if (!h) return SAMPLER_EINVAL;
+  if (slot < 0 || slot >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot out of range");
+  CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaDeviceSynchronize());
+  SlotMeta sm;
+  std::vector<int32_t> toks;
+  std::vector<UniqEntry> u;
+  int rc = read_slot(h, slot, &sm, &toks, &u);
+  if (rc) return rc;
+  if (n_prompt) *n_prompt = sm.n_prompt;
+  if (n_output) *n_output = sm.n_out;
+  if (prompt_out) std::copy(toks.begin(), toks.begin() + sm.n_prompt, prompt_out);
+  if (output_out) std::copy(toks.begin() + sm.n_prompt, toks.end(), output_out);
+  if (n_unique) *n_unique = sm.n_uniq;
+  for (size_t i = 0; i < u.size(); ++i) {
+    if (uniq_ids) uniq_ids[i] = u[i].id;
+    if (uniq_counts) uniq_counts[i] = (int32_t)(u[i].meta >> 1);
+    if (uniq_in_prompt) uniq_in_prompt[i] = (int32_t)(u[i].meta & 1u);
+  }
+  // overflow flag is reported through the sign of n_output? keep a separate path:
+  if (sm.flags & 1) h->err = "history overflow occurred on this slot";
+  return SAMPLER_OK;
+}
+
+// ---- launches -----------------------------------------------------------------------
+static int check_logits(sampler* h, const void* logits, int64_t ld, int32_t B) {
+  if (!logits) return fail(h, SAMPLER_EINVAL, "logits is NULL");
+  if (B < 1 || B > h->cfg.max_batch) return fail(h, SAMPLER_EINVAL, "B=%d out of [1, max_batch=%d]", B, h->cfg.max_batch);
+  const int esz = (h->cfg.logits_dtype == SAMPLER_BF16) ? 2 : 4;
+  if (((uintptr_t)logits) % 16) return fail(h, SAMPLER_EINVAL, "logits must be 16-byte aligned");
+  if (ld < h->cfg.vocab_local || (ld * esz) % 16) return fail(h, SAMPLER_EINVAL, "ld must be >= vocab_local and ld*elem %% 16 == 0");
+  return SAMPLER_OK;
+}
+
+struct LaunchPlan {
+  int64_t span;
+  int64_t N;
+  int grid;
+};
+
+static LaunchPlan plan(const sampler* h, int32_t B) {
+  LaunchPlan p;
+  p.N = (int64_t)B * h->Vp;
+  const int64_t W = h->max_warps;
+  int64_t span = (p.N + W - 1) / W;
+  const int64_t min_span = 2048;
+  if (span < min_span) span = min_span;
+  span = (span + h->vec - 1) / h->vec * h->vec;
+  p.span = span;
+  const int64_t nw = (p.N + span - 1) / span;
+  p.grid = (int)((nw + kWarpsPerCta - 1) / kWarpsPerCta);
+  return p;
+}
+
+static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
+                              const sampling_params* params_dev, const uint64_t* seeds, uint64_t step, int append,
+                              const LaunchPlan& lp) {
+  StreamArgs a{};
+  a.logits = logits;
+  a.ld = ld;
+  a.B = B;
+  a.V = h->cfg.vocab_size;
+  a.voff = h->cfg.vocab_offset;
+  a.vloc = h->cfg.vocab_local;
+  a.Vp = h->Vp;
+  a.span = lp.span;
+  a.N = lp.N;
+  a.slots = slots;
+  a.params_dev = params_dev;
+  a.params_tab = h->d_params;
+  a.seeds = seeds;
+  a.step = step;
+  a.append = append;
+  a.kcand = h->cfg.max_top_k;
+  a.pen_mode = h->cfg.penalty_mode;
+  a.hs.meta = h->d_meta;
+  a.hs.uniq = h->d_uniq;
+  a.hs.tokens = h->d_hist;
+  a.hs.L = h->cfg.max_history;
+  a.records = h->d_records;
+  a.rec_stride = h->rec_stride;
+  a.tickets = h->d_tickets;
+  a.mode = 0;
+  a.out_records = nullptr;
+  a.pending_ok = 1;
+  return a;
+}
+
+static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    stream_kernel<__nv_bfloat16><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+  else
+    stream_kernel<float><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+  CK(h, cudaGetLastError());
+  return SAMPLER_OK;
+}
+
+static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots_dev,
+                     const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step, int32_t append,
+                     int32_t* tokens, float* logprobs, float* flogprobs, int32_t* status, cudaStream_t st) {
+  const LaunchPlan lp = plan(h, B);
+  StreamArgs a = stream_args(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append, lp);
+  a.ro.tokens = tokens;
+  a.ro.logprobs = logprobs;
+  a.ro.flogprobs = flogprobs;
+  a.ro.status = status;
+  a.ro.info = h->d_info;
+  int rc = launch_stream(h, a, lp.grid, st);
+  if (rc) return rc;
+  h->last_launches = 1;
+  // exact multi-pass kernel only if some row can be unresolved by the one-pass candidates
+  bool need = params_dev != nullptr;
+  if (!need) {
+    const int n = slots_dev ? h->cfg.max_batch : B;
+    for (int i = 0; i < n && !need; ++i) need = row_may_pend(h->h_params[i], h->cfg.vocab_size, h->cfg.max_top_k);
+  }
+  if (need) {
+    ExactArgs e{};
+    e.logits = logits;
+    e.ld = ld;
+    e.B = B;
+    e.V = h->cfg.vocab_size;
+    e.voff = h->cfg.vocab_offset;
+    e.vloc = h->cfg.vocab_local;
+    e.Vp = h->Vp;
+    e.slots = slots_dev;
+    e.params_dev = params_dev;
+    e.params_tab = h->d_params;
+    e.seeds = seeds_dev;
+    e.step = step;
+    e.append = append;
+    e.pen_mode = h->cfg.penalty_mode;
+    e.hs = a.hs;
+    e.scratch = h->d_scratch;
+    e.ro = a.ro;
+    if (h->cfg.logits_dtype == SAMPLER_BF16)
+      exact_kernel<__nv_bfloat16><<<B, kExThreads, kExactSmem, st>>>(e);
+    else
+      exact_kernel<float><<<B, kExThreads, kExactSmem, st>>>(e);
+    CK(h, cudaGetLastError());
+    h->last_launches = 2;
+  }
+  return SAMPLER_OK;
+}
+
+int sampler_sample(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots_dev,
+                   const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step,
+                   int32_t append_to_history, int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                   int32_t* row_status_dev, void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  int rc = check_logits(h, logits, ld, B);
+  if (rc) return rc;
+  if (!tokens_dev || !logprobs_dev) return fail(h, SAMPLER_EINVAL, "tokens/logprobs output is NULL");
+  if (h->cfg.vocab_local != h->cfg.vocab_size)
+    return fail(h, SAMPLER_EINVAL, "sharded handle: use sampler_sample_local + sampler_merge");
+  CK(h, cudaSetDevice(h->cfg.device));
+  return do_sample(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append_to_history, tokens_dev,
+                   logprobs_dev, filtered_logprobs_dev, row_status_dev, (cudaStream_t)cuda_stream);
+}
+
+int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots_dev,
+                               const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step,
+                               int32_t* tokens_dev, float* logprobs_dev, float* q_dev, void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  int rc = check_logits(h, logits, ld, B);
+  if (rc) return rc;
+  if (!tokens_dev || !logprobs_dev || !q_dev) return fail(h, SAMPLER_EINVAL, "output is NULL");
+  if (h->cfg.vocab_local != h->cfg.vocab_size) return fail(h, SAMPLER_EINVAL, "sharded handle");
+  CK(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  rc = do_sample(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, 0, tokens_dev, logprobs_dev, nullptr,
+                 nullptr, st);
+  if (rc) return rc;
+  HistState hs{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  dim3 grid((unsigned)std::min(64, (h->cfg.vocab_local + 255) / 256), (unsigned)B);
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    debug_q_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(logits, ld, h->cfg.vocab_size, h->cfg.vocab_offset,
+                                                         h->cfg.vocab_local, slots_dev, params_dev, h->d_params,
+                                                         h->cfg.penalty_mode, hs, h->d_info, q_dev);
+  else
+    debug_q_kernel<float><<<grid, 256, 0, st>>>(logits, ld, h->cfg.vocab_size, h->cfg.vocab_offset,
+                                                 h->cfg.vocab_local, slots_dev, params_dev, h->d_params,
+                                                 h->cfg.penalty_mode, hs, h->d_info, q_dev);
+  CK(h, cudaGetLastError());
+  h->last_launches += 1;
+  return SAMPLER_OK;
+}
+
+int64_t sampler_record_bytes(const sampler* h, int32_t B) {
+  if (!h || B < 0) return -1;
+  return h->rec_stride * (int64_t)B;
+}
+
+int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32_t B, const int32_t* slots_dev,
+                         const sampling_params* params_dev, void* records_dev, void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  int rc = check_logits(h, logits_slice, ld, B);
+  if (rc) return rc;
+  if (!records_dev) return fail(h, SAMPLER_EINVAL, "records_dev is NULL");
+  if (((uintptr_t)records_dev) % 16) return fail(h, SAMPLER_EINVAL, "records_dev must be 16-byte aligned");
+  CK(h, cudaSetDevice(h->cfg.device));
+  const LaunchPlan lp = plan(h, B);
+  StreamArgs a = stream_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, lp);
+  a.mode = 1;
+  a.out_records = (uint8_t*)records_dev;
+  a.ro.info = h->d_info;
+  rc = launch_stream(h, a, lp.grid, (cudaStream_t)cuda_stream);
+  if (rc) return rc;
+  h->last_launches = 1;
+  return SAMPLER_OK;
+}
+
+int sampler_merge(sampler* h, const void* gathered, int32_t world, int32_t B, const int32_t* slots_dev,
+                  const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step, int32_t append,
+                  int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev, int32_t* row_status_dev,
+                  void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  if (!gathered || !tokens_dev || !logprobs_dev) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (world < 1 || world > 4096) return fail(h, SAMPLER_EINVAL, "bad world size");
+  if (B < 1 || B > h->cfg.max_batch) return fail(h, SAMPLER_EINVAL, "B out of range");
+  CK(h, cudaSetDevice(h->cfg.device));
+  HistState hs{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  RowOut ro{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
+  const int grid = (B + kWarpsPerCta - 1) / kWarpsPerCta;
+  merge_kernel<<<grid, kWarpsPerCta * 32, kWarpsPerCta * (kCapW * 8 + 1024), (cudaStream_t)cuda_stream>>>(
+      (const uint8_t*)gathered, h->rec_stride * B, h->rec_stride, world, B, slots_dev, params_dev, h->d_params,
+      seeds_dev, step, h->cfg.vocab_size, h->cfg.max_top_k, append, hs, ro);
+  CK(h, cudaGetLastError());
+  h->last_launches = 1;
+  return SAMPLER_OK;
+}
+
+}  // extern "C"
