@@ -220,8 +220,10 @@ __device__ __forceinline__ RowCfg decode_row(const sampling_params& p, int V, in
   else
     r.keff = kcand;
   r.c_d = kLog2e / (double)r.tau;
-  r.c_hi = (float)r.c_d;
-  r.c_lo = (float)(r.c_d - (double)r.c_hi);
+  // two-term log2(e)/tau with c_lo > 0 (c_hi rounded down) so that -inf * c_lo never makes
+  // +inf and (-inf)*c_hi + (-inf)*c_lo stays -inf for -inf logits / sentinels
+  r.c_hi = __double2float_rd(r.c_d);
+  r.c_lo = fmaxf((float)(r.c_d - (double)r.c_hi), 1e-30f);
   r.delta = (float)(8.0 / r.c_d);
   return r;
 }

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) stream_kernel(const Stre
     }
     // ---- penalties: sparse scatter from the slot's unique-token table
     const int gid0 = a.voff + (int)off;
-    const int gid1 = gid0 + len;
+    const int gid1 = gid0 + (int)min((int64_t)len, (int64_t)a.vloc - off);  // no padding ids
     while (pc < pend) {
       const int i = pc + lane;
       UniqEntry e;
@@ -359,15 +359,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) stream_kernel(const Stre
         }
       }
       if (__any_sync(kFull, want)) {
-        uint64_t cv[VEC];
-        int np = 0;
+        uint32_t msk = 0;
         if (want) {
-          const int id0 = gid0 + v * VEC;
 #pragma unroll
-          for (int i = 0; i < VEC; ++i)
-            if (z[i] >= wc.theta) cv[np++] = make_comp(z[i], id0 + i);
+          for (int i = 0; i < VEC; ++i) msk |= (z[i] >= wc.theta) ? (1u << i) : 0u;
         }
-        warp_push<VEC>(wc, cv, np, lane);
+        int total;
+        int pos = warp_push_slot(wc, __popc(msk), lane, &total);
+        const int id0 = gid0 + v * VEC;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          if (msk & (1u << i)) wc.buf[pos++] = make_comp(z[i], id0 + i);
+        warp_push_done(wc, total, lane);
       }
     }
     __syncwarp();

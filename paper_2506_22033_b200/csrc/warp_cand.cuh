@@ -120,6 +120,19 @@ __device__ __forceinline__ void warp_shrink(WarpCand& w, int lane) {
   w.dropped = true;
 }
 
+// Two-phase append: every lane calls warp_push_slot(np) to get its first slot, writes its np
+// composites to buf[slot..slot+np), then all lanes call warp_push_done(total).
+__device__ __forceinline__ int warp_push_slot(const WarpCand& w, int np, int lane, int* total) {
+  const int incl = warp_incl_scan_i(np, lane);
+  *total = __shfl_sync(kFull, incl, 31);
+  return w.cnt + incl - np;
+}
+__device__ __forceinline__ void warp_push_done(WarpCand& w, int total, int lane) {
+  w.cnt += total;
+  __syncwarp();
+  if (w.cnt > kShrinkAt) warp_shrink(w, lane);
+}
+
 // Append this lane's `np` composites (vals[0..np)) to the warp buffer.
 template <int NV>
 __device__ __forceinline__ void warp_push(WarpCand& w, const uint64_t (&vals)[NV], int np, int lane) {
