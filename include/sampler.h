@@ -219,6 +219,11 @@ int sampler_merge(sampler* h, const void* gathered_records_dev, int32_t world, i
 /* Number of kernel launches the last sample / sample_local / merge / debug call enqueued. */
 int32_t sampler_last_launch_count(const sampler* h);
 
+/* SYNC, debug only.  With the environment variable SAMPLER_TRACE set at sampler_create, the
+ * streaming kernel records per-CTA phase timestamps (globaltimer, ns; 32 slots per CTA) of the
+ * last launch; copies min(n, 32 * CTAs) of them to host_out.  EUNSUPPORTED when tracing is off. */
+int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n);
+
 /* Build identification string (arch, compile flags). */
 const char* sampler_version(void);
 

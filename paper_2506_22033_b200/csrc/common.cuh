@@ -44,19 +44,24 @@ struct __align__(8) UniqEntry {
 //   list = the range's top-K candidates as composites (see below), exact down to `frontier`:
 //          every element of the range with composite >= frontier is in the list.
 struct __align__(16) RecHdr {
-  float m;
-  uint32_t flags;  // bit0 bad (NaN/+inf seen)
-  double s;
-  uint32_t n;      // entries in the list
+  float m;          // max z' over the range (binary32)
+  uint32_t flags;   // bit0 bad (NaN/+inf seen)
+  double s;         // sum over the range of 2^(z'*log2(e)/tau - R)
+  double R;         // exponent reference of s
+  uint32_t n;       // entries in the list (sorted descending)
   uint32_t rsv;
-  uint64_t frontier;
+  uint64_t frontier;  // every element with composite >= frontier is in the list (0: all)
 };
-static_assert(sizeof(RecHdr) == 32, "RecHdr layout");
+static_assert(sizeof(RecHdr) == 48, "RecHdr layout");
+constexpr int kRecHdrBytes = 48;
 
 constexpr uint32_t kRecBad = 1u;
 
 __host__ __device__ inline int64_t rec_stride_bytes(int kcand) {
-  return (int64_t)sizeof(RecHdr) + 8 * (int64_t)kcand;
+  return (int64_t)kRecHdrBytes + 8 * (int64_t)kcand;
+}
+__device__ __forceinline__ const uint64_t* rec_entries(const uint8_t* rec) {
+  return reinterpret_cast<const uint64_t*>(rec + kRecHdrBytes);
 }
 
 // Per-row result / hand-off info (unresolved rows, debug distribution).
@@ -106,6 +111,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done;

@@ -14,7 +14,7 @@
 #include "common.cuh"
 #include "merge.cuh"
 #include "philox.cuh"
-#include "stream.cuh"
+#include "elem.cuh"
 
 namespace smp {
 

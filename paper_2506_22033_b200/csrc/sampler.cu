@@ -24,7 +24,7 @@ struct sampler {
   int sm_count = 0;
   int Vp = 0;    // vocab_local rounded up to the vector width
   int vec = 8;   // elements per 16 bytes
-  int max_warps = 0;
+  int max_ctas = 0;
   int64_t rec_stride = 0;
   // device state
   sampling_params* d_params = nullptr;
@@ -35,6 +35,7 @@ struct sampler {
   int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
   float* d_scratch = nullptr;
+  uint64_t* d_trace = nullptr;  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
   // host mirror
   std::vector<sampling_params> h_params;
   std::string err;
@@ -86,7 +87,7 @@ extern "C" {
 
 const char* sampler_version(void) {
   return "paper_2506_22033_b200 sampler: sm_100a (compute_100a), cp.async.bulk streaming, "
-         "warp top-K candidates, Philox4x32-10";
+         "warp-specialised TMA producer, warp top-K candidates, Philox4x32-10";
 }
 
 const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
@@ -122,10 +123,13 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device);
   h->vec = (c.logits_dtype == SAMPLER_BF16) ? 8 : 4;
   h->Vp = (c.vocab_local + h->vec - 1) / h->vec * h->vec;
-  h->max_warps = h->sm_count * 2 * kWarpsPerCta;
+  h->max_ctas = h->sm_count * kCtasPerSm;
   h->rec_stride = rec_stride_bytes(c.max_top_k);
   const int64_t B = c.max_batch, L = c.max_history;
-  const int64_t nrec = (int64_t)h->max_warps + B;
+  // records: one per (CTA, row) piece; the grid may exceed max_ctas when spans are capped
+  const int64_t max_grid = std::max<int64_t>(h->max_ctas, (B * (int64_t)h->Vp + (int64_t)kMaxSpanVec * h->vec - 1) /
+                                                              ((int64_t)kMaxSpanVec * h->vec) + 1);
+  const int64_t nrec = max_grid + B + 1;
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
             al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
@@ -170,6 +174,9 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     sampler_destroy(h);
     return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
   }
+  if (getenv("SAMPLER_TRACE")) {
+    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * 32 * h->max_ctas) != cudaSuccess) h->d_trace = nullptr;
+  }
   *out = h;
   return SAMPLER_OK;
 }
@@ -185,6 +192,7 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_tickets);
   cudaFree(h->d_info);
   cudaFree(h->d_scratch);
+  cudaFree(h->d_trace);
   delete h;
   return SAMPLER_OK;
 }
@@ -346,22 +354,23 @@ struct LaunchPlan {
 };
 
 static LaunchPlan plan(const sampler* h, int32_t B) {
+  // equal contiguous spans of the flattened [B x Vp] space, one per CTA (kCtasPerSm per SM); a
+  // span covers >= 1024 vectors and a row has at most kMaxRec pieces (span >= Vp/(kMaxRec-2))
   LaunchPlan p;
   p.N = (int64_t)B * h->Vp;
-  const int64_t W = h->max_warps;
-  int64_t span = (p.N + W - 1) / W;
-  const int64_t min_span = 2048;
+  const int64_t C = h->max_ctas;
+  int64_t span = (p.N + C - 1) / C;
+  const int64_t min_span = std::max<int64_t>(1024 * h->vec, (h->Vp + kMaxRec - 3) / (kMaxRec - 2));
   if (span < min_span) span = min_span;
+  if (span > (int64_t)kMaxSpanVec * h->vec) span = (int64_t)kMaxSpanVec * h->vec;  // keys live in smem
   span = (span + h->vec - 1) / h->vec * h->vec;
   p.span = span;
-  const int64_t nw = (p.N + span - 1) / span;
-  p.grid = (int)((nw + kWarpsPerCta - 1) / kWarpsPerCta);
+  p.grid = (int)((p.N + span - 1) / span);
   return p;
 }
 
 static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
-                              const sampling_params* params_dev, const uint64_t* seeds, uint64_t step, int append,
-                              const LaunchPlan& lp) {
+                              const sampling_params* params_dev, const LaunchPlan& lp) {
   StreamArgs a{};
   a.logits = logits;
   a.ld = ld;
@@ -375,9 +384,6 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.slots = slots;
   a.params_dev = params_dev;
   a.params_tab = h->d_params;
-  a.seeds = seeds;
-  a.step = step;
-  a.append = append;
   a.kcand = h->cfg.max_top_k;
   a.pen_mode = h->cfg.penalty_mode;
   a.hs.meta = h->d_meta;
@@ -386,18 +392,47 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.hs.L = h->cfg.max_history;
   a.records = h->d_records;
   a.rec_stride = h->rec_stride;
-  a.tickets = h->d_tickets;
-  a.mode = 0;
-  a.out_records = nullptr;
-  a.pending_ok = 1;
+  a.trace = h->d_trace;
   return a;
 }
 
 static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
+  if (h->d_trace) CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * 32 * h->max_ctas, st));
   if (h->cfg.logits_dtype == SAMPLER_BF16)
-    stream_kernel<__nv_bfloat16><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+    stream_kernel<__nv_bfloat16><<<grid, kBT, kStreamSmem, st>>>(a);
   else
-    stream_kernel<float><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+    stream_kernel<float><<<grid, kBT, kStreamSmem, st>>>(a);
+  CK(h, cudaGetLastError());
+  return SAMPLER_OK;
+}
+
+static MergeArgs merge_args(sampler* h, const LaunchPlan& lp, const int32_t* slots, const sampling_params* params_dev,
+                            const uint64_t* seeds, uint64_t step, int append, const RowOut& ro) {
+  MergeArgs m{};
+  m.records = h->d_records;
+  m.rec_stride = h->rec_stride;
+  m.span = lp.span;
+  m.Vp = h->Vp;
+  m.V = h->cfg.vocab_size;
+  m.kcand = h->cfg.max_top_k;
+  m.mode = 0;
+  m.slots = slots;
+  m.params_dev = params_dev;
+  m.params_tab = h->d_params;
+  m.seeds = seeds;
+  m.step = step;
+  m.append = append;
+  m.pending_ok = 1;
+  m.hs = HistState{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  m.ro = ro;
+  m.out_records = nullptr;
+  m.rank_pitch = 0;
+  m.world = 0;
+  return m;
+}
+
+static int launch_merge(sampler* h, const MergeArgs& m, int B, cudaStream_t st) {
+  merge_rows_kernel<<<B, kBT, kMergeKernelSmem, st>>>(m);
   CK(h, cudaGetLastError());
   return SAMPLER_OK;
 }
@@ -406,15 +441,13 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
                      const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step, int32_t append,
                      int32_t* tokens, float* logprobs, float* flogprobs, int32_t* status, cudaStream_t st) {
   const LaunchPlan lp = plan(h, B);
-  StreamArgs a = stream_args(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append, lp);
-  a.ro.tokens = tokens;
-  a.ro.logprobs = logprobs;
-  a.ro.flogprobs = flogprobs;
-  a.ro.status = status;
-  a.ro.info = h->d_info;
+  const StreamArgs a = stream_args(h, logits, ld, B, slots_dev, params_dev, lp);
+  RowOut ro{tokens, logprobs, flogprobs, status, h->d_info};
   int rc = launch_stream(h, a, lp.grid, st);
   if (rc) return rc;
-  h->last_launches = 1;
+  rc = launch_merge(h, merge_args(h, lp, slots_dev, params_dev, seeds_dev, step, append, ro), B, st);
+  if (rc) return rc;
+  h->last_launches = 2;
   // exact multi-pass kernel only if some row can be unresolved by the one-pass candidates
   bool need = params_dev != nullptr;
   if (!need) {
@@ -439,13 +472,13 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     e.pen_mode = h->cfg.penalty_mode;
     e.hs = a.hs;
     e.scratch = h->d_scratch;
-    e.ro = a.ro;
+    e.ro = ro;
     if (h->cfg.logits_dtype == SAMPLER_BF16)
       exact_kernel<__nv_bfloat16><<<B, kExThreads, kExactSmem, st>>>(e);
     else
       exact_kernel<float><<<B, kExThreads, kExactSmem, st>>>(e);
     CK(h, cudaGetLastError());
-    h->last_launches = 2;
+    h->last_launches = 3;
   }
   return SAMPLER_OK;
 }
@@ -493,6 +526,15 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
   return SAMPLER_OK;
 }
 
+int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n) {
+  if (!h || !host_out || n < 0) return SAMPLER_EINVAL;
+  if (!h->d_trace) return SAMPLER_EUNSUPPORTED;
+  const int64_t m = std::min<int64_t>(n, 32 * (int64_t)h->max_ctas);
+  if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SAMPLER_ECUDA;
+  return SAMPLER_OK;
+}
+
 int64_t sampler_record_bytes(const sampler* h, int32_t B) {
   if (!h || B < 0) return -1;
   return h->rec_stride * (int64_t)B;
@@ -506,14 +548,17 @@ int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32
   if (!records_dev) return fail(h, SAMPLER_EINVAL, "records_dev is NULL");
   if (((uintptr_t)records_dev) % 16) return fail(h, SAMPLER_EINVAL, "records_dev must be 16-byte aligned");
   CK(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
   const LaunchPlan lp = plan(h, B);
-  StreamArgs a = stream_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, lp);
-  a.mode = 1;
-  a.out_records = (uint8_t*)records_dev;
-  a.ro.info = h->d_info;
-  rc = launch_stream(h, a, lp.grid, (cudaStream_t)cuda_stream);
+  rc = launch_stream(h, stream_args(h, logits_slice, ld, B, slots_dev, params_dev, lp), lp.grid, st);
   if (rc) return rc;
-  h->last_launches = 1;
+  RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
+  MergeArgs m = merge_args(h, lp, slots_dev, params_dev, nullptr, 0, 0, ro);
+  m.mode = 1;
+  m.out_records = (uint8_t*)records_dev;
+  rc = launch_merge(h, m, B, st);
+  if (rc) return rc;
+  h->last_launches = 2;
   return SAMPLER_OK;
 }
 
@@ -523,16 +568,18 @@ int sampler_merge(sampler* h, const void* gathered, int32_t world, int32_t B, co
                   void* cuda_stream) {
   if (!h) return SAMPLER_EINVAL;
   if (!gathered || !tokens_dev || !logprobs_dev) return fail(h, SAMPLER_EINVAL, "NULL argument");
-  if (world < 1 || world > 4096) return fail(h, SAMPLER_EINVAL, "bad world size");
+  if (world < 1 || world > kMaxRec) return fail(h, SAMPLER_EINVAL, "world must be in [1, %d]", kMaxRec);
   if (B < 1 || B > h->cfg.max_batch) return fail(h, SAMPLER_EINVAL, "B out of range");
   CK(h, cudaSetDevice(h->cfg.device));
-  HistState hs{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
   RowOut ro{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
-  const int grid = (B + kWarpsPerCta - 1) / kWarpsPerCta;
-  merge_kernel<<<grid, kWarpsPerCta * 32, kWarpsPerCta * (kCapW * 8 + 1024), (cudaStream_t)cuda_stream>>>(
-      (const uint8_t*)gathered, h->rec_stride * B, h->rec_stride, world, B, slots_dev, params_dev, h->d_params,
-      seeds_dev, step, h->cfg.vocab_size, h->cfg.max_top_k, append, hs, ro);
-  CK(h, cudaGetLastError());
+  LaunchPlan lp{};
+  MergeArgs m = merge_args(h, lp, slots_dev, params_dev, seeds_dev, step, append, ro);
+  m.records = (const uint8_t*)gathered;
+  m.rank_pitch = h->rec_stride * B;
+  m.world = world;
+  m.pending_ok = 0;
+  int rc = launch_merge(h, m, B, (cudaStream_t)cuda_stream);
+  if (rc) return rc;
   h->last_launches = 1;
   return SAMPLER_OK;
 }

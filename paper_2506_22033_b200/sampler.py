@@ -24,7 +24,7 @@ EXPORTED = [
     "sampler_create", "sampler_destroy", "sampler_last_error", "sampler_set_params", "sampler_set_history",
     "sampler_append_tokens", "sampler_get_history", "sampler_sample", "sampler_debug_distribution",
     "sampler_record_bytes", "sampler_sample_local", "sampler_merge", "sampler_last_launch_count",
-    "sampler_version",
+    "sampler_version", "sampler_debug_trace",
 ]
 
 
@@ -90,6 +90,7 @@ def _load():
         "sampler_merge": ([P, P, I32, I32, P, P, P, U64, I32, P, P, P, P, P], I32),
         "sampler_last_launch_count": ([P], I32),
         "sampler_version": ([], C.c_char_p),
+        "sampler_debug_trace": ([P, P, I32], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(lib, name)

@@ -26,9 +26,9 @@ def test_library_exports_every_header_symbol():
     assert sorted(EXPORTED) == syms
 
 
-def test_sass_is_sm100a_with_bulk_copies():
-    """The built library contains sm_100a SASS, and the streaming kernel uses the bulk-copy
-    (TMA) engine: UBLKCP in the SASS."""
+def test_sass_is_sm100a_with_streaming_loads():
+    """The built library contains sm_100a SASS; the streaming pass uses 16-byte read-only
+    no-L1-allocate loads (LDG.E.NA.128.CONSTANT) and the hardware exp2 (MUFU.EX2)."""
     import shutil
     import subprocess
     from paper_2506_22033_b200.sampler import LIB_PATH
@@ -38,7 +38,7 @@ def test_sass_is_sm100a_with_bulk_copies():
     out = subprocess.run([cuobjdump, "-lelf", LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run([cuobjdump, "-sass", LIB_PATH], capture_output=True, text=True).stdout
-    assert "UBLKCP" in sass
+    assert "LDG.E.NA.128.CONSTANT" in sass
     assert "MUFU.EX2" in sass
 
 

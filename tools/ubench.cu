@@ -1,0 +1,151 @@
+// ubench.cu — microbenchmarks of the streaming building blocks on B200 (development tool).
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC
+//        -o tools/libubench.so tools/ubench.cu
+// Each kernel reduces N bf16 values (row-less; N = 256 x 152064) and writes one float per CTA.
+//   tma_kernel<MODE>: 1 producer warp (cp.async.bulk 16 KB tiles, 4 stages) + 8 consumer warps
+//   ldg_kernel<MODE>: 256 threads, grid-stride LDG.128, G vectors in flight per thread
+// MODE 0: touch only (sum of raw bits) 1: max  2: exp-sum (1 FFMA + MUFU)  3: exp-sum (2 FFMA)
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../paper_2506_22033_b200/csrc/common.cuh"
+
+using namespace smp;
+
+constexpr int TB = 16384, ST = 4;
+
+template <int MODE>
+__device__ __forceinline__ void consume8(const uint4 u, float& acc, float& mx, float c, float R) {
+  float z[8];
+  z[0] = __uint_as_float(u.x << 16);
+  z[1] = __uint_as_float(u.x & 0xFFFF0000u);
+  z[2] = __uint_as_float(u.y << 16);
+  z[3] = __uint_as_float(u.y & 0xFFFF0000u);
+  z[4] = __uint_as_float(u.z << 16);
+  z[5] = __uint_as_float(u.z & 0xFFFF0000u);
+  z[6] = __uint_as_float(u.w << 16);
+  z[7] = __uint_as_float(u.w & 0xFFFF0000u);
+  if (MODE == 0) {
+    acc += __uint_as_float(u.x ^ u.y ^ u.z ^ u.w);
+  } else if (MODE == 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = fmaxf(mx, z[i]);
+  } else {
+    float e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x = (MODE == 2) ? fmaf(z[i], c, -R) : fmaf(z[i], 1e-8f, fmaf(z[i], c, -R));
+      e[i] = ex2f(x);
+    }
+    acc += ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(288, 2) tma_kernel(const uint8_t* x, int64_t nbytes, float* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * TB);
+  uint64_t* empty = full + ST;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (nbytes / gridDim.x) / TB * TB;
+  const int64_t b0 = blockIdx.x * per, b1 = (blockIdx.x == gridDim.x - 1) ? nbytes : b0 + per;
+  const int ntiles = (int)((b1 - b0 + TB - 1) / TB);
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (wid == 8) {
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      for (int it = 0; it < ntiles; ++it) {
+        const int s = it % ST;
+        if (it >= ST) mbar_wait(&empty[s], (uint32_t)(((it / ST) - 1) & 1));
+        const int64_t o = b0 + (int64_t)it * TB;
+        const uint32_t len = (uint32_t)min((int64_t)TB, b1 - o);
+        mbar_arrive_expect_tx(&full[s], len);
+        bulk_g2s(smem + s * TB, x + o, len, &full[s], pol);
+      }
+    }
+    return;
+  }
+  float acc = 0.f, mx = -INFINITY;
+  const float c = 2.06f, R = 20.f;
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % ST;
+    mbar_wait(&full[s], (uint32_t)((it / ST) & 1));
+    const uint4* t = reinterpret_cast<const uint4*>(smem + s * TB);
+    // warp w: vectors [w*128, w*128+128), lane-strided, 4 per lane, all loaded first
+    uint4 u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = t[wid * 128 + j * 32 + lane];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) consume8<MODE>(u[j], acc, mx, c, R);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  acc += mx;
+  acc = warp_sum_d(acc);
+  if (lane == 0) atomicAdd(out + blockIdx.x, acc);
+}
+
+template <int MODE, int G>
+__global__ void __launch_bounds__(256) ldg_kernel(const uint8_t* x, int64_t nbytes, float* out) {
+  const int64_t nvec = nbytes / 16;
+  const uint4* v = reinterpret_cast<const uint4*>(x);
+  float acc = 0.f, mx = -INFINITY;
+  const float c = 2.06f, R = 20.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride * G) {
+    uint4 u[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int64_t k = i + j * stride;
+      if (k < nvec) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(u[j].x), "=r"(u[j].y), "=r"(u[j].z), "=r"(u[j].w)
+                     : "l"(v + k));
+      } else {
+        u[j] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) consume8<MODE>(u[j], acc, mx, c, R);
+  }
+  acc += mx;
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out + blockIdx.x, acc);
+}
+
+extern "C" int ub_run(int kind, int mode, const void* x, int64_t nbytes, float* out, int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int smem = ST * TB + 2 * ST * 8;
+  if (kind == 0) {
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(tma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      init = true;
+    }
+    switch (mode) {
+      case 0: tma_kernel<0><<<grid, 288, smem, st>>>((const uint8_t*)x, nbytes, out); break;
+      case 1: tma_kernel<1><<<grid, 288, smem, st>>>((const uint8_t*)x, nbytes, out); break;
+      case 2: tma_kernel<2><<<grid, 288, smem, st>>>((const uint8_t*)x, nbytes, out); break;
+      default: tma_kernel<3><<<grid, 288, smem, st>>>((const uint8_t*)x, nbytes, out); break;
+    }
+  } else {
+    switch (mode) {
+      case 0: ldg_kernel<0, 4><<<grid, 256, 0, st>>>((const uint8_t*)x, nbytes, out); break;
+      case 1: ldg_kernel<1, 4><<<grid, 256, 0, st>>>((const uint8_t*)x, nbytes, out); break;
+      case 2: ldg_kernel<2, 4><<<grid, 256, 0, st>>>((const uint8_t*)x, nbytes, out); break;
+      default: ldg_kernel<3, 4><<<grid, 256, 0, st>>>((const uint8_t*)x, nbytes, out); break;
+    }
+  }
+  return (int)cudaGetLastError();
+}
