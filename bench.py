@@ -35,8 +35,8 @@ CHUNK = 250
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--batch", type=int, default=None, help="override B (c5 latency sweep)")
@@ -241,16 +241,25 @@ def main():
     esize = 2 if wl.dtype == "bf16" else 4
     B, V = wl.B, wl.V
     total_steps = a.warmup + a.steps + 2 * CHUNK
-    L = max(len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)) + total_steps + a.e2e_steps + 64
+    # Every step appends its sampled token to the row's history (in-kernel).  To keep the workload
+    # at the config's history shape for any --steps, steps rotate over NSET independent slot sets
+    # (set = step mod NSET), so each history grows by at most GROW tokens over the run.
+    GROW = 256
+    nset = max(1, -(-(total_steps + a.e2e_steps + 8) // GROW))
+    L = max(len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)) + GROW + 64
     if vocab_mode:
         from paper_2506_22033_b200.distributed import vocab_shard_bounds
         lo, hi = vocab_shard_bounds(V, world, rank)
     else:
         lo, hi = 0, V
-    s = Sampler(V, B, max_history=L, max_top_k=128, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
-    s.set_params(list(range(B)), wl.params)
-    for b in range(B):
-        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    s = Sampler(V, B * nset, max_history=L, max_top_k=128, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
+    slot_sets = []
+    for k in range(nset):
+        sl = list(range(k * B, (k + 1) * B))
+        s.set_params(sl, wl.params)
+        for b in range(B):
+            s.set_history(k * B + b, wl.prompts[b], wl.outputs[b])
+        slot_sets.append(torch.tensor(sl, dtype=torch.int32, device=dev))
     uniq0 = [len(s.get_history(b)["uniq_ids"]) for b in range(B)]
     xs = [device_logits(w)[:, lo:hi] for w in wls]
     out = s._outs(B, None)
@@ -261,12 +270,13 @@ def main():
 
     def one(i):
         x = xs[i % NBUF]
+        sl = slot_sets[i % nset]
         if vocab_mode:
-            s.sample_local(x, rec)
+            s.sample_local(x, rec, slots=sl)
             dist.all_gather_into_tensor(gathered, rec)
-            s.merge(gathered, world, B, i, append=True, out=out)
+            s.merge(gathered, world, B, i, slots=sl, append=True, out=out)
         else:
-            s.sample(x, i, append=True, out=out)
+            s.sample(x, i, slots=sl, append=True, out=out)
 
     launches_per_step = None
     one(0)
@@ -385,7 +395,8 @@ def main():
                    "parallelism": (f"vocab{world}" if vocab_mode else (f"rows{world}" if world > 1 else "1gpu")),
                    "l2": f"{NBUF} rotating logits buffers ({NBUF * B * V * esize / 1e6:.0f} MB > L2 126 MB)",
                    "history": f"{np.mean([len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)]):.0f} tokens/row "
-                              f"+1 per step (appended in-kernel)",
+                              f"+1 per step (appended in-kernel; {nset} rotating slot sets, each history grows "
+                              f"by <= {GROW})",
                    "graph": use_graph},
         "gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

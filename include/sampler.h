@@ -224,6 +224,15 @@ int32_t sampler_last_launch_count(const sampler* h);
  * last launch; copies min(n, 32 * CTAs) of them to host_out.  EUNSUPPORTED when tracing is off. */
 int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n);
 
+/* Per-kernel timing (measurement support).  sampler_set_timing(h, 1) makes every subsequent
+ * sample / sample_local / merge call record CUDA events on its stream around each kernel it
+ * launches (do not enable while capturing a CUDA graph).  sampler_kernel_times (SYNC: waits for
+ * the last call's final event) writes the last call's per-kernel durations in milliseconds, in
+ * launch order, to ms_out[0..min(n, count)) and the kernel count to *count.  EINVAL when timing
+ * is off or nothing was timed yet. */
+int sampler_set_timing(sampler* h, int32_t enable);
+int sampler_kernel_times(sampler* h, float* ms_out, int32_t n, int32_t* count);
+
 /* Build identification string (arch, compile flags). */
 const char* sampler_version(void);
 

@@ -108,9 +108,17 @@ struct LaneAcc {
   }
 };
 
+// x * 2^d for an integer-valued d <= 0 (exact unless the result is subnormal)
+__device__ __forceinline__ double scale_pow2(double x, float d) {
+  if (!(d > -1022.0f)) return d > -2200.0f ? ldexp(x, (int)d) : 0.0;
+  return x * __hiloint2double(((int)d + 1023) << 20, 0);
+}
+
+// The exponent reference R is an integer (floor(vmax * c_hi)), so every rescale of a sum by
+// 2^(R_old - R_new) — here and in the partial reductions — is an exact power-of-two multiply.
 __device__ __forceinline__ void lane_rebase(LaneAcc& a, float vmax, const RowCfg& rc) {
-  const float Rn = vmax * rc.c_hi;
-  if (a.acc != 0.0) a.acc *= exp2((double)a.R - (double)Rn);
+  const float Rn = floorf(vmax * rc.c_hi);
+  if (a.acc != 0.0) a.acc = scale_pow2(a.acc, a.R - Rn);
   a.R = Rn;
   a.thr = (Rn + 8.0f) / rc.c_hi;
 }

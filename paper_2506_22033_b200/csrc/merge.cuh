@@ -88,86 +88,291 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
   __syncwarp();
 }
 
-// number of entries of the descending list L[0..n) strictly greater than c
-__device__ __forceinline__ int count_gt(const uint64_t* L, int n, uint64_t c) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (L[mid] > c) lo = mid + 1;
-    else hi = mid;
+// Final decision for one row by one warp (R6-R11): top-k -> top-p (renormalised over
+// the top-k survivors) -> min-p over the candidates top[0..n) (sorted by pi), exact down to the
+// frontier F; inverse-CDF draw over the kept set in ascending id order with the Philox uniform;
+// outputs + RowInfo.  Returns the sampled token when the row's status is OK, else -1.
+// Candidates live in registers (candidate i = lane + 32q); the id-order cumulative mass of each
+// kept candidate is accumulated by broadcasting every kept (id, w) once — no sort, no barrier.
+__device__ __noinline__ int warp_decide(const MergeSmem& ms, int n, float M, double S, uint64_t F, bool bad,
+                                        const RowCfg& rc, const sampling_params& p, uint64_t seed, uint64_t step,
+                                        int row, const RowOut& ro, bool pending_ok, uint64_t* tr,
+                                        bool pre = false, double logS_pre = 0.0, double u_pre = 0.0) {
+  constexpr int Q = SAMPLER_KCAND_MAX / 32;
+  constexpr int UNK = 0x7FFFFFFF;
+  const int lane = threadIdx.x & 31;
+#define DTR(k)                             \
+  do {                                     \
+    if (tr && lane == 0) tr[k] = gtimer(); \
+  } while (0)
+  DTR(8);
+  const double inv_tau = 1.0 / (double)rc.tau;
+  const uint64_t* top = ms.top;
+  uint64_t c[Q];
+  double w[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = lane + 32 * q;
+    c[q] = (i < n) ? top[i] : 0ull;
+    w[q] = (i < n && !rc.greedy) ? (pre ? ms.wv[i] : exp(((double)comp_val(c[q]) - (double)M) * inv_tau)) : 0.0;
   }
-  return lo;
+  DTR(9);
+  int status = SAMPLER_ROW_OK;
+  if (bad)
+    status = SAMPLER_ROW_NONFINITE;
+  else if (n == 0 || !(M > -INFINITY))
+    status = SAMPLER_ROW_ALL_NEG_INF;
+  int32_t tok = -1;
+  double lp = NAN, flp = NAN, W = 0.0;
+  uint64_t cutoff = 0;
+  if (status == SAMPLER_ROW_OK) {
+    int n_exact = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) n_exact += __popc(__ballot_sync(kFull, lane + 32 * q < n && c[q] >= F));
+    const bool complete = (F == 0);
+    int n3 = -1;
+    if (rc.greedy) {
+      n3 = (n_exact >= 1) ? 1 : -1;  // the top candidate must be certified (F)
+    } else {
+      int n1 = UNK;
+      if (rc.topk_on) {
+        if (rc.k <= n_exact) n1 = rc.k;
+        else if (complete) n1 = n;
+      } else if (complete) {
+        n1 = n;
+      }
+      int cand = n1;
+      bool ok = true;
+      if (rc.top_p < 1.0f) {
+        double W1 = 0.0;
+        bool w1k = false;
+        if (n1 != UNK) {
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+            if (lane + 32 * q < n1) a += w[q];
+          W1 = warp_sum_d(a);
+          w1k = true;
+        } else if (!rc.topk_on) {
+          W1 = S;
+          w1k = true;
+        }
+        if (!w1k) {
+          ok = false;
+        } else {
+          const double target = (double)rc.top_p * W1;
+          const int lim = (n1 != UNK && n1 < n_exact) ? n1 : n_exact;
+          int n2 = UNK;
+          double run = 0.0;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int i = lane + 32 * q;
+            const double cq = run + warp_incl_scan_d((i < lim) ? w[q] : 0.0, lane);
+            const unsigned hit = __ballot_sync(kFull, (i < lim) && (cq >= target));
+            if (hit && n2 == UNK) n2 = 32 * q + __ffs(hit);
+            run = __shfl_sync(kFull, cq, 31);
+          }
+          if (n2 == UNK && n1 != UNK && n1 <= n_exact) n2 = n1;  // rounding shortfall
+          if (n2 != UNK) cand = cand < n2 ? cand : n2;
+        }
+      }
+      DTR(10);
+      if (ok && rc.min_p > 0.0f) {
+        int nm = UNK;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const unsigned hit = __ballot_sync(kFull, (lane + 32 * q < n_exact) && (w[q] < (double)rc.min_p));
+          if (hit && nm == UNK) nm = 32 * q + __ffs(hit) - 1;
+        }
+        if (nm == UNK && complete) nm = n;
+        if (nm != UNK) cand = cand < nm ? cand : nm;
+      }
+      if (ok && cand != UNK && cand <= n_exact && cand >= 1) n3 = cand;
+    }
+    DTR(11);
+    if (n3 < 0) {
+      status = kRowPending;
+    } else {
+      cutoff = __shfl_sync(kFull, c[0], 0);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const uint64_t cc = __shfl_sync(kFull, c[q], (n3 - 1) & 31);
+        if (q == (n3 - 1) >> 5) cutoff = cc;
+      }
+      if (rc.greedy) {
+        const uint64_t c0 = __shfl_sync(kFull, c[0], 0);
+        tok = comp_id(c0);
+        W = 1.0;
+        lp = ((double)comp_val(c0) - (double)M) - (pre ? logS_pre : log(S));
+        flp = 0.0;
+      } else {
+        // kept set K3 = first n3 of pi; the draw walks it in ascending id order (R10): every
+        // kept candidate's id-rank (integer walk over the kept ids, smem broadcast), weights
+        // placed in id order, one prefix scan, first cumulative mass > u*W
+        int id[Q], rk[Q];
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const bool kept = lane + 32 * q < n3;
+          id[q] = kept ? comp_id(c[q]) : 0x7FFFFFFF;
+          rk[q] = 0;
+          if (kept) a += w[q];
+        }
+        W = warp_sum_d(a);
+        const double u = pre ? u_pre : philox_uniform(seed, p.request_id, step);
+        const double target = u * W;
+        DTR(12);
+#pragma unroll 4
+        for (int j = 0; j < n3; ++j) {
+          const int idj = comp_id(top[j]);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) rk[q] += (idj < id[q]) ? 1 : 0;
+        }
+        double* wid = reinterpret_cast<double*>(ms.byid);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (lane + 32 * q < n3) wid[rk[q]] = w[q];
+        __syncwarp();
+        int pick = -1;
+        double run = 0.0;
+        for (int base = 0; base < n3 && pick < 0; base += 32) {
+          const int i = base + lane;
+          const double cq = run + warp_incl_scan_d((i < n3) ? wid[i] : 0.0, lane);
+          const unsigned hit = __ballot_sync(kFull, (i < n3) && (cq > target));
+          if (hit) pick = base + __ffs(hit) - 1;
+          run = __shfl_sync(kFull, cq, 31);
+        }
+        if (pick < 0) pick = n3 - 1;  // u*W at the top of the mass: the last in id order
+        DTR(13);
+        double lpl = 0.0, flpl = 0.0;
+        int own = 0, tl = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (lane + 32 * q < n3 && rk[q] == pick) {
+            own = 1;
+            tl = id[q];
+            lpl = ((double)comp_val(c[q]) - (double)M) * inv_tau - (pre ? logS_pre : log(S));
+            flpl = log(w[q] / W);
+          }
+        const int src = __ffs(__ballot_sync(kFull, own)) - 1;
+        tok = __shfl_sync(kFull, tl, src);
+        lp = __shfl_sync(kFull, lpl, src);
+        flp = __shfl_sync(kFull, flpl, src);
+        DTR(14);
+      }
+    }
+  }
+  if (lane == 0) {
+    RowInfo ri;
+    ri.M = M;
+    ri.status = status;
+    ri.S = S;
+    ri.W = W;
+    ri.cutoff = cutoff;
+    ri.token = tok;
+    ri.greedy = rc.greedy;
+    ro.info[row] = ri;
+    const bool pend = status == kRowPending;
+    if (!pend || !pending_ok) {
+      const int st = pend ? SAMPLER_ROW_UNRESOLVED : status;
+      ro.tokens[row] = (st == SAMPLER_ROW_OK) ? tok : -1;
+      ro.logprobs[row] = (st == SAMPLER_ROW_OK) ? (float)lp : NAN;
+      if (ro.flogprobs) ro.flogprobs[row] = (st == SAMPLER_ROW_OK) ? (float)flp : NAN;
+      if (ro.status) ro.status[row] = st;
+    }
+  }
+  DTR(15);
+#undef DTR
+  return (status == SAMPLER_ROW_OK) ? tok : -1;
 }
 
 // Merge `nrec` records (pitch `pitch` bytes, first at `recs`) of one row; all kBT threads.
 // mode 0: final decision + outputs (+ append).  mode 1: write one merged record to out_rec.
+// Latency-shaped: one global round trip brings every header and the first keff entries of every
+// record (fixed stride keff in the pool) together with the slot's history state; the rank merge
+// runs the per-list searches side by side; one barrier later warp 0 decides.
 __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch, int nrec, int row, int slot,
                                              const sampling_params& p, uint64_t seed, uint64_t step, int V,
                                              int kcand, int mode, uint8_t* out_rec, const RowOut& ro, int append,
-                                             const HistState& hs, bool pending_ok, const MergeSmem& ms) {
+                                             const HistState& hs, bool pending_ok, const MergeSmem& ms,
+                                             uint64_t* tr) {
+#define MTR(k)                              \
+  do {                                      \
+    if (tr && threadIdx.x == 0) tr[k] = gtimer(); \
+  } while (0)
+  MTR(1);
   const RowCfg rc = decode_row(p, V, kcand);
   const int tid = threadIdx.x, lane = tid & 31;
   const int keff = rc.keff;
-  // ---- headers
+  const bool do_app = append && mode == 0;
+  // ---- one round trip: headers, entries, history meta
+  const int nslot = nrec * keff;  // <= kMaxRec * SAMPLER_KCAND_MAX == kPool
+  for (int i = tid; i < nslot; i += kBT) {
+    const int rr = i / keff;
+    ms.pool[i] = rec_entries(recs + (int64_t)rr * pitch)[i - rr * keff];
+  }
   if (tid < nrec) ms.hdr[tid] = *reinterpret_cast<const RecHdr*>(recs + (int64_t)tid * pitch);
+  SlotMeta smeta = {0, 0, 0, 0};
+  if (do_app) smeta = hs.meta[slot];
   cbar();
-  if (tid == 0) {
-    int o = 0;
-    for (int i = 0; i < nrec; ++i) {
-      ms.off[i] = o;
-      const int n = (int)ms.hdr[i].n < keff ? (int)ms.hdr[i].n : keff;
-      o += n;
-    }
-    ms.off[nrec] = o;
+  MTR(2);
+  // ---- the slot's unique-token table into registers (used by the append after the decision)
+  constexpr int kUR = 4;
+  const int nu = smeta.n_uniq;
+  const bool reg_app = do_app && nu <= kBT * kUR;
+  UniqEntry ue[kUR];
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    ue[q].id = 0x7FFFFFFF;
+    ue[q].meta = 0;
+    if (reg_app && i < nu) ue[q] = hs.uniq[(int64_t)slot * hs.L + i];
   }
-  cbar();
-  const int U = ms.off[nrec];
-  // ---- load the (sorted) lists into the pool
-  for (int i = 0; i < nrec; ++i) {
-    const uint64_t* e = rec_entries(recs + (int64_t)i * pitch);
-    const int o = ms.off[i], n = ms.off[i + 1] - o;
-    for (int j = tid; j < n; j += kBT) ms.pool[o + j] = e[j];
-  }
-  cbar();
-  // ---- rank-merge: element at position q of list i has rank q + sum_{j != i} count_gt(list j)
-  for (int i = 0; i < nrec; ++i) {
-    const int o = ms.off[i], n = ms.off[i + 1] - o;
-    for (int q = tid; q < n; q += kBT) {
-      const uint64_t c = ms.pool[o + q];
-      int rank = q;
-      for (int j = 0; j < nrec && rank < keff; ++j)
-        if (j != i) rank += count_gt(ms.pool + ms.off[j], ms.off[j + 1] - ms.off[j], c);
-      if (rank < keff) ms.top[rank] = c;
+  // ---- rank merge: element q of list r has rank q + sum_{o != r} |{entries of o > c}|
+  int U = 0;
+  for (int o = 0; o < nrec; ++o) U += min((int)ms.hdr[o].n, keff);
+  for (int i = tid; i < nslot; i += kBT) {
+    const int rr = i / keff, q = i - rr * keff;
+    if (q >= min((int)ms.hdr[rr].n, keff)) continue;
+    const uint64_t c = ms.pool[i];
+    int rank = q;
+    for (int o = 0; o < nrec; ++o) {
+      if (o == rr) continue;
+      const int no = min((int)ms.hdr[o].n, keff);
+      const uint64_t* L = ms.pool + o * keff;
+      int pos = 0;
+#pragma unroll
+      for (int st = 128; st; st >>= 1)
+        if (pos + st <= no && L[pos + st - 1] > c) pos += st;
+      rank += pos;
     }
+    if (rank < keff) ms.top[rank] = c;
   }
-  cbar();
-  const int n = U < keff ? U : keff;
-  // ---- M, S, frontier (fixed record order)
-  if (tid == 0) {
-    float M = -INFINITY;
-    uint32_t fl = 0;
-    uint64_t F = 0;
-    for (int i = 0; i < nrec; ++i) {
-      M = fmaxf(M, ms.hdr[i].m);
-      fl |= ms.hdr[i].flags;
-      F = ms.hdr[i].frontier > F ? ms.hdr[i].frontier : F;
-    }
+  // ---- M, S, frontier, flags (warp 0, fixed record order within the warp tree)
+  if (tid < 32) {
+    const bool has = lane < nrec;
+    const RecHdr hd = has ? ms.hdr[lane] : RecHdr{};
+    const float M = warp_max(has ? hd.m : -INFINITY);
     const double RM = (double)M * rc.c_d;
-    double S = 0.0;
-    for (int i = 0; i < nrec; ++i)
-      if (ms.hdr[i].s != 0.0) S += ms.hdr[i].s * exp2(ms.hdr[i].R - RM);
-    if (U > keff && n > 0) F = ms.top[n - 1] > F ? ms.top[n - 1] : F;
-    ms.bs.f[0] = M;
-    ms.bs.d[0] = S;
-    ms.bs.u[0] = F;
-    ms.bs.i[0] = (int)fl;
+    const double term = (has && hd.s != 0.0) ? hd.s * exp2(hd.R - RM) : 0.0;
+    const double S = warp_sum_d(term);
+    const uint64_t F = warp_max_u64(has ? hd.frontier : 0ull);
+    const unsigned fl = __reduce_or_sync(kFull, has ? hd.flags : 0u);
+    if (lane == 0) {
+      ms.bs.f[0] = M;
+      ms.bs.d[0] = S;
+      ms.bs.u[0] = F;
+      ms.bs.i[0] = (int)fl;
+    }
   }
   cbar();
+  MTR(3);
+  const int n = U < keff ? U : keff;
   const float M = ms.bs.f[0];
   const double S = ms.bs.d[0];
-  const uint64_t F = ms.bs.u[0];
+  uint64_t F = ms.bs.u[0];
+  if (U > keff && n > 0) F = ms.top[n - 1] > F ? ms.top[n - 1] : F;
   const bool bad = (ms.bs.i[0] & kRecBad) != 0;
-  cbar();
 
   if (mode == 1) {  // ---- local merge: emit one record
     uint64_t* oe = reinterpret_cast<uint64_t*>(out_rec + kRecHdrBytes);
@@ -187,160 +392,103 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
     return;
   }
 
-  // ---- final decision (warp 0; the other warps compute weights first)
-  const double inv_tau = 1.0 / (double)rc.tau;
-  for (int i = tid; i < n; i += kBT) ms.wv[i] = exp(((double)comp_val(ms.top[i]) - (double)M) * inv_tau);
-  cbar();
+  // ---- final decision (warp 0)
   if (tid < 32) {
-    int status = SAMPLER_ROW_OK;
-    if (bad)
-      status = SAMPLER_ROW_NONFINITE;
-    else if (n == 0 || !(M > -INFINITY))
-      status = SAMPLER_ROW_ALL_NEG_INF;
-    int32_t tok = -1;
-    double lp = NAN, flp = NAN, W = 0.0;
-    uint64_t cutoff = 0;
-    if (status == SAMPLER_ROW_OK) {
-      int n_exact = 0;
-      for (int i = lane; i < n; i += 32) n_exact += (ms.top[i] >= F) ? 1 : 0;
-      n_exact = warp_sum_i(n_exact);
-      const bool complete = (F == 0);
-      int n3 = -1;
-      if (rc.greedy) {
-        n3 = 1;
-      } else {
-        const int UNK = 0x7FFFFFFF;
-        int n1 = UNK;
-        if (rc.topk_on) {
-          if (rc.k <= n_exact) n1 = rc.k;
-          else if (complete) n1 = n;
-        } else if (complete) {
-          n1 = n;
-        }
-        int cand = n1;
-        bool ok = true;
-        if (rc.top_p < 1.0f) {
-          double W1 = 0.0;
-          bool w1k = false;
-          if (n1 != UNK) {
-            double a = 0.0;
-            for (int i = lane; i < n1; i += 32) a += ms.wv[i];
-            W1 = warp_sum_d(a);
-            w1k = true;
-          } else if (!rc.topk_on) {
-            W1 = S;
-            w1k = true;
-          }
-          if (!w1k) {
-            ok = false;
-          } else {
-            const double target = (double)rc.top_p * W1;
-            const int lim = (n1 != UNK && n1 < n_exact) ? n1 : n_exact;
-            int n2 = UNK;
-            double run = 0.0;
-            for (int base = 0; base < lim && n2 == UNK; base += 32) {
-              const int i = base + lane;
-              const double x = (i < lim) ? ms.wv[i] : 0.0;
-              const double c = run + warp_incl_scan_d(x, lane);
-              const unsigned hit = __ballot_sync(kFull, (i < lim) && (c >= target));
-              if (hit) n2 = base + __ffs(hit);
-              run = __shfl_sync(kFull, c, 31);
-            }
-            if (n2 == UNK && n1 != UNK && n1 <= n_exact) n2 = n1;  // rounding shortfall
-            if (n2 != UNK) cand = cand < n2 ? cand : n2;
-          }
-        }
-        if (ok && rc.min_p > 0.0f) {
-          int nm = UNK;
-          for (int base = 0; base < n_exact && nm == UNK; base += 32) {
-            const int i = base + lane;
-            const unsigned hit = __ballot_sync(kFull, (i < n_exact) && (ms.wv[i] < (double)rc.min_p));
-            if (hit) nm = base + __ffs(hit) - 1;
-          }
-          if (nm == UNK && complete) nm = n;
-          if (nm != UNK) cand = cand < nm ? cand : nm;
-        }
-        if (ok && cand != UNK && cand <= n_exact && cand >= 1) n3 = cand;
-      }
-      if (n3 < 0) {
-        status = kRowPending;
-      } else {
-        cutoff = ms.top[n3 - 1];
-        if (rc.greedy) {
-          tok = comp_id(ms.top[0]);
-          W = 1.0;
-          lp = ((double)comp_val(ms.top[0]) - (double)M) - log(S);
-          flp = 0.0;
-        } else {
-          // kept set K3 = first n3 of pi, walked in ascending id order (R10); rank by id
-          for (int i = lane; i < n3; i += 32)
-            ms.byid[i] = ((uint64_t)(uint32_t)comp_id(ms.top[i]) << 32) | (uint32_t)i;
-          __syncwarp();
-          int N = 1;
-          while (N < n3) N <<= 1;
-          for (int i = n3 + lane; i < N; i += 32) ms.byid[i] = ~0ull;
-          __syncwarp();
-          for (int k = 2; k <= N; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-              for (int i = lane; i < N; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                  const uint64_t a = ms.byid[i], b = ms.byid[ixj];
-                  const bool asc = (i & k) == 0;
-                  if (asc ? (a > b) : (a < b)) {
-                    ms.byid[i] = b;
-                    ms.byid[ixj] = a;
-                  }
-                }
-              }
-              __syncwarp();
-            }
-          double a = 0.0;
-          for (int i = lane; i < n3; i += 32) a += ms.wv[i];
-          W = warp_sum_d(a);
-          const double u = philox_uniform(seed, p.request_id, step);
-          const double target = u * W;
-          int pick = -1;
-          double run = 0.0;
-          for (int base = 0; base < n3 && pick < 0; base += 32) {
-            const int i = base + lane;
-            const double x = (i < n3) ? ms.wv[(uint32_t)ms.byid[i]] : 0.0;
-            const double c = run + warp_incl_scan_d(x, lane);
-            const unsigned hit = __ballot_sync(kFull, (i < n3) && (c > target));
-            if (hit) pick = base + __ffs(hit) - 1;
-            run = __shfl_sync(kFull, c, 31);
-          }
-          if (pick < 0) pick = n3 - 1;
-          const int rank = (int)(uint32_t)ms.byid[pick];
-          tok = comp_id(ms.top[rank]);
-          lp = ((double)comp_val(ms.top[rank]) - (double)M) * inv_tau - log(S);
-          flp = log(ms.wv[rank] / W);
-        }
-      }
-    }
-    if (lane == 0) {
-      RowInfo ri;
-      ri.M = M;
-      ri.status = status;
-      ri.S = S;
-      ri.W = W;
-      ri.cutoff = cutoff;
-      ri.token = tok;
-      ri.greedy = rc.greedy;
-      ro.info[row] = ri;
-      const bool pend = status == kRowPending;
-      if (!pend || !pending_ok) {
-        const int st = pend ? SAMPLER_ROW_UNRESOLVED : status;
-        ro.tokens[row] = (st == SAMPLER_ROW_OK) ? tok : -1;
-        ro.logprobs[row] = (st == SAMPLER_ROW_OK) ? (float)lp : NAN;
-        if (ro.flogprobs) ro.flogprobs[row] = (st == SAMPLER_ROW_OK) ? (float)flp : NAN;
-        if (ro.status) ro.status[row] = st;
-      }
-    }
-    __syncwarp();
-    if (append && status == SAMPLER_ROW_OK) warp_append_token(hs, slot, tok, lane);
+    const int t = warp_decide(ms, n, M, S, F, bad, rc, p, seed, step, row, ro, pending_ok, tr);
+    if (lane == 0) ms.bs.i[1] = t;
   }
+  MTR(4);
   cbar();
+  // ---- history append (P:371 incremental update), whole block; the table is in registers
+  const int32_t tok = ms.bs.i[1];
+  if (!do_app || tok < 0) return;
+  if (!reg_app) {  // very long unique tables: one warp, chunked shift through global memory
+    if (tid < 32) warp_append_token(hs, slot, tok, lane);
+    return;
+  }
+  const int np = smeta.n_prompt, no = smeta.n_out;
+  if (np + no + 1 > hs.L) {
+    if (tid == 0) hs.meta[slot].flags |= 1;
+    return;
+  }
+  int cl = 0;
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    if (i < nu) cl += (ue[q].id < tok ? 1 : 0) + (ue[q].id == tok ? (1 << 20) : 0);
+  }
+  const int cs = block_sum_i(cl, ms.bs);
+  const int less = cs & ((1 << 20) - 1);
+  const bool found = (cs >> 20) != 0;
+  UniqEntry* u = hs.uniq + (int64_t)slot * hs.L;
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    if (i < nu) {
+      if (found && i == less) u[i].meta = ue[q].meta + 2u;
+      if (!found && i >= less) u[i + 1] = ue[q];
+    }
+  }
+  if (tid == 0) {
+    if (!found) {
+      UniqEntry e;
+      e.id = tok;
+      e.meta = 2u;
+      u[less] = e;
+    }
+    hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
+    SlotMeta m2 = smeta;
+    m2.n_out = no + 1;
+    if (!found) m2.n_uniq = nu + 1;
+    hs.meta[slot] = m2;
+  }
+  MTR(5);
+#undef MTR
+}
+
+// Sharded phase 2: one CTA per row merges the row's per-rank candidate records (rank order,
+// P:375) into the final sample.
+struct MergeArgs {
+  const uint8_t* records;   // gathered: world blocks of B records
+  int64_t rec_stride;
+  int64_t rank_pitch;       // bytes between ranks' blocks
+  int world;
+  int V, kcand;
+  const int32_t* slots;
+  const sampling_params* params_dev;
+  const sampling_params* params_tab;
+  const uint64_t* seeds;
+  uint64_t step;
+  int append;
+  HistState hs;
+  RowOut ro;
+  uint64_t* trace;  // debug: per-row phase timestamps (32 per row), nullable
+};
+constexpr int kMergeKernelSmem = kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8 + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12 + 512;
+
+__global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const MergeArgs m) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int r = blockIdx.x;
+  MergeSmem ms;
+  ms.pool = reinterpret_cast<uint64_t*>(smem);
+  ms.top = reinterpret_cast<uint64_t*>(smem + kPool * 8);
+  ms.wv = reinterpret_cast<double*>(smem + kPool * 8 + SAMPLER_KCAND_MAX * 8);
+  ms.byid = reinterpret_cast<uint64_t*>(smem + kPool * 8 + 2 * SAMPLER_KCAND_MAX * 8);
+  uint8_t* rest = smem + kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8;
+  ms.hdr = reinterpret_cast<RecHdr*>(rest);
+  ms.off = reinterpret_cast<int*>(rest + kMaxRec * 48);
+  uint8_t* scr = rest + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12;
+  scr = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(scr) + 15) & ~(uintptr_t)15);
+  ms.bs.f = reinterpret_cast<float*>(scr);
+  ms.bs.d = reinterpret_cast<double*>(scr + 32);
+  ms.bs.u = reinterpret_cast<uint64_t*>(scr + 96);
+  ms.bs.i = reinterpret_cast<int*>(scr + 224);
+  uint64_t* tr = m.trace ? m.trace + 32 * (int64_t)r : nullptr;
+  const int slot = m.slots ? m.slots[r] : r;
+  const sampling_params prm = m.params_dev ? m.params_dev[r] : m.params_tab[slot];
+  const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
+  block_merge_row(m.records + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step, m.V,
+                  m.kcand, 0, nullptr, m.ro, m.append, m.hs, false, ms, tr);
 }
 
 }  // namespace smp

@@ -2,7 +2,10 @@
 //
 // Owns per-handle device state (params table, per-slot history + incremental unique-token
 // penalty table, workspace), validates every call on the host before any launch, and enqueues
-// the sm_100a kernels of stream.cuh / exact.cuh on the caller's stream.
+// the sm_100a kernels on the caller's stream: phase A (stream.cuh), phase B (select.cuh, launched
+// with programmatic dependent launch so its prologue overlaps phase A's tail), the exact
+// multi-pass kernel (exact.cuh) only when some row can stay unresolved, and the sharded merge
+// (merge.cuh).
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -15,6 +18,7 @@
 #include "common.cuh"
 #include "exact.cuh"
 #include "merge.cuh"
+#include "select.cuh"
 #include "stream.cuh"
 
 using namespace smp;
@@ -24,6 +28,7 @@ struct sampler {
   int sm_count = 0;
   int Vp = 0;    // vocab_local rounded up to the vector width
   int vec = 8;   // elements per 16 bytes
+  int64_t Vq = 0;  // padded row length in vectors (piece.cuh)
   int max_ctas = 0;
   int64_t rec_stride = 0;
   // device state
@@ -35,12 +40,24 @@ struct sampler {
   int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
   float* d_scratch = nullptr;
+  uint16_t* d_gkeys = nullptr;  // [max_batch][Vq/4] group keys (phase A -> phase B)
   uint64_t* d_trace = nullptr;  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
   // host mirror
   std::vector<sampling_params> h_params;
   std::string err;
   int32_t last_launches = 0;
+  // per-kernel timing (sampler_set_timing)
+  bool timing = false;
+  cudaEvent_t tev[4] = {};
+  int tev_n = 0;  // kernels timed by the last call
 };
+
+// event after the k-th kernel of a call (k = 0: before the first)
+static void tmark(sampler* h, int k, cudaStream_t st) {
+  if (!h->timing) return;
+  cudaEventRecord(h->tev[k], st);
+  h->tev_n = k;
+}
 
 static thread_local std::string g_create_err;
 
@@ -86,13 +103,32 @@ static bool row_may_pend(const sampling_params& p, int V, int kcand) {
 extern "C" {
 
 const char* sampler_version(void) {
-  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a), cp.async.bulk streaming, "
-         "warp-specialised TMA producer, warp top-K candidates, Philox4x32-10";
+  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a), 16-byte LDG streaming pass with "
+         "per-vector max keys and lane-max bound, per-row merge, exact multi-pass fallback, Philox4x32-10";
 }
 
 const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 int32_t sampler_last_launch_count(const sampler* h) { return h ? h->last_launches : 0; }
+
+int sampler_set_timing(sampler* h, int32_t enable) {
+  if (!h) return SAMPLER_EINVAL;
+  cudaSetDevice(h->cfg.device);
+  if (enable && !h->tev[0])
+    for (auto& e : h->tev) CK(h, cudaEventCreate(&e));
+  h->timing = enable != 0;
+  h->tev_n = 0;
+  return SAMPLER_OK;
+}
+
+int sampler_kernel_times(sampler* h, float* ms_out, int32_t n, int32_t* count) {
+  if (!h || !ms_out || !count) return SAMPLER_EINVAL;
+  if (!h->timing || h->tev_n < 1) return fail(h, SAMPLER_EINVAL, "timing off or nothing timed");
+  CK(h, cudaEventSynchronize(h->tev[h->tev_n]));
+  for (int k = 0; k < h->tev_n && k < n; ++k) CK(h, cudaEventElapsedTime(&ms_out[k], h->tev[k], h->tev[k + 1]));
+  *count = h->tev_n;
+  return SAMPLER_OK;
+}
 
 int sampler_create(const sampler_config* cfg, sampler** out) {
   if (!out) return fail(nullptr, SAMPLER_EINVAL, "out is NULL");
@@ -124,18 +160,19 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   h->vec = (c.logits_dtype == SAMPLER_BF16) ? 8 : 4;
   h->Vp = (c.vocab_local + h->vec - 1) / h->vec * h->vec;
   h->max_ctas = h->sm_count * kCtasPerSm;
-  h->rec_stride = rec_stride_bytes(c.max_top_k);
+  h->Vq = vq_of(c.vocab_local, h->vec);
+  h->rec_stride = (rec_stride_bytes(c.max_top_k) + 127) / 128 * 128;
   const int64_t B = c.max_batch, L = c.max_history;
-  // records: one per (CTA, row) piece; the grid may exceed max_ctas when spans are capped
-  const int64_t max_grid = std::max<int64_t>(h->max_ctas, (B * (int64_t)h->Vp + (int64_t)kMaxSpanVec * h->vec - 1) /
-                                                              ((int64_t)kMaxSpanVec * h->vec) + 1);
-  const int64_t nrec = max_grid + B + 1;
+  // records: candidate records (sharded exchange) and one warp record per (warp, row) sub-piece
+  const int64_t nrec = std::max<int64_t>(B + 1, ((int64_t)h->max_ctas * kWarpsPerCta + B + 1) * kWarpRecStride /
+                                                    h->rec_stride + 1);
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
             al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
             al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_records, h->rec_stride * nrec) &&
             al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
-            al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp);
+            al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
+            al((void**)&h->d_gkeys, sizeof(uint16_t) * B * (h->Vq / kG));
   if (!ok) {
     cudaGetLastError();
     sampler_destroy(h);
@@ -167,6 +204,10 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
           cudaSuccess ||
       cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kExactSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(select_rows_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSelectSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(select_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelectSmem) !=
+          cudaSuccess ||
       cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExactSmem) !=
           cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
@@ -175,7 +216,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
   }
   if (getenv("SAMPLER_TRACE")) {
-    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * 32 * h->max_ctas) != cudaSuccess) h->d_trace = nullptr;
+    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (64 * (int64_t)h->max_ctas + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;
   }
   *out = h;
   return SAMPLER_OK;
@@ -193,6 +234,9 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_info);
   cudaFree(h->d_scratch);
   cudaFree(h->d_trace);
+  cudaFree(h->d_gkeys);
+  for (auto& e : h->tev)
+    if (e) cudaEventDestroy(e);
   delete h;
   return SAMPLER_OK;
 }
@@ -354,18 +398,18 @@ struct LaunchPlan {
 };
 
 static LaunchPlan plan(const sampler* h, int32_t B) {
-  // equal contiguous spans of the flattened [B x Vp] space, one per CTA (kCtasPerSm per SM); a
-  // span covers >= 1024 vectors and a row has at most kMaxRec pieces (span >= Vp/(kMaxRec-2))
+  // equal STEP-aligned warp spans of the padded [B x Vq] vector space, kWarpsPerCta per CTA,
+  // kCtasPerSm CTAs per SM; a row has at most kMaxRecW sub-pieces (span >= Vq / (kMaxRecW - 2))
   LaunchPlan p;
-  p.N = (int64_t)B * h->Vp;
-  const int64_t C = h->max_ctas;
-  int64_t span = (p.N + C - 1) / C;
-  const int64_t min_span = std::max<int64_t>(1024 * h->vec, (h->Vp + kMaxRec - 3) / (kMaxRec - 2));
+  p.N = (int64_t)B * h->Vq;
+  const int64_t W = (int64_t)h->max_ctas * kWarpsPerCta;
+  auto up = [](int64_t x) { return (x + kStepVec - 1) / kStepVec * kStepVec; };
+  int64_t span = up((p.N + W - 1) / W);
+  const int64_t min_span = up((h->Vq + kMaxRecW - 3) / (kMaxRecW - 2));
   if (span < min_span) span = min_span;
-  if (span > (int64_t)kMaxSpanVec * h->vec) span = (int64_t)kMaxSpanVec * h->vec;  // keys live in smem
-  span = (span + h->vec - 1) / h->vec * h->vec;
   p.span = span;
-  p.grid = (int)((p.N + span - 1) / span);
+  const int64_t warps = (p.N + span - 1) / span;
+  p.grid = (int)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
   return p;
 }
 
@@ -378,7 +422,7 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.V = h->cfg.vocab_size;
   a.voff = h->cfg.vocab_offset;
   a.vloc = h->cfg.vocab_local;
-  a.Vp = h->Vp;
+  a.Vq = h->Vq;
   a.span = lp.span;
   a.N = lp.N;
   a.slots = slots;
@@ -391,43 +435,93 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.hs.tokens = h->d_hist;
   a.hs.L = h->cfg.max_history;
   a.records = h->d_records;
-  a.rec_stride = h->rec_stride;
+  a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
   return a;
 }
 
 static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
-  if (h->d_trace) CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * 32 * h->max_ctas, st));
+  if (h->d_trace)
+    CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * (64 * (int64_t)h->max_ctas + 32 * (int64_t)h->cfg.max_batch), st));
   if (h->cfg.logits_dtype == SAMPLER_BF16)
-    stream_kernel<__nv_bfloat16><<<grid, kBT, kStreamSmem, st>>>(a);
+    stream_kernel<__nv_bfloat16><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
   else
-    stream_kernel<float><<<grid, kBT, kStreamSmem, st>>>(a);
+    stream_kernel<float><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
   CK(h, cudaGetLastError());
   return SAMPLER_OK;
 }
 
-static MergeArgs merge_args(sampler* h, const LaunchPlan& lp, const int32_t* slots, const sampling_params* params_dev,
+static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
+                              const sampling_params* params_dev, const uint64_t* seeds, uint64_t step, int append,
+                              const RowOut& ro, const LaunchPlan& lp) {
+  SelectArgs s{};
+  s.logits = logits;
+  s.ld = ld;
+  s.B = B;
+  s.V = h->cfg.vocab_size;
+  s.voff = h->cfg.vocab_offset;
+  s.vloc = h->cfg.vocab_local;
+  s.Vq = h->Vq;
+  s.span = lp.span;
+  s.N = lp.N;
+  s.slots = slots;
+  s.params_dev = params_dev;
+  s.params_tab = h->d_params;
+  s.seeds = seeds;
+  s.step = step;
+  s.kcand = h->cfg.max_top_k;
+  s.pen_mode = h->cfg.penalty_mode;
+  s.mode = 0;
+  s.append = append;
+  s.pending_ok = 1;
+  s.hs = HistState{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  s.records = h->d_records;
+  s.gkeys = h->d_gkeys;
+  s.ro = ro;
+  s.out_records = nullptr;
+  s.out_stride = h->rec_stride;
+  s.trace = h->d_trace ? h->d_trace + 64 * (int64_t)h->max_ctas : nullptr;
+  return s;
+}
+
+// phase B with programmatic dependent launch: its CTAs may start (prologue) while phase A's last
+// CTAs run; griddepcontrol.wait in the kernel orders every read of phase A's outputs
+static int launch_select(sampler* h, const SelectArgs& s, int B, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)B);
+  cfg.blockDim = dim3(kBT);
+  cfg.dynamicSmemBytes = kSelectSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    CK(h, cudaLaunchKernelEx(&cfg, select_rows_kernel<__nv_bfloat16>, s));
+  else
+    CK(h, cudaLaunchKernelEx(&cfg, select_rows_kernel<float>, s));
+  return SAMPLER_OK;
+}
+
+static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_params* params_dev,
                             const uint64_t* seeds, uint64_t step, int append, const RowOut& ro) {
   MergeArgs m{};
-  m.records = h->d_records;
+  m.records = nullptr;
   m.rec_stride = h->rec_stride;
-  m.span = lp.span;
-  m.Vp = h->Vp;
+  m.rank_pitch = 0;
+  m.world = 0;
   m.V = h->cfg.vocab_size;
   m.kcand = h->cfg.max_top_k;
-  m.mode = 0;
   m.slots = slots;
   m.params_dev = params_dev;
   m.params_tab = h->d_params;
   m.seeds = seeds;
   m.step = step;
   m.append = append;
-  m.pending_ok = 1;
   m.hs = HistState{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
   m.ro = ro;
-  m.out_records = nullptr;
-  m.rank_pitch = 0;
-  m.world = 0;
+  m.trace = h->d_trace ? h->d_trace + 64 * (int64_t)h->max_ctas : nullptr;
   return m;
 }
 
@@ -443,10 +537,13 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
   const LaunchPlan lp = plan(h, B);
   const StreamArgs a = stream_args(h, logits, ld, B, slots_dev, params_dev, lp);
   RowOut ro{tokens, logprobs, flogprobs, status, h->d_info};
+  tmark(h, 0, st);
   int rc = launch_stream(h, a, lp.grid, st);
   if (rc) return rc;
-  rc = launch_merge(h, merge_args(h, lp, slots_dev, params_dev, seeds_dev, step, append, ro), B, st);
+  tmark(h, 1, st);
+  rc = launch_select(h, select_args(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append, ro, lp), B, st);
   if (rc) return rc;
+  tmark(h, 2, st);
   h->last_launches = 2;
   // exact multi-pass kernel only if some row can be unresolved by the one-pass candidates
   bool need = params_dev != nullptr;
@@ -478,6 +575,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     else
       exact_kernel<float><<<B, kExThreads, kExactSmem, st>>>(e);
     CK(h, cudaGetLastError());
+    tmark(h, 3, st);
     h->last_launches = 3;
   }
   return SAMPLER_OK;
@@ -529,7 +627,7 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
 int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n) {
   if (!h || !host_out || n < 0) return SAMPLER_EINVAL;
   if (!h->d_trace) return SAMPLER_EUNSUPPORTED;
-  const int64_t m = std::min<int64_t>(n, 32 * (int64_t)h->max_ctas);
+  const int64_t m = std::min<int64_t>(n, 64 * (int64_t)h->max_ctas + 32 * (int64_t)h->cfg.max_batch);
   if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
     return SAMPLER_ECUDA;
   return SAMPLER_OK;
@@ -550,14 +648,17 @@ int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32
   CK(h, cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const LaunchPlan lp = plan(h, B);
+  tmark(h, 0, st);
   rc = launch_stream(h, stream_args(h, logits_slice, ld, B, slots_dev, params_dev, lp), lp.grid, st);
   if (rc) return rc;
+  tmark(h, 1, st);
   RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
-  MergeArgs m = merge_args(h, lp, slots_dev, params_dev, nullptr, 0, 0, ro);
-  m.mode = 1;
-  m.out_records = (uint8_t*)records_dev;
-  rc = launch_merge(h, m, B, st);
+  SelectArgs s = select_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, ro, lp);
+  s.mode = 1;
+  s.out_records = (uint8_t*)records_dev;
+  rc = launch_select(h, s, B, st);
   if (rc) return rc;
+  tmark(h, 2, st);
   h->last_launches = 2;
   return SAMPLER_OK;
 }
@@ -572,14 +673,14 @@ int sampler_merge(sampler* h, const void* gathered, int32_t world, int32_t B, co
   if (B < 1 || B > h->cfg.max_batch) return fail(h, SAMPLER_EINVAL, "B out of range");
   CK(h, cudaSetDevice(h->cfg.device));
   RowOut ro{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
-  LaunchPlan lp{};
-  MergeArgs m = merge_args(h, lp, slots_dev, params_dev, seeds_dev, step, append, ro);
+  MergeArgs m = merge_args(h, slots_dev, params_dev, seeds_dev, step, append, ro);
   m.records = (const uint8_t*)gathered;
   m.rank_pitch = h->rec_stride * B;
   m.world = world;
-  m.pending_ok = 0;
+  tmark(h, 0, (cudaStream_t)cuda_stream);
   int rc = launch_merge(h, m, B, (cudaStream_t)cuda_stream);
   if (rc) return rc;
+  tmark(h, 1, (cudaStream_t)cuda_stream);
   h->last_launches = 1;
   return SAMPLER_OK;
 }

@@ -24,7 +24,7 @@ EXPORTED = [
     "sampler_create", "sampler_destroy", "sampler_last_error", "sampler_set_params", "sampler_set_history",
     "sampler_append_tokens", "sampler_get_history", "sampler_sample", "sampler_debug_distribution",
     "sampler_record_bytes", "sampler_sample_local", "sampler_merge", "sampler_last_launch_count",
-    "sampler_version", "sampler_debug_trace",
+    "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
 ]
 
 
@@ -91,6 +91,8 @@ def _load():
         "sampler_last_launch_count": ([P], I32),
         "sampler_version": ([], C.c_char_p),
         "sampler_debug_trace": ([P, P, I32], I32),
+        "sampler_set_timing": ([P, I32], I32),
+        "sampler_kernel_times": ([P, P, I32, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(lib, name)
@@ -197,6 +199,17 @@ class Sampler:
 
     def last_launch_count(self) -> int:
         return int(_lib.sampler_last_launch_count(self.h))
+
+    def set_timing(self, enable=True):
+        """Record CUDA events around each kernel of every following call (not under graph capture)."""
+        self._check(_lib.sampler_set_timing(self.h, 1 if enable else 0))
+
+    def kernel_times_ms(self):
+        """Per-kernel durations (ms, launch order) of the last call; waits for it."""
+        buf = (C.c_float * 8)()
+        n = C.c_int32(0)
+        self._check(_lib.sampler_kernel_times(self.h, buf, 8, C.byref(n)))
+        return [float(buf[i]) for i in range(n.value)]
 
     def record_bytes(self, B) -> int:
         return int(_lib.sampler_record_bytes(self.h, B))

@@ -29,6 +29,36 @@ def timeit(fn, xs, iters=50, warm=5):
     return e0.elapsed_time(e1) / iters * 1000.0  # us
 
 
+def ktimes(s, fn, xs, iters=30, warm=3):
+    """Per-kernel device times (us) via the library's own CUDA events on the launch stream."""
+    for i in range(warm):
+        fn(xs[i % len(xs)], i)
+    s.set_timing(True)
+    acc = None
+    for i in range(iters):
+        fn(xs[i % len(xs)], warm + i)
+        t = s.kernel_times_ms()
+        acc = t if acc is None else [a + b for a, b in zip(acc, t)]
+    s.set_timing(False)
+    return [round(a / iters * 1000.0, 2) for a in acc]
+
+
+def c3_bench(nbuf=5, append=True):
+    """The bench.py c3 workload (synthetic logits + histories + params), per-kernel times."""
+    from workloads.synth import make_workload
+    from tests._helpers import device_logits
+    wls = [make_workload("c3", seed_offset=i) for i in range(nbuf)]
+    wl = wls[0]
+    s = Sampler(wl.V, wl.B, max_history=2048, max_top_k=128, dtype=wl.dtype)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    xs = [device_logits(w) for w in wls]
+    out = s._outs(wl.B, None)
+    fn = lambda x, i: s.sample(x, i, append=append, out=out)
+    return {"c3_total_us": timeit(fn, xs, iters=30), "c3_kernels_us": ktimes(s, fn, xs)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--B", type=int, default=256)
@@ -60,9 +90,10 @@ def main():
                 s.set_history(b, rng.integers(0, V, 384).tolist(), rng.integers(0, V, 128).tolist())
         out = s._outs(B, None)
         res[name + "_us"] = timeit(lambda x, i: s.sample(x, i, out=out), xs)
-        res[name + "_launches"] = s.last_launch_count()
+        res[name + "_kernels_us"] = ktimes(s, lambda x, i: s.sample(x, i, out=out), xs)
     mb = B * V * 2 / 1e6
     res["MB"] = mb
+    res.update(c3_bench())
     print(json.dumps(res))
 
 
@@ -82,15 +113,21 @@ def trace(B=32, V=152064, variant="greedy"):
     for i in range(3):
         s.sample(x, i)
     torch.cuda.synchronize()
-    n = 32 * 1024
+    mc = torch.cuda.get_device_properties(0).multi_processor_count * 3
+    n = 64 * mc + 32 * B
     buf = (ctypes.c_uint64 * n)()
     assert lib().sampler_debug_trace(s.h, buf, n) == 0
-    t = np.array(buf[:], dtype=np.int64).reshape(-1, 32)
-    t = t[t[:, 0] > 0]
-    t0 = t[:, 0].min()
-    rel = np.where(t > 0, t - t0, -1)
-    print("CTAs", len(t))
-    for c in list(range(0, len(t), max(1, len(t) // 8))):
-        print(c, [int(v) for v in rel[c] if v >= 0][:20], "end", rel[c, 31])
-    ends = rel[:, 31]
-    print("end ns: min %d med %d max %d" % (ends.min(), np.median(ends), ends.max()))
+    allt = np.array(buf[:], dtype=np.int64)
+    wt = allt[:64 * mc].reshape(-1, 8)
+    mt = allt[64 * mc:64 * mc + 32 * B].reshape(-1, 32)
+    wt = wt[wt[:, 0] > 0]
+    t0 = wt[:, 0].min()
+    st_ = wt[:, 0] - t0
+    en = wt[:, 7] - t0
+    print("warps", len(wt), "start ns: med %d max %d" % (np.median(st_), st_.max()),
+          "end ns: min %d med %d p90 %d max %d" % (en.min(), np.median(en), np.percentile(en, 90), en.max()))
+    mrel = np.where(mt > 0, mt - t0, -1)
+    for c in list(range(0, B, max(1, B // 6))):
+        print("merge row", c, [int(v) for v in mrel[c] if v >= 0][:20])
+    st = mrel[:, 0]
+    print("merge start ns: min %d med %d max %d" % (st.min(), np.median(st), st.max()))
