@@ -157,6 +157,12 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// named barrier 2 among the first N threads of the CTA (warp-specialised kernels)
+template <int N>
+__device__ __forceinline__ void cbar_n() {
+  asm volatile("bar.sync 2, %0;" ::"n"(N) : "memory");
+}
+
 // ---- warp collectives ---------------------------------------------------------------
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll

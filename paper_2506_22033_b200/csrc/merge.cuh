@@ -28,12 +28,30 @@ struct RowOut {
   RowInfo* info;     // per-row hand-off / debug
 };
 
+// Per-slot history state.  offs[slot][b] = number of unique-table entries with
+// id < voff + min(kOffsBucket * b, vloc), b = 0..nb (nb = ceil(vloc / kOffsBucket)): the
+// table position of any STEP-aligned vocabulary boundary in O(1) (phase A's penalty ranges).
+constexpr int kOffsBucket = 512;
 struct HistState {
   SlotMeta* meta;
   UniqEntry* uniq;
   int32_t* tokens;
   int L;
+  int32_t* offs;  // [max_batch][nb + 1]
+  int nb;
+  int voff, vloc;
 };
+__host__ __device__ inline int offs_nb(int vloc) { return (vloc + kOffsBucket - 1) / kOffsBucket; }
+
+// a new unique id `tok` entered the table: every boundary above it moves up by one
+__device__ __forceinline__ void offs_bump(const HistState& hs, int slot, int32_t tok, int tid, int nthr) {
+  int b0;
+  if (tok < hs.voff) b0 = 0;
+  else if (tok - hs.voff < hs.vloc) b0 = (tok - hs.voff) / kOffsBucket + 1;
+  else return;
+  int32_t* o = hs.offs + (int64_t)slot * (hs.nb + 1);
+  for (int b = b0 + tid; b <= hs.nb; b += nthr) o[b] += 1;
+}
 
 struct MergeSmem {
   uint64_t* pool;   // [kPool]
@@ -79,6 +97,7 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
       e.meta = 2u;
       u[less] = e;
     }
+    offs_bump(hs, slot, tok, lane, 32);
   }
   if (lane == 0) {
     hs.tokens[(int64_t)slot * hs.L + np + no] = tok;

@@ -14,11 +14,11 @@
 //     CTA barrier anywhere in phase A); a warp span crossing a row boundary yields one
 //     "sub-piece" per row, and every sub-piece gets a warp record.
 //   * Phase A writes, per group, the order-preserving bf16 key of the group max (rounded down)
-//     to gkeys[row][group]; per sub-piece, a warp record with its max / exp-sum and its 32 lane
-//     maxima (each lane's max over the groups it streamed), sorted descending.
-//   * Phase B: T = K-th largest lane max of the row.  K distinct lanes have a max >= T, so K
-//     distinct elements are >= T: T is a lower bound of the row's K-th largest z', and every
-//     top-K element lies in a group whose key is >= key(T).  Only those groups are re-read.
+//     to gkeys[row][group]; per sub-piece, a warp record with its max / exp-sum.
+//   * Phase B: T = K-th largest key among the row's group keys and penalised elements.  K
+//     distinct elements are >= val(T): T is a lower bound of the row's K-th largest z', and every
+//     top-K element lies in a group whose key is >= T (or is penalised).  Only those groups are
+//     re-read.
 #pragma once
 #include "common.cuh"
 #include "elem.cuh"
@@ -30,9 +30,9 @@ constexpr int kStepVec = 32 * kG;           // vectors per warp step (= 4 groups
 constexpr int kLaneList = 32;               // lane-max list entries per warp record
 constexpr int kMaxRecW = 64;                // warp records per row (plan)
 
-// warp record: RecHdr | u32 lane-max keys [32] (descending; 0 = lane saw no finite element)
-constexpr int kWarpRecBytes = kRecHdrBytes + 4 * kLaneList;
-constexpr int kWarpRecStride = 192;
+// warp record: RecHdr {m, flags, s, R = m * log2(e)/tau}
+constexpr int kWarpRecBytes = kRecHdrBytes;
+constexpr int kWarpRecStride = 64;
 static_assert(kWarpRecBytes <= kWarpRecStride, "warp record layout");
 
 __host__ __device__ inline int64_t vq_of(int vloc, int vec) {  // padded row length in vectors
@@ -40,6 +40,8 @@ __host__ __device__ inline int64_t vq_of(int vloc, int vec) {  // padded row len
   return (nv + kStepVec - 1) / kStepVec * kStepVec;
 }
 __host__ __device__ inline int64_t groups_of(int64_t vq) { return vq / kG; }
+// per-row key block in gkeys: [Vq / kG group keys | Vq / kStepVec step keys | pad to 8]
+__host__ __device__ inline int64_t gk_stride(int64_t vq) { return (vq / kG + vq / kStepVec + 7) / 8 * 8; }
 
 __device__ __forceinline__ uint4 ldg_stream(const uint8_t* p) {
   uint4 u;
@@ -60,6 +62,11 @@ __device__ __forceinline__ uint32_t key16_down(float f) {
   return h ^ ((h >> 15) ? 0xFFFFu : 0x8000u);
 }
 constexpr uint32_t kKey16NegInf = 0x007Fu;  // key16_down(-inf)
+// the bf16 value of a 16-bit key (inverse of key16_down on bf16 values)
+__device__ __forceinline__ float key16_val(uint32_t k) {
+  const uint32_t h = k ^ ((k >> 15) ? 0x8000u : 0xFFFFu);
+  return __uint_as_float(h << 16);
+}
 
 template <typename T>
 struct Dec;

@@ -40,8 +40,11 @@ struct sampler {
   int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
   float* d_scratch = nullptr;
+  int32_t* d_offs = nullptr;    // [max_batch][nb + 1] unique-table bucket offsets (HistState)
+  PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
   uint16_t* d_gkeys = nullptr;  // [max_batch][Vq/4] group keys (phase A -> phase B)
-  uint64_t* d_trace = nullptr;  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
+  uint64_t* d_trace = nullptr;
+  int dbg = 0;                  // SAMPLER_DBG development switches (stream.cuh)  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
   // host mirror
   std::vector<sampling_params> h_params;
   std::string err;
@@ -57,6 +60,23 @@ static void tmark(sampler* h, int k, cudaStream_t st) {
   if (!h->timing) return;
   cudaEventRecord(h->tev[k], st);
   h->tev_n = k;
+}
+
+static HistState hist_state(const sampler* h) {
+  HistState s;
+  s.meta = h->d_meta;
+  s.uniq = h->d_uniq;
+  s.tokens = h->d_hist;
+  s.L = h->cfg.max_history;
+  s.offs = h->d_offs;
+  s.nb = offs_nb(h->cfg.vocab_local);
+  s.voff = h->cfg.vocab_offset;
+  s.vloc = h->cfg.vocab_local;
+  return s;
+}
+
+static int64_t trace_a_len(const sampler* h) {  // phase-A trace entries (64 per CTA, worst-case grid)
+  return 64 * ((int64_t)h->cfg.max_batch * (h->Vq / kStepVec) / kTileSteps + 1);
 }
 
 static thread_local std::string g_create_err;
@@ -159,20 +179,21 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device);
   h->vec = (c.logits_dtype == SAMPLER_BF16) ? 8 : 4;
   h->Vp = (c.vocab_local + h->vec - 1) / h->vec * h->vec;
-  h->max_ctas = h->sm_count * kCtasPerSm;
+  h->max_ctas = h->sm_count;
   h->Vq = vq_of(c.vocab_local, h->vec);
   h->rec_stride = (rec_stride_bytes(c.max_top_k) + 127) / 128 * 128;
   const int64_t B = c.max_batch, L = c.max_history;
   // records: candidate records (sharded exchange) and one warp record per (warp, row) sub-piece
-  const int64_t nrec = std::max<int64_t>(B + 1, ((int64_t)h->max_ctas * kWarpsPerCta + B + 1) * kWarpRecStride /
-                                                    h->rec_stride + 1);
+  const int64_t nrec = B + 1;
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
             al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
             al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_records, h->rec_stride * nrec) &&
             al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
             al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
-            al((void**)&h->d_gkeys, sizeof(uint16_t) * B * (h->Vq / kG));
+            al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
+            al((void**)&h->d_offs, sizeof(int32_t) * B * (offs_nb(c.vocab_local) + 1)) &&
+            al((void**)&h->d_parts, sizeof(PartRec) * B * kCW * ((h->Vq / kStepVec + kTileSteps - 1) / kTileSteps + 1));
   if (!ok) {
     cudaGetLastError();
     sampler_destroy(h);
@@ -196,6 +217,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   if (cudaMemcpy(h->d_params, h->h_params.data(), sizeof(sampling_params) * B, cudaMemcpyHostToDevice) !=
           cudaSuccess ||
       cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
+      cudaMemset(h->d_offs, 0, sizeof(int32_t) * B * (offs_nb(c.vocab_local) + 1)) != cudaSuccess ||
       cudaMemset(h->d_tickets, 0, sizeof(int32_t) * B) != cudaSuccess ||
       cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
       cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -215,8 +237,9 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     sampler_destroy(h);
     return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
   }
+  if (getenv("SAMPLER_DBG")) h->dbg = atoi(getenv("SAMPLER_DBG"));
   if (getenv("SAMPLER_TRACE")) {
-    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (64 * (int64_t)h->max_ctas + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;
+    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;
   }
   *out = h;
   return SAMPLER_OK;
@@ -235,6 +258,8 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_scratch);
   cudaFree(h->d_trace);
   cudaFree(h->d_gkeys);
+  cudaFree(h->d_offs);
+  cudaFree(h->d_parts);
   for (auto& e : h->tev)
     if (e) cudaEventDestroy(e);
   delete h;
@@ -283,6 +308,17 @@ static int upload_slot(sampler* h, int slot, const std::vector<int32_t>& prompt,
     CK(h, cudaMemcpy(h->d_uniq + (int64_t)slot * L, u.data(), sizeof(UniqEntry) * u.size(), cudaMemcpyHostToDevice));
   if (!toks.empty())
     CK(h, cudaMemcpy(h->d_hist + (int64_t)slot * L, toks.data(), sizeof(int32_t) * toks.size(), cudaMemcpyHostToDevice));
+  // bucket offsets of the sorted unique table (HistState::offs)
+  const int nb = offs_nb(h->cfg.vocab_local);
+  std::vector<int32_t> offs(nb + 1);
+  size_t j = 0;
+  for (int b = 0; b <= nb; ++b) {
+    const int64_t bound = (int64_t)h->cfg.vocab_offset + std::min<int64_t>((int64_t)kOffsBucket * b, h->cfg.vocab_local);
+    while (j < u.size() && u[j].id < bound) ++j;
+    offs[b] = (int32_t)j;
+  }
+  CK(h, cudaMemcpy(h->d_offs + (int64_t)slot * (nb + 1), offs.data(), sizeof(int32_t) * (nb + 1),
+                   cudaMemcpyHostToDevice));
   CK(h, cudaMemcpy(h->d_meta + slot, &sm, sizeof(SlotMeta), cudaMemcpyHostToDevice));
   return SAMPLER_OK;
 }
@@ -392,24 +428,25 @@ static int check_logits(sampler* h, const void* logits, int64_t ld, int32_t B) {
 }
 
 struct LaunchPlan {
-  int64_t span;
-  int64_t N;
+  int spr;         // steps (2 KB of one row) per row
+  int span;        // steps per CTA
+  int rpr;         // CTA record blocks per row
+  int64_t nsteps;  // B * spr
   int grid;
 };
 
+// Phase A geometry (stream.cuh): equal contiguous spans of the padded step space, one persistent
+// CTA per SM; a span is >= one tile (16 steps) and covers at most kMaxSeg - 2 whole rows.
 static LaunchPlan plan(const sampler* h, int32_t B) {
-  // equal STEP-aligned warp spans of the padded [B x Vq] vector space, kWarpsPerCta per CTA,
-  // kCtasPerSm CTAs per SM; a row has at most kMaxRecW sub-pieces (span >= Vq / (kMaxRecW - 2))
   LaunchPlan p;
-  p.N = (int64_t)B * h->Vq;
-  const int64_t W = (int64_t)h->max_ctas * kWarpsPerCta;
-  auto up = [](int64_t x) { return (x + kStepVec - 1) / kStepVec * kStepVec; };
-  int64_t span = up((p.N + W - 1) / W);
-  const int64_t min_span = up((h->Vq + kMaxRecW - 3) / (kMaxRecW - 2));
-  if (span < min_span) span = min_span;
-  p.span = span;
-  const int64_t warps = (p.N + span - 1) / span;
-  p.grid = (int)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
+  p.spr = (int)(h->Vq / kStepVec);
+  p.nsteps = (int64_t)B * p.spr;
+  int64_t span = (p.nsteps + h->sm_count - 1) / h->sm_count;
+  span = std::max<int64_t>(span, kTileSteps);
+  span = std::min<int64_t>(span, (int64_t)(kMaxSeg - 2) * p.spr);
+  p.span = (int)span;
+  p.grid = (int)((p.nsteps + span - 1) / span);
+  p.rpr = (p.spr + p.span - 1) / p.span + 1;
   return p;
 }
 
@@ -423,30 +460,28 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.voff = h->cfg.vocab_offset;
   a.vloc = h->cfg.vocab_local;
   a.Vq = h->Vq;
+  a.spr = lp.spr;
   a.span = lp.span;
-  a.N = lp.N;
+  a.rpr = lp.rpr;
+  a.nsteps = lp.nsteps;
   a.slots = slots;
   a.params_dev = params_dev;
   a.params_tab = h->d_params;
-  a.kcand = h->cfg.max_top_k;
-  a.pen_mode = h->cfg.penalty_mode;
-  a.hs.meta = h->d_meta;
-  a.hs.uniq = h->d_uniq;
-  a.hs.tokens = h->d_hist;
-  a.hs.L = h->cfg.max_history;
-  a.records = h->d_records;
+  a.hs = hist_state(h);
+  a.parts = h->d_parts;
   a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
+  a.dbg = h->dbg;
   return a;
 }
 
 static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
   if (h->d_trace)
-    CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * (64 * (int64_t)h->max_ctas + 32 * (int64_t)h->cfg.max_batch), st));
+    CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)h->cfg.max_batch), st));
   if (h->cfg.logits_dtype == SAMPLER_BF16)
-    stream_kernel<__nv_bfloat16><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+    stream_kernel<__nv_bfloat16><<<grid, kStreamThreads, kStreamSmem, st>>>(a);
   else
-    stream_kernel<float><<<grid, kWarpsPerCta * 32, kStreamSmem, st>>>(a);
+    stream_kernel<float><<<grid, kStreamThreads, kStreamSmem, st>>>(a);
   CK(h, cudaGetLastError());
   return SAMPLER_OK;
 }
@@ -462,8 +497,9 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.voff = h->cfg.vocab_offset;
   s.vloc = h->cfg.vocab_local;
   s.Vq = h->Vq;
+  s.spr = lp.spr;
   s.span = lp.span;
-  s.N = lp.N;
+  s.rpr = lp.rpr;
   s.slots = slots;
   s.params_dev = params_dev;
   s.params_tab = h->d_params;
@@ -474,13 +510,13 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.mode = 0;
   s.append = append;
   s.pending_ok = 1;
-  s.hs = HistState{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
-  s.records = h->d_records;
+  s.hs = hist_state(h);
+  s.parts = h->d_parts;
   s.gkeys = h->d_gkeys;
   s.ro = ro;
   s.out_records = nullptr;
   s.out_stride = h->rec_stride;
-  s.trace = h->d_trace ? h->d_trace + 64 * (int64_t)h->max_ctas : nullptr;
+  s.trace = h->d_trace ? h->d_trace + trace_a_len(h) : nullptr;
   return s;
 }
 
@@ -519,9 +555,9 @@ static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_par
   m.seeds = seeds;
   m.step = step;
   m.append = append;
-  m.hs = HistState{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  m.hs = hist_state(h);
   m.ro = ro;
-  m.trace = h->d_trace ? h->d_trace + 64 * (int64_t)h->max_ctas : nullptr;
+  m.trace = h->d_trace ? h->d_trace + trace_a_len(h) : nullptr;
   return m;
 }
 
@@ -609,7 +645,7 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
   rc = do_sample(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, 0, tokens_dev, logprobs_dev, nullptr,
                  nullptr, st);
   if (rc) return rc;
-  HistState hs{h->d_meta, h->d_uniq, h->d_hist, h->cfg.max_history};
+  HistState hs = hist_state(h);
   dim3 grid((unsigned)std::min(64, (h->cfg.vocab_local + 255) / 256), (unsigned)B);
   if (h->cfg.logits_dtype == SAMPLER_BF16)
     debug_q_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(logits, ld, h->cfg.vocab_size, h->cfg.vocab_offset,
@@ -627,7 +663,7 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
 int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n) {
   if (!h || !host_out || n < 0) return SAMPLER_EINVAL;
   if (!h->d_trace) return SAMPLER_EUNSUPPORTED;
-  const int64_t m = std::min<int64_t>(n, 64 * (int64_t)h->max_ctas + 32 * (int64_t)h->cfg.max_batch);
+  const int64_t m = std::min<int64_t>(n, trace_a_len(h) + 32 * (int64_t)h->cfg.max_batch);
   if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
     return SAMPLER_ECUDA;
   return SAMPLER_OK;

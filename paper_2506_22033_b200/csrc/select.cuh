@@ -4,9 +4,10 @@
 // One dependent chain per row, shaped for latency (the GPU is otherwise idle while it runs):
 //   prologue   (independent of phase A; overlaps its tail under programmatic dependent launch)
 //              the slot's unique-token table -> smem, raw logits of its ids -> registers
-//   RT1        piece headers, lane-max lists, the row's group keys (one round trip)
-//   bound      T = K-th largest lane max of the row (every list entry counts the entries >= it
-//              across the lists by binary lifting).  K distinct elements are >= T.
+//   RT1        piece headers and the row's group keys (one round trip); M, S from the headers
+//   bound      T = K-th largest 16-bit key among the group keys and the penalised elements: one
+//              smem histogram over the kHistBins key steps below key(M) (one bin per key value,
+//              so T is exact).  K distinct elements are >= val(T)
 //   collect    penalised ids: exact penalised value from the prefetched raws;
 //              groups with key >= key(T): re-read (RT2), penalised ids and padding masked, every
 //              element >= T pushed — the pool then holds EVERY element of the row >= T, exactly
@@ -21,6 +22,7 @@
 #include "merge.cuh"
 #include "philox.cuh"
 #include "piece.cuh"
+#include "stream.cuh"
 
 namespace smp {
 
@@ -33,7 +35,8 @@ struct SelectArgs {
   const void* logits;
   int64_t ld;
   int B, V, voff, vloc;
-  int64_t Vq, span, N;
+  int64_t Vq;
+  int spr, span, rpr;  // phase A geometry (stream.cuh)
   const int32_t* slots;
   const sampling_params* params_dev;
   const sampling_params* params_tab;
@@ -41,7 +44,7 @@ struct SelectArgs {
   uint64_t step;
   int kcand, pen_mode, mode, append, pending_ok;
   HistState hs;
-  const uint8_t* records;  // warp records (kWarpRecStride), index = global warp + row
+  const PartRec* parts;    // phase A partial records [B][rpr][kCW]
   const uint16_t* gkeys;
   RowOut ro;
   uint8_t* out_records;  // mode 1: one candidate record per row
@@ -51,8 +54,9 @@ struct SelectArgs {
 
 // shared-memory carve-up (phase B)
 constexpr int kSOffUe = 0;                                         // [kSelPen] UniqEntry
-constexpr int kSOffLm = kSOffUe + kSelPen * 8;                     // [kMaxRecW][32] u32
-constexpr int kSOffPool = kSOffLm + kMaxRecW * kLaneList * 4;      // [kPool] u64
+constexpr int kHistBins = 1024;                                    // bound histogram (key steps)
+constexpr int kSOffHist = kSOffUe + kSelPen * 8;                   // [kHistBins] u32
+constexpr int kSOffPool = kSOffHist + kHistBins * 4;               // [kPool] u64
 constexpr int kSOffQl = kSOffPool + kPool * 8;                     // [kSelQ] u32
 constexpr int kSOffTop = kSOffQl + kSelQ * 4;                      // [KC] u64
 constexpr int kSOffWv = kSOffTop + SAMPLER_KCAND_MAX * 8;          // [KC] double
@@ -61,7 +65,8 @@ constexpr int kSOffHdr = kSOffById + SAMPLER_KCAND_MAX * 8;        // [kMaxRecW]
 constexpr int kSOffScr = kSOffHdr + kMaxRecW * 48;                 // f[8] d[8] u[16] i[16]
 constexpr int kSOffCtl = kSOffScr + 288;                           // ints [16]
 constexpr int kSOffGk = kSOffCtl + 64;                             // [kSelGR * kBT] uint4 group keys
-constexpr int kSelectSmem = kSOffGk + kSelGR * kBT * 16;
+constexpr int kSOffSk = kSOffGk + kSelGR * kBT * 16;               // [kBT] u16 step keys
+constexpr int kSelectSmem = kSOffSk + kBT * 2;
 
 
 // Append `tok` to the slot's history (P:371 incremental update) from the smem copy of the sorted
@@ -91,6 +96,7 @@ __device__ __forceinline__ void block_append_smem(const HistState& hs, int slot,
       e.meta = 2u;
       u[less] = e;
     }
+    offs_bump(hs, slot, tok, tid, kBT);
   }
   if (tid == 0) {
     hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
@@ -145,7 +151,7 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
     cbar();
     shrink();
   }
-  const uint16_t* gk = a.gkeys + (int64_t)blockIdx.x * (a.Vq / kG);
+  const uint16_t* gk = a.gkeys + (int64_t)blockIdx.x * gk_stride(a.Vq);
   for (int g0 = 0; g0 < gwords * 8; g0 += 32) {  // 32 groups = 128 vectors per round
     if (tid < 128) {
       const int g = g0 + (tid >> 2);
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   const int r = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
   UniqEntry* s_ue = reinterpret_cast<UniqEntry*>(smem + kSOffUe);
-  uint32_t* lm = reinterpret_cast<uint32_t*>(smem + kSOffLm);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kSOffHist);
   int* ctl = reinterpret_cast<int*>(smem + kSOffCtl);  // [0] T key [1] pool count [2] group count
   MergeSmem ms;
   ms.pool = reinterpret_cast<uint64_t*>(smem + kSOffPool);
@@ -237,115 +243,156 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     ctl[2] = 0;
     ctl[5] = 0;
   }
+  // exact penalised values (binary32 ops), NaN for "not in this slice"
+#pragma unroll
+  for (int q = 0; q < kSelPR; ++q)
+    raw[q] = (lid[q] >= 0) ? apply_penalty(raw[q], s_ue[tid + q * kBT].meta, prm, a.pen_mode) : NAN;
   griddep_wait();  // phase A's records and group keys are visible from here on
-  // ---- RT1: warp-record headers, lane-max lists, group keys
-  const int64_t w_first = ((int64_t)r * a.Vq) / a.span;
-  const int64_t w_last = ((int64_t)(r + 1) * a.Vq - 1) / a.span;
-  const int nrec = (int)(w_last - w_first + 1);  // <= kMaxRecW (plan)
-  const uint8_t* recs = a.records + (w_first + r) * (int64_t)kWarpRecStride;
-  if (tid < nrec) ms.hdr[tid] = *reinterpret_cast<const RecHdr*>(recs + (int64_t)tid * kWarpRecStride);
-  for (int i = tid; i < nrec * kLaneList; i += kBT)
-    lm[i] = reinterpret_cast<const uint32_t*>(recs + (int64_t)(i >> 5) * kWarpRecStride + kRecHdrBytes)[i & 31];
+  // ---- RT1: the row's partial records, step keys and group keys (one round trip)
+  const int64_t cfirst = ((int64_t)r * a.spr) / a.span;
+  const int64_t clast = ((int64_t)(r + 1) * a.spr - 1) / a.span;
+  const int nparts = (int)(clast - cfirst + 1) * kCW;
+  const PartRec* prow = a.parts + (int64_t)r * a.rpr * kCW;
+  PartRec p0;
+  p0.m = -INFINITY;
+  p0.bad = 0u;
+  p0.s = 0.0;
+  if (tid < nparts) p0 = prow[tid];
   const int nvv = (a.vloc + VEC - 1) / VEC;
   const int gwords = ((nvv + kStepVec - 1) / kStepVec) * 32 / 8;  // valid group-key words (8 keys)
-  const uint4* gk4 = reinterpret_cast<const uint4*>(a.gkeys + (int64_t)r * (a.Vq / kG));
+  const uint4* gk4 = reinterpret_cast<const uint4*>(a.gkeys + (int64_t)r * gk_stride(a.Vq));
+  const uint16_t* sk = a.gkeys + (int64_t)r * gk_stride(a.Vq) + a.Vq / kG;  // step keys
+  const int nsv = (nvv + kStepVec - 1) / kStepVec;                             // real steps
+  uint16_t* s_sk = reinterpret_cast<uint16_t*>(smem + kSOffSk);
+  if (tid < nsv && tid < kBT) s_sk[tid] = sk[tid];
   uint4* s_gk = reinterpret_cast<uint4*>(smem + kSOffGk);
 #pragma unroll
   for (int q = 0; q < kSelGR; ++q) {  // staged in smem: every load of RT1 completes at one barrier
     const int w = tid + q * kBT;
     s_gk[w] = (w < gwords) ? gk4[w] : make_uint4(0, 0, 0, 0);
   }
-  cbar();
+  for (int i = tid; i < kHistBins; i += kBT) hist[i] = 0u;
+  // ---- M = max of the stream partials and the exact penalised values;
+  //      S = sum_parts s 2^((m - M) c) + sum_pen 2^((z' - M) c)   (fixed order: deterministic)
+  float mloc = p0.m;
+  unsigned fl = p0.bad;
+  for (int o = tid + kBT; o < nparts; o += kBT) {
+    const PartRec pr = prow[o];
+    mloc = fmaxf(mloc, pr.m);
+    fl |= pr.bad;
+  }
+#pragma unroll
+  for (int q = 0; q < kSelPR; ++q)
+    if (lid[q] >= 0) {
+      if (!(raw[q] < INFINITY)) fl |= kRecBad;  // NaN / +inf logit (or penalised value)
+      else mloc = fmaxf(mloc, raw[q]);
+    }
+  for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
+    const UniqEntry ue = utab[e];
+    const int l = ue.id - a.voff;
+    if (l < 0 || l >= a.vloc) continue;
+    const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+    if (!(zp < INFINITY)) fl |= kRecBad;
+    else mloc = fmaxf(mloc, zp);
+  }
+  const float M = block_max_f(mloc, ms.bs);
+  const bool bad = block_or_i((int)(fl & kRecBad), ms.bs) != 0;
   STR(1);
-  // ---- bound: T = K-th largest lane max of the row; M, S, flags (warp 0)
-  // prefilter (every thread, smem broadcast): with m = ceil(K / nrec), the lists holding >= m
-  // entries contribute m entries each >= LB = min of their m-th entries; if that is >= K
-  // entries, T >= LB and only entries >= LB need an exact count
-  uint32_t lb = 0;
-  {
-    const int m = (keff + nrec - 1) / nrec;
-    uint32_t mn = 0xFFFFFFFFu;
-    int have = 0;
-    if (m <= kLaneList)
-      for (int o = 0; o < nrec; ++o)
-        if ((int)ms.hdr[o].n >= m) {
-          mn = min(mn, lm[o * kLaneList + m - 1]);
-          have += m;
-        }
-    if (have >= keff) lb = mn;
-  }
-  // the entries >= LB, compacted (warp-aggregated), then one exact count per entry
-  uint32_t* cx = ql;  // scratch until the collect phase
-  for (int i0 = 0; i0 < nrec * kLaneList; i0 += kBT) {
-    const int i = i0 + tid;
-    const uint32_t x = (i < nrec * kLaneList) ? lm[i] : 0u;
-    const bool pass = x != 0u && x >= lb;
-    const unsigned bal = __ballot_sync(kFull, pass);
-    int at = 0;
-    if (lane == 0 && bal) at = atomicAdd(&ctl[5], __popc(bal));
-    at = __shfl_sync(kFull, at, 0) + __popc(bal & ((1u << lane) - 1u));
-    if (pass) cx[at] = x;
-  }
-  cbar();
-  const int ncx = ctl[5];
-  uint32_t tbest = 0;  // largest own entry with count >= K (warp-reduced: one atomic per warp)
-  for (int j = tid; j < ncx; j += kBT) {
-    const uint32_t x = cx[j];
-    if (x <= tbest) continue;
-    int c = 0;
-    for (int o0 = 0; o0 < nrec; o0 += 8) {  // 8 lists side by side (independent lifting chains)
-      int pos[8], no[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        pos[t] = 0;
-        no[t] = (o0 + t < nrec) ? (int)ms.hdr[o0 + t].n : 0;
-      }
-#pragma unroll
-      for (int st = 32; st; st >>= 1)
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (pos[t] + st <= no[t] && lm[(o0 + t) * kLaneList + pos[t] + st - 1] >= x) pos[t] += st;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) c += pos[t];
+  double term = 0.0;
+  if (M > -INFINITY && !bad) {
+    if (p0.s != 0.0) term += p0.s * exp2(((double)p0.m - (double)M) * rc.c_d);
+    for (int o = tid + kBT; o < nparts; o += kBT) {
+      const PartRec pr = prow[o];
+      if (pr.s != 0.0) term += pr.s * exp2(((double)pr.m - (double)M) * rc.c_d);
     }
-    if (c >= keff) tbest = x;
-  }
-  STR(16);
-  tbest = __reduce_max_sync(kFull, tbest);
-  if (lane == 0 && tbest) atomicMax(reinterpret_cast<unsigned*>(&ctl[0]), tbest);
-  STR(17);
-  if (tid >= kBT - 32) {  // the last warp (the counting above uses the first warps)
-    float mloc = -INFINITY;
-    unsigned fl = 0;
-    for (int o = lane; o < nrec; o += 32) {
-      mloc = fmaxf(mloc, ms.hdr[o].m);
-      fl |= ms.hdr[o].flags;
+#pragma unroll
+    for (int q = 0; q < kSelPR; ++q)
+      if (lid[q] >= 0 && raw[q] > -INFINITY) term += exp2(((double)raw[q] - (double)M) * rc.c_d);
+    for (int e = kSelPen + tid; e < nu; e += kBT) {
+      const UniqEntry ue = utab[e];
+      const int l = ue.id - a.voff;
+      if (l < 0 || l >= a.vloc) continue;
+      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+      if (zp > -INFINITY) term += exp2(((double)zp - (double)M) * rc.c_d);
     }
-    const float M = warp_max(mloc);
-    const double RM = (double)M * rc.c_d;
-    double term = 0.0;
-    for (int o = lane; o < nrec; o += 32)
-      if (ms.hdr[o].s != 0.0) term += ms.hdr[o].s * exp2(ms.hdr[o].R - RM);
-    const double S = warp_sum_d(term);
-    fl = __reduce_or_sync(kFull, fl);
-    if (lane == 0) {
-      ms.bs.f[0] = M;
-      ms.bs.d[0] = S;
-      ms.bs.d[1] = log(S);
-      ms.bs.i[0] = (int)fl;
-    }
-    STR(18);
   }
-  cbar();
+  const double S = block_sum_d(term, ms.bs);
+  const double logS = log(S);
   STR(2);
-  const float M = ms.bs.f[0];  // (the block scratch is reused below)
-  const double S = ms.bs.d[0];
-  const double logS = ms.bs.d[1];
-  const bool bad = (ms.bs.i[0] & kRecBad) != 0;
-  const uint32_t tkey = (uint32_t)ctl[0];
-  const bool bounded = tkey != 0u;
-  const float Tv = bounded ? key2f(tkey) : -3.402823466e38f;
-  const uint32_t lo_k = bounded ? max(key16_down(Tv), kKey16NegInf + 1) : kKey16NegInf + 1;
+  // ---- bound: T = the K-th largest step key (each step key = the max of 1024 / 512 elements
+  // rounded down, so K distinct elements are >= val(T)); every element >= val(T) lies in a
+  // group with key >= T or is penalised.  One rank count per step key (smem broadcast).
+  // Fallback (fewer than K finite step keys, or more steps than threads): T = the K-th largest
+  // 16-bit key among the group keys and the penalised elements, by one histogram pass over the
+  // kHistBins key steps below key(M) (one bin per key value: exact); a row whose K-th key lies
+  // below that window takes every finite element (the collection then shrinks in bounded rounds).
+  const bool rowok = !bad && M > -INFINITY;
+  const uint32_t kmax = rowok ? key16_down(M) : 0u;
+  uint32_t lo_k = kKey16NegInf + 1;
+  bool need_hist = rowok;
+  if (rowok && nsv >= keff && nsv <= kBT) {
+    const uint32_t x = (tid < nsv) ? (uint32_t)s_sk[tid] : 0u;
+    if (x > kKey16NegInf) {
+      int gt = 0, ge = 0;
+      for (int j = 0; j < nsv; ++j) {
+        const uint32_t y = s_sk[j];
+        gt += y > x;
+        ge += y >= x;
+      }
+      if (gt < keff && ge >= keff) ctl[0] = (int)x;  // every such thread writes the same x
+    }
+    cbar();
+    if (ctl[0] != 0) {
+      lo_k = (uint32_t)ctl[0];
+      need_hist = false;
+    }
+  }
+  if (need_hist) {
+    auto add_key = [&](uint32_t key) {
+      const uint32_t d = kmax - key;
+      if (key > kKey16NegInf && d < (uint32_t)kHistBins) atomicAdd(&hist[d], 1u);
+    };
+#pragma unroll
+    for (int q = 0; q < kSelPR; ++q)
+      if (lid[q] >= 0 && raw[q] > -INFINITY && raw[q] < INFINITY) add_key(key16_down(raw[q]));
+    for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
+      const UniqEntry ue = utab[e];
+      const int l = ue.id - a.voff;
+      if (l < 0 || l >= a.vloc) continue;
+      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+      if (zp > -INFINITY && zp < INFINITY) add_key(key16_down(zp));
+    }
+    for (int w = tid; w < gwords; w += kBT) {
+      const uint4 g = (w < kSelGR * kBT) ? s_gk[w] : gk4[w];
+      const uint32_t x[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        add_key(x[t] & 0xFFFFu);
+        add_key(x[t] >> 16);
+      }
+    }
+    cbar();
+    // exclusive prefix over bins (bin 0 = key(M)): thread t owns bins [4t, 4t + 4)
+    static_assert(kHistBins == 4 * kBT, "histogram scan layout");
+    const uint4 hb = reinterpret_cast<const uint4*>(hist)[tid];
+    const int own = (int)(hb.x + hb.y + hb.z + hb.w);
+    const int incl = warp_incl_scan_i(own, lane);
+    if (lane == 31) ms.bs.i[8 + (tid >> 5)] = incl;
+    cbar();
+    int before = incl - own;
+    for (int w = 0; w < (tid >> 5); ++w) before += ms.bs.i[8 + w];
+    if (tid == 0) ctl[0] = 0;
+    cbar();
+    if (before < keff && before + own >= keff) {
+      const uint32_t h4[4] = {hb.x, hb.y, hb.z, hb.w};
+      int cum = before, b = 0;
+      while (cum + (int)h4[b] < keff) cum += (int)h4[b++];
+      ctl[0] = (int)(kmax - (uint32_t)(4 * tid + b));
+    }
+    cbar();
+    if (ctl[0] != 0) lo_k = (uint32_t)ctl[0];
+  }
+  const float Tv = key16_val(lo_k);
   // ---- collect: penalised elements (exact), then the qualifying groups
   auto push = [&](uint64_t c) {
     const int at = atomicAdd(&ctl[1], 1);
@@ -354,7 +401,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
 #pragma unroll
   for (int q = 0; q < kSelPR; ++q) {
     if (lid[q] < 0) continue;
-    const float zp = apply_penalty(raw[q], s_ue[tid + q * kBT].meta, prm, a.pen_mode);
+    const float zp = raw[q];
     if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, a.voff + lid[q]));
   }
   for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
@@ -397,7 +444,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   }
   cbar();
   STR(3);
-  const bool slow = ctl[2] > kSelQ || ctl[1] + ctl[2] * kG * VEC > kPool;
+  bool slow = ctl[2] > kSelQ;
   const int nq = slow ? 0 : ctl[2];
   const int ns = nus;
   for (int it0 = 0; it0 < nq * kG; it0 += kBT) {  // uniform per warp: aggregated pushes
@@ -436,6 +483,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
         ++at;
       }
   }
+  cbar();
+  slow = slow || ctl[1] > kPool;  // uniform: after the barrier
   uint64_t floor = 0;
   if (slow) floor = select_collect_slow<T>(a, rowp, utab, s_ue, nu, nus, prm, Tv, lo_k, nvv, gwords, keff, ms, ctl, ql);
   cbar();
@@ -462,7 +511,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   STR(5);
   const int n = nc < keff ? nc : keff;
   // every element >= T is in the pool: the candidates are exact from the top down to T
-  uint64_t F = bounded ? make_comp(Tv, 0x7FFFFFFF) : 0ull;
+  uint64_t F = rowok ? make_comp(Tv, 0x7FFFFFFF) : 0ull;
   F = floor > F ? floor : F;
   if (nc > keff) F = ms.top[keff - 1] > F ? ms.top[keff - 1] : F;
 

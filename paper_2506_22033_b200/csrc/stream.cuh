@@ -1,23 +1,24 @@
 // stream.cuh — phase A of the sampling step: one streaming pass over the logits [B x V].
 //
-// Every warp works alone (piece.cuh: the padded [B x Vq] vector space cut into equal STEP-
-// aligned warp spans; a span crossing a row boundary yields one sub-piece per row) — there is no
-// CTA barrier in phase A, so no warp ever waits for another's epilogue or metadata:
-//   * metadata: the row's params and the slot's incremental unique-token table: the
-//     warp counts the entries below / inside its sub-piece and stages those into its own smem
-//     region; the raw logits of the penalised ids are prefetched into registers.
-//   * the stream: 16-byte read-only no-L1-allocate loads, 4 vectors (32 bf16 / 16 f32 logits)
-//     per lane per step, the next step's loads issued before the current step is computed; the
-//     penalised ids and the padding tail are masked to -inf in registers (the staged ids walked
-//     in order with the stream), then one NaN-propagating max per vector, the group key (bf16
-//     key of the group max, rounded down) stored to gkeys[row], and the exp-sum: 2 FFMA + 1
-//     MUFU.EX2 per logit into a float64 lane accumulator with an integer exponent reference.
-//   * the penalised elements enter as single exact values: OPENAI_CTRL / LINEAR penalty in
-//     exact binary32 ops, exp-sum, lane max.
-//   * epilogue: the 32 lane maxima sorted by a shuffle bitonic network and written with the
-//     sub-piece's max / exp-sum / bad flag as the warp record.
-// The selection (bound, re-read of the qualifying groups, exact top-K, decision, draw) is phase B
-// (select.cuh).
+// Persistent CTAs (one per SM), warp-specialised.  The padded step space [B x Vq/128] (a step =
+// 128 16-byte vectors = 2 KB of one row) is cut into equal contiguous CTA spans:
+//   * producer warp: one 1-D bulk copy (cp.async.bulk, TMA engine, L2 evict-first) per step into a
+//     ring of kNS tiles of 16 steps (32 KB each), full / empty mbarriers;
+//   * 16 consumer warps: warp w takes step w of every tile (4 vectors = 32 bf16 / 16 f32 logits per
+//     lane); the row's penalised ids (the slot's incremental unique-token table, located in
+//     O(1) by its bucket offsets) are a CTA-wide smem bitmap built once per bitmap phase, and
+//     masked to -inf in registers with the padding tail; then per lane and step (a "group"):
+//       - the group max by a NaN-propagating packed max tree (bf16x2 HMNMX2), its order-preserving
+//         16-bit key stored to gkeys[row][group] (phase B selects the top-k from these keys);
+//       - the exp-sum of P:149's softmax denominator, sum 2^((z - m_ref) * log2(e)/tau):
+//         bf16: t = z - m_ref straight from the packed register half (mixed-precision FHFMA.BF16,
+//         exact for bf16 operands), x = t * c by packed FMUL2, MUFU.EX2, packed FADD2 tree, one
+//         float64 add per group.  m_ref (lane-private) is rebased only when a group max exceeds
+//         it by 8 / c (every term <= 2^8), the float64 sum rescaled by exp2 in float64.
+//   * when a warp leaves a row: its partial record {max m, s = sum 2^((z - m) log2(e)/tau)
+//     (float64), bad} (phase B adds the penalised elements as exact single values).
+// The selection (bound from the group keys, re-read of the qualifying groups, exact top-K,
+// decision, draw) is phase B (select.cuh).
 #pragma once
 #include "common.cuh"
 #include "elem.cuh"
@@ -26,11 +27,26 @@
 
 namespace smp {
 
-constexpr int kWarpsPerCta = 8;
-constexpr int kCtasPerSm = 3;
-constexpr int kPenW = 128;         // penalty entries staged per warp (more: read from global)
-constexpr int kPenWQ = kPenW / 32;  // raw penalised logits prefetched per lane
-constexpr int kStreamSmem = kWarpsPerCta * kPenW * 8;
+// ---- geometry of phase A (persistent CTAs, warp-specialised) ----------------------
+constexpr int kCW = 24;                    // consumer warps per CTA (one step of each tile each)
+constexpr int kTileSteps = kCW;            // steps per ring tile (24 x 2 KB = 48 KB)
+constexpr int kNS = 3;                     // ring tiles (144 KB of bulk copies in flight per SM)
+constexpr int kBmMax = 384;                // steps covered by one penalty-bitmap phase
+constexpr int kMaxSeg = 48;                // rows per CTA span (the host caps the span)
+constexpr int kStreamThreads = (kCW + 1) * 32;  // + one producer warp
+constexpr int kStepBytes = kStepVec * 16;
+constexpr int kSOffRing = 0;
+constexpr int kSOffBm = kSOffRing + kNS * kTileSteps * kStepBytes;
+constexpr int kSOffBar = kSOffBm + kBmMax * 32 * 4;
+constexpr int kSOffSeg = kSOffBar + 2 * kNS * 8;
+constexpr int kStreamSmem = kSOffSeg + kMaxSeg * 8;
+
+// one consumer warp's partial reduction of one row: max m and s = sum 2^((z - m) log2(e)/tau)
+struct __align__(16) PartRec {
+  float m;
+  uint32_t bad;
+  double s;
+};
 
 struct StreamArgs {
   const void* logits;
@@ -39,197 +55,367 @@ struct StreamArgs {
   int V;               // global vocab
   int voff, vloc;      // local slice
   int64_t Vq;          // padded row length in vectors (multiple of kStepVec)
-  int64_t span;        // vectors per warp (multiple of kStepVec)
-  int64_t N;           // B * Vq
+  int spr;             // steps per row = Vq / kStepVec
+  int span;            // steps per CTA
+  int rpr;             // CTA record blocks per row
+  int64_t nsteps;      // B * spr
   const int32_t* slots;
   const sampling_params* params_dev;  // nullable
   const sampling_params* params_tab;
-  int kcand;
-  int pen_mode;
   HistState hs;
-  uint8_t* records;    // warp records (kWarpRecStride bytes), index = global warp + row
-  uint16_t* gkeys;     // [B][Vq / 4] group keys
-  uint64_t* trace;     // debug: per-warp start / end timestamps (globaltimer ns, 8 per warp), nullable
+  PartRec* parts;      // [B][rpr][kCW]
+  uint16_t* gkeys;     // [B][gk_stride(Vq)]: group keys | step keys
+  uint64_t* trace;     // debug: per-CTA start / end timestamps (globaltimer ns, 64 per CTA), nullable
+  int dbg;             // development switches (SAMPLER_DBG): bit0 no exp-sum, bit1 no keys, bit2 no mask
 };
 
+// ---- packed binary32 pairs (sm_100a FADD2 / FMUL2) ----------------------------------
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// (lo, hi) bf16 halves of w minus m, each correctly rounded to binary32 (exact when m is a
+// bf16 value: the difference of two bf16 numbers fits binary32): fma.rn.f32.bf16(z, 1, -m)
+__device__ __forceinline__ uint64_t bf16x2_sub(uint32_t w, float nm) {
+  float a, b;
+  asm("{.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, l, %3, %4;\n\tfma.rn.f32.bf16 %1, h, %3, %4;}"
+      : "=f"(a), "=f"(b)
+      : "r"(w), "h"((unsigned short)0x3F80), "f"(nm));
+  return f2_pack(a, b);
+}
+
+// Per-step (group) math.  u = the lane's 4 vectors of the step (masked).  gmax(): NaN-propagating
+// max; esum(): sum over the group of 2^((z + nm) * c), nm = -m_ref (the terms of -inf are 0).
 template <typename T>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, kCtasPerSm) stream_kernel(const StreamArgs a) {
+struct GroupMath;
+template <>
+struct GroupMath<__nv_bfloat16> {
+  static __device__ __forceinline__ float gmax(const uint4 (&u)[kG]) {
+    __nv_bfloat162 m[4];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u[j].x);
+      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u[j].y);
+      const __nv_bfloat162 c = *reinterpret_cast<const __nv_bfloat162*>(&u[j].z);
+      const __nv_bfloat162 d = *reinterpret_cast<const __nv_bfloat162*>(&u[j].w);
+      m[j] = __hmax2_nan(__hmax2_nan(a, b), __hmax2_nan(c, d));
+    }
+    const __nv_bfloat162 r = __hmax2_nan(__hmax2_nan(m[0], m[1]), __hmax2_nan(m[2], m[3]));
+    return fmax_nan(__low2float(r), __high2float(r));
+  }
+  static __device__ __forceinline__ float esum(const uint4 (&u)[kG], float nm, uint64_t c2) {
+    uint64_t e[2 * kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+      uint64_t p[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float a, b;
+        f2_unpack(f2_mul(bf16x2_sub(w[i], nm), c2), a, b);
+        p[i] = f2_pack(ex2f(a), ex2f(b));
+      }
+      e[2 * j] = f2_add(p[0], p[1]);
+      e[2 * j + 1] = f2_add(p[2], p[3]);
+    }
+#pragma unroll
+    for (int s = 1; s < 2 * kG; s <<= 1)
+#pragma unroll
+      for (int i = 0; i < 2 * kG; i += 2 * s) e[i] = f2_add(e[i], e[i + s]);
+    float a, b;
+    f2_unpack(e[0], a, b);
+    return a + b;
+  }
+};
+template <>
+struct GroupMath<float> {
+  static __device__ __forceinline__ float gmax(const uint4 (&u)[kG]) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) m = fmax_nan(m, Dec<float>::vmax(u[j]));
+    return m;
+  }
+  static __device__ __forceinline__ float esum(const uint4 (&u)[kG], float nm, uint64_t c2) {
+    const uint64_t nm2 = f2_pack(nm, nm);
+    uint64_t e[2 * kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const uint64_t t0 = f2_add(f2_pack(__uint_as_float(u[j].x), __uint_as_float(u[j].y)), nm2);
+      const uint64_t t1 = f2_add(f2_pack(__uint_as_float(u[j].z), __uint_as_float(u[j].w)), nm2);
+      float a, b, c, d;
+      f2_unpack(f2_mul(t0, c2), a, b);
+      f2_unpack(f2_mul(t1, c2), c, d);
+      e[2 * j] = f2_pack(ex2f(a), ex2f(b));
+      e[2 * j + 1] = f2_pack(ex2f(c), ex2f(d));
+    }
+#pragma unroll
+    for (int s = 1; s < 2 * kG; s <<= 1)
+#pragma unroll
+      for (int i = 0; i < 2 * kG; i += 2 * s) e[i] = f2_add(e[i], e[i + s]);
+    float a, b;
+    f2_unpack(e[0], a, b);
+    return a + b;
+  }
+};
+
+// Lane-private online softmax state: acc = sum 2^((z - mref) * c) (float64); a new mref is
+// taken when an element exceeds thr = mref + 8 / c.
+struct LaneSum {
+  float mref, thr, nm, mmax;
+  double acc;
+  int bad;
+  __device__ __forceinline__ void reset() {
+    mref = -INFINITY;
+    thr = -INFINITY;
+    nm = INFINITY;
+    mmax = -INFINITY;
+    acc = 0.0;
+    bad = 0;
+  }
+  __device__ __forceinline__ void rebase(float m, float c, float inv8) {
+    if (acc != 0.0) acc *= (double)ex2f((mref - m) * c);
+    mref = m;
+    nm = -m;
+    thr = m + inv8;
+  }
+};
+
+// Consumer-side prologue of one bitmap phase: CTA-relative steps [pa, pb) of the span that
+// starts at global step s0.  bm word (i - pa, lane), bit j*VEC + t <=> element t of vector
+// 128 k + lane + 32 j (k = the step's index in its row) is penalised: those elements are masked
+// to -inf in the stream (phase B applies their exact penalised values).
+template <int VEC>
+__device__ __forceinline__ void build_bitmap(const StreamArgs& a, int64_t s0, int pa, int pb, uint32_t* bm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < kBmMax * 32; i += kCW * 32) bm[i] = 0u;
+  cbar_n<kCW * 32>();
+  const int nvv = (a.vloc + VEC - 1) / VEC;
+  const int rA = (int)((s0 + pa) / a.spr), rB = (int)((s0 + pb - 1) / a.spr);
+  for (int r = rA + w; r <= rB; r += kCW) {
+    const int slot = a.slots ? a.slots[r] : r;
+    const int64_t rs = (int64_t)r * a.spr;
+    const int k0 = (int)(max(rs, s0 + pa) - rs), k1 = (int)(min(rs + a.spr, s0 + pb) - rs);  // row steps
+    const int32_t* offs = a.hs.offs + (int64_t)slot * (a.hs.nb + 1);
+    const int lo = offs[k0 * kStepVec * VEC / kOffsBucket];
+    const int hi = offs[(k1 * kStepVec >= nvv) ? a.hs.nb : k1 * kStepVec * VEC / kOffsBucket];
+    const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
+    const int ibase = (int)(rs - s0) - pa;  // bitmap step index of row step 0
+    for (int e = lo + lane; e < hi; e += 32) {
+      const int le = ut[e].id - a.voff;
+      const int v = le / VEC;
+      const int k = v / kStepVec, d = v - k * kStepVec;
+      atomicOr(&bm[(ibase + k) * 32 + (d & 31)], 1u << ((d >> 5) * VEC + (le & (VEC - 1))));
+    }
+  }
+  cbar_n<kCW * 32>();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamArgs a) {
   constexpr int VEC = Dec<T>::N;
   constexpr int ESZ = (int)sizeof(T);
-
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + wid;  // global warp index
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint8_t* ring = smem + kSOffRing;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + kSOffBm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSOffBar);
+  uint64_t* empty = full + kNS;
+  float2* segc = reinterpret_cast<float2*>(smem + kSOffSeg);  // per row of the span: (c, 8 / c)
   const uint4 kNegInfVec = make_uint4(Dec<T>::kNegInfWord, Dec<T>::kNegInfWord, Dec<T>::kNegInfWord,
                                       Dec<T>::kNegInfWord);
   griddep_launch();  // phase B's CTAs may be scheduled as this grid's CTAs retire
-  const int64_t a0 = gw * a.span;
-  const int64_t a1 = min(a.N, a0 + a.span);
-  UniqEntry* wpen = reinterpret_cast<UniqEntry*>(smem) + wid * kPenW;
+  const int64_t s0 = (int64_t)blockIdx.x * a.span;
+  const int nspan = (int)min((int64_t)a.span, a.nsteps - s0);  // steps of this CTA
+  const int ntiles = (nspan + kTileSteps - 1) / kTileSteps;
+  const int nvv = (a.vloc + VEC - 1) / VEC;
   const uint8_t* lg = reinterpret_cast<const uint8_t*>(a.logits);
-  const int nvv = (a.vloc + VEC - 1) / VEC;  // real vectors per row
-  if (a.trace && lane == 0) a.trace[gw * 8 + 0] = gtimer();
-
-  int64_t pos = a0;
-  while (pos < a1) {
-    // ---------------- sub-piece = row vectors [p0, p1) of row r (STEP-aligned)
-    const int r = (int)(pos / a.Vq);
-    const int p0 = (int)(pos - (int64_t)r * a.Vq);
-    const int64_t pend = min(a1, (int64_t)(r + 1) * a.Vq);
-    const int p1 = (int)(pend - (int64_t)r * a.Vq);
-    const int pv1 = min(p1, nvv);  // real vectors end
-    const int nsteps = pv1 > p0 ? (pv1 - p0 + kStepVec - 1) / kStepVec : 0;
-    const uint8_t* rowp = lg + (int64_t)r * a.ld * ESZ;
-    // first loads go out before any metadata round trip
-    uint4 u[kG];
-#pragma unroll
-    for (int j = 0; j < kG; ++j) {
-      const int v = p0 + lane + 32 * j;
-      u[j] = (nsteps > 0 && v < nvv) ? ldg_stream(rowp + (int64_t)v * 16) : kNegInfVec;
+  const int64_t ldb = a.ld * ESZ;
+  if (a.trace && tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.trace[blockIdx.x * 64 + 0] = gtimer();
+    a.trace[blockIdx.x * 64 + 1] = smid;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kCW);
     }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (w == kCW) {
+    // ================= producer warp: 1-D bulk copies (TMA engine), one per step =================
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      int r = (int)(s0 / a.spr), k = (int)(s0 - (int64_t)r * a.spr);
+      for (int t = 0; t < ntiles; ++t) {
+        const int sl = t % kNS;
+        if (t >= kNS) mbar_wait(empty + sl, (uint32_t)((t / kNS - 1) & 1));
+        const int n = min(kTileSteps, nspan - t * kTileSteps);
+        uint32_t bytes = 0;
+        {
+          int rr = r, kk = k;
+          for (int j = 0; j < n; ++j) {
+            bytes += (uint32_t)min(kStepVec, nvv - kk * kStepVec) * 16u;
+            if (++kk == a.spr) { kk = 0; ++rr; }
+          }
+        }
+        mbar_arrive_expect_tx(full + sl, bytes);
+        uint8_t* dst = ring + sl * (kTileSteps * kStepBytes);
+        // one bulk copy per run of consecutive steps of one row (contiguous in global memory)
+        for (int j = 0; j < n;) {
+          const int j0 = j, k0 = k;
+          uint32_t nb = 0;
+          do {
+            nb += (uint32_t)min(kStepVec, nvv - k * kStepVec) * 16u;
+            ++j;
+            ++k;
+          } while (j < n && k < a.spr);
+          bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
+          if (k == a.spr) { k = 0; ++r; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ================= consumer warps =================
+  // span rows: constants, and every (row, this CTA, warp) partial record initialised empty
+  const int r_cta0 = (int)(s0 / a.spr);
+  const int r_cta1 = (int)((s0 + nspan - 1) / a.spr);
+  for (int g = w; g <= r_cta1 - r_cta0; g += kCW) {
+    const int r = r_cta0 + g;
     const int slot = a.slots ? a.slots[r] : r;
     const sampling_params* gprm = a.params_dev ? a.params_dev + r : a.params_tab + slot;
-    const RowCfg rc = decode_row(*gprm, a.V, a.kcand);
-    // penalty entries of the sub-piece: global ids in [g0, g1)
-    const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
-    const int nu = a.hs.meta[slot].n_uniq;
-    const int g0 = a.voff + p0 * VEC, g1 = a.voff + min(pv1 * VEC, a.vloc);
-    int lo = 0, hi = 0;
-    for (int i = lane; i < nu; i += 32) {
-      const int id = utab[i].id;
-      lo += id < g0;
-      hi += id < g1;
+    const float temp = gprm->temperature;
+    const float tau = (temp < kGreedyEps) ? 1.0f : temp;
+    const float c = __fdiv_rn((float)kLog2e, tau);
+    if (lane == 0) segc[g] = make_float2(c, __fdiv_rn(8.0f, c));
+    const int64_t cfirst = ((int64_t)r * a.spr) / a.span;
+    if (lane < kCW) {
+      PartRec pr;
+      pr.m = -INFINITY;
+      pr.bad = 0u;
+      pr.s = 0.0;
+      a.parts[((int64_t)r * a.rpr + (blockIdx.x - cfirst)) * kCW + lane] = pr;
     }
-    lo = warp_sum_i(lo);
-    hi = warp_sum_i(hi);
-    const int pcount = max(0, hi - lo);
-    const bool staged = pcount <= kPenW;
-    const UniqEntry* psrc = staged ? wpen : utab + lo;
-    if (staged)
-      for (int i = lane; i < pcount; i += 32) wpen[i] = utab[lo + i];
-    __syncwarp();
-    // raw logits of the penalised ids (scattered single elements): issued now, consumed after
-    // the stream, so their latency hides under it
-    float praw[kPenWQ];
-#pragma unroll
-    for (int q = 0; q < kPenWQ; ++q) {
-      const int e = lane + 32 * q;
-      praw[q] = (e < pcount) ? Dec<T>::load1(rowp, psrc[e].id - a.voff) : 0.f;
-    }
-    LaneAcc la;
-    la.reset();
-    int wcur = 0;
-    int next_pen = (pcount > 0) ? psrc[0].id - a.voff : 0x7FFFFFFF;  // row-local element id
-    uint16_t* gk = a.gkeys + (int64_t)r * (a.Vq / kG);
+  }
+  build_bitmap<VEC>(a, s0, 0, min(nspan, kBmMax), bm);  // (begins and ends with a consumer barrier)
 
-    // ================= the stream =================
-    for (int k = 0; k < nsteps; ++k) {
-      const int vb = p0 + k * kStepVec;      // row vector index of the step
-      const int s1 = (vb + kStepVec) * VEC;  // row-local element end of the step
-      uint4 cur[kG];  // this step's vectors (past the row: -inf)
-#pragma unroll
-      for (int j = 0; j < kG; ++j) cur[j] = u[j];
-#pragma unroll
-      for (int j = 0; j < kG; ++j) {
-        const int v = vb + kStepVec + lane + 32 * j;
-        u[j] = (k + 1 < nsteps && v < nvv) ? ldg_stream(rowp + (int64_t)v * 16) : kNegInfVec;
+  int cur = -1;  // row being accumulated
+  LaneSum ls;
+  ls.reset();
+  float c = 0.f, inv8 = 0.f;
+  uint64_t c2 = 0;
+  uint16_t* gkr = nullptr;
+  int pa = 0;  // bitmap phase start (CTA-relative step)
+  auto flush = [&]() {
+    const float m = warp_max(ls.mmax);
+    double sv = (ls.acc != 0.0) ? ls.acc * (double)ex2f((ls.mref - m) * c) : 0.0;
+    sv = warp_sum_d(sv);
+    const int bad = __any_sync(kFull, ls.bad);
+    if (lane == 0) {
+      const int64_t cfirst = ((int64_t)cur * a.spr) / a.span;
+      PartRec pr;
+      pr.m = m;
+      pr.bad = bad ? kRecBad : 0u;
+      pr.s = sv;
+      a.parts[((int64_t)cur * a.rpr + (blockIdx.x - cfirst)) * kCW + w] = pr;
+    }
+  };
+  // this warp's step cursor: CTA-relative step i = 16 t + w  <->  (row r, row step k)
+  int r = (int)((s0 + w) / a.spr), k = (int)(s0 + w - (int64_t)r * a.spr);
+  for (int t = 0; t < ntiles; ++t) {
+    const int i = t * kTileSteps + w;
+    if (t * kTileSteps - pa >= kBmMax) {  // next bitmap phase (uniform over the consumer warps)
+      pa = t * kTileSteps;
+      build_bitmap<VEC>(a, s0, pa, min(nspan, pa + kBmMax), bm);
+    }
+    const int sl = t % kNS;
+    if (i < nspan) {
+      if (r != cur) {
+        if (cur >= 0) flush();
+        cur = r;
+        const float2 cc = segc[r - r_cta0];
+        c = cc.x;
+        inv8 = cc.y;
+        c2 = f2_pack(c, c);
+        ls.reset();
+        gkr = a.gkeys + (int64_t)r * gk_stride(a.Vq);
       }
-      // penalised ids and the padding tail are masked to -inf here (bit j*VEC+t of pm); the
-      // penalised elements enter the sums and the candidates as single exact values instead
-      uint32_t pm = 0;
-      while (next_pen < s1) {
-        const int d = next_pen / VEC - vb;  // vector offset within the step
-        if ((d & 31) == lane) pm |= 1u << ((d >> 5) * VEC + (next_pen & (VEC - 1)));
-        ++wcur;
-        next_pen = (wcur < pcount) ? psrc[wcur].id - a.voff : 0x7FFFFFFF;
-      }
-      if (s1 > a.vloc) {
+      const int vb = k * kStepVec;
+      uint4 cur4[kG];
+      mbar_wait(full + sl, (uint32_t)((t / kNS) & 1));
+      const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
+      uint32_t pm = bm[(i - pa) * 32 + lane];
+      if (vb + kStepVec <= nvv) {
+#pragma unroll
+        for (int j = 0; j < kG; ++j) cur4[j] = tile[lane + 32 * j];
+      } else {  // the row's last (partial) step: past the row -inf, the padding tail masked
+#pragma unroll
+        for (int j = 0; j < kG; ++j) cur4[j] = (vb + lane + 32 * j < nvv) ? tile[lane + 32 * j] : kNegInfVec;
 #pragma unroll
         for (int j = 0; j < kG; ++j)
 #pragma unroll
-          for (int t = 0; t < VEC; ++t)
-            if ((vb + lane + 32 * j) * VEC + t >= a.vloc) pm |= 1u << (j * VEC + t);
+          for (int tt = 0; tt < VEC; ++tt)
+            if ((vb + lane + 32 * j) * VEC + tt >= a.vloc) pm |= 1u << (j * VEC + tt);
       }
-      if (pm) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + sl);  // this warp's part of the slot is consumed
+      if (pm && !(a.dbg & 4)) {
 #pragma unroll
         for (int j = 0; j < kG; ++j) {
           const uint32_t b = (pm >> (j * VEC)) & ((1u << VEC) - 1u);
-          if (b) cur[j] = Dec<T>::mask(cur[j], b);
+          if (b) cur4[j] = Dec<T>::mask(cur4[j], b);
         }
       }
-      float vm[kG];
-#pragma unroll
-      for (int j = 0; j < kG; ++j) vm[j] = Dec<T>::vmax(cur[j]);
-      const float gm = fmax_nan(fmax_nan(vm[0], vm[1]), fmax_nan(vm[2], vm[3]));
-      la.bad |= !(gm < INFINITY) ? 1 : 0;  // NaN or +inf in the group
-      gk[vb / kG + lane] = (uint16_t)key16_down(gm);
-      const float gmax = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
-      if (gmax > -INFINITY) {
-        if (gmax > la.thr) lane_rebase(la, gmax, rc);
-        float sj[kG];
-#pragma unroll
-        for (int j = 0; j < kG; ++j) {
-          float e[VEC];
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) e[i] = lane_exp(Dec<T>::elem(cur[j], i), la, rc);
-#pragma unroll
-          for (int st = 1; st < VEC; st <<= 1)
-#pragma unroll
-            for (int i = 0; i < VEC; i += 2 * st) e[i] += e[i + st];
-          sj[j] = e[0];
-        }
-        la.acc += (double)((sj[0] + sj[1]) + (sj[2] + sj[3]));
-        la.mmax = fmaxf(la.mmax, gmax);
+      // the exp-sum is taken against the current reference speculatively (independent of the
+      // max tree, so the two chains overlap); a group that needs a new reference (rare) redoes it
+      float es = (a.dbg & 1) ? __uint_as_float(cur4[0].x ^ cur4[1].y ^ cur4[2].z ^ cur4[3].w) : GroupMath<T>::esum(cur4, ls.nm, c2);
+      const float gm = GroupMath<T>::gmax(cur4);
+      ls.bad |= !(gm < INFINITY) ? 1 : 0;  // NaN or +inf in the group
+      if (!(a.dbg & 2)) {
+        const uint32_t key = key16_down(gm);
+        gkr[k * 32 + lane] = (uint16_t)key;
+        const uint32_t skey = __reduce_max_sync(kFull, key);
+        if (lane == 0) gkr[a.Vq / kG + k] = (uint16_t)skey;
       }
-    }
-    // penalised elements: exact values (OPENAI_CTRL / LINEAR) into the lane sums
-    // and maxima
-    if (pcount > 0) {
-      const sampling_params prm = *gprm;
-      for (int q = 0; lane + 32 * q < pcount; ++q) {
-        const int e = lane + 32 * q;
-        const UniqEntry ue = psrc[e];
-        float raw = 0.f;
-#pragma unroll
-        for (int qq = 0; qq < kPenWQ; ++qq)
-          if (qq == q) raw = praw[qq];
-        if (q >= kPenWQ) raw = Dec<T>::load1(rowp, ue.id - a.voff);
-        la.bad |= !(raw < INFINITY) ? 1 : 0;
-        const float zp = apply_penalty(raw, ue.meta, prm, a.pen_mode);
-        la.bad |= !(zp < INFINITY) ? 1 : 0;
-        if (zp > -INFINITY && zp < INFINITY) {
-          if (zp > la.thr) lane_rebase(la, zp, rc);
-          la.acc += (double)lane_exp(zp, la, rc);
-          la.mmax = fmaxf(la.mmax, zp);
+      if (gm > -INFINITY) {
+        if (gm > ls.thr) {
+          ls.rebase(gm, c, inv8);
+          if (!(a.dbg & 1)) es = GroupMath<T>::esum(cur4, ls.nm, c2);
         }
+        ls.acc += (double)es;
+        ls.mmax = fmaxf(ls.mmax, gm);
       }
+    } else if (lane == 0) {
+      mbar_arrive(empty + sl);
     }
-    // ================= epilogue: the warp record =================
-    uint32_t x = (la.mmax > -INFINITY) ? f2key(la.mmax) : 0u;  // 0 = no finite element
-    x = warp_sort_desc_u32(x, lane);
-    const float m = warp_max(la.mmax);
-    const float Rl = warp_max(la.acc != 0.0 ? la.R : -INFINITY);
-    double sv = (la.acc != 0.0) ? scale_pow2(la.acc, la.R - Rl) : 0.0;
-    sv = warp_sum_d(sv);
-    const int bad = __any_sync(kFull, la.bad);
-    const int cnt = __popc(__ballot_sync(kFull, x != 0u));
-    uint8_t* rec = a.records + (gw + r) * (int64_t)kWarpRecStride;
-    reinterpret_cast<uint32_t*>(rec + kRecHdrBytes)[lane] = x;
-    if (lane == 0) {
-      RecHdr h;
-      h.m = m;
-      h.flags = bad ? kRecBad : 0u;
-      h.s = sv;
-      h.R = (double)Rl;
-      h.n = (uint32_t)cnt;
-      h.rsv = 0;
-      h.frontier = 0;
-      *reinterpret_cast<RecHdr*>(rec) = h;
+    k += kTileSteps;
+    while (k >= a.spr) {
+      k -= a.spr;
+      ++r;
     }
-    __syncwarp();  // the staged entries are rewritten by the next sub-piece
-    pos = pend;
   }
-  if (a.trace && lane == 0) a.trace[gw * 8 + 7] = gtimer();
+  if (cur >= 0) flush();
+  if (a.trace && tid == 0) a.trace[blockIdx.x * 64 + 7] = gtimer();
 }
 
 }  // namespace smp

@@ -121,6 +121,82 @@ __global__ void __launch_bounds__(256) ldg_kernel(const uint8_t* x, int64_t nbyt
   if ((threadIdx.x & 31) == 0) atomicAdd(out + blockIdx.x, acc);
 }
 
+
+// generic: CW consumer warps, ST stages of TBB bytes; consumer warp w reads its TBB/CW slice
+template <int CW, int ST2, int TBB>
+__global__ void __launch_bounds__((CW + 1) * 32, 1) tma_gen(const uint8_t* x, int64_t nbytes, float* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST2 * TBB);
+  uint64_t* empty = full + ST2;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (nbytes / gridDim.x) / TBB * TBB;
+  const int64_t b0 = blockIdx.x * per, b1 = (blockIdx.x == gridDim.x - 1) ? nbytes : b0 + per;
+  const int ntiles = (int)((b1 - b0 + TBB - 1) / TBB);
+  if (tid == 0) {
+    for (int s = 0; s < ST2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (wid == CW) {
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      for (int it = 0; it < ntiles; ++it) {
+        const int s = it % ST2;
+        if (it >= ST2) mbar_wait(&empty[s], (uint32_t)(((it / ST2) - 1) & 1));
+        const int64_t o = b0 + (int64_t)it * TBB;
+        const uint32_t len = (uint32_t)min((int64_t)TBB, b1 - o);
+        mbar_arrive_expect_tx(&full[s], len);
+        bulk_g2s(smem + s * TBB, x + o, len, &full[s], pol);
+      }
+    }
+    return;
+  }
+  float acc = 0.f;
+  constexpr int VPW = TBB / 16 / CW / 32;  // vectors per lane per tile
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % ST2;
+    mbar_wait(&full[s], (uint32_t)((it / ST2) & 1));
+    const uint4* t = reinterpret_cast<const uint4*>(smem + s * TBB);
+    uint4 u[VPW];
+#pragma unroll
+    for (int j = 0; j < VPW; ++j) u[j] = t[wid * (VPW * 32) + j * 32 + lane];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+    for (int j = 0; j < VPW; ++j) acc += __uint_as_float(u[j].x ^ u[j].y ^ u[j].z ^ u[j].w);
+  }
+  acc = warp_sum_d(acc);
+  if (lane == 0) atomicAdd(out + blockIdx.x, acc);
+}
+
+template <int CW, int ST2, int TBB>
+static void run_gen(const void* x, int64_t nbytes, float* out, int grid, cudaStream_t st) {
+  const int smem = ST2 * TBB + 2 * ST2 * 8;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(tma_gen<CW, ST2, TBB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  tma_gen<CW, ST2, TBB><<<grid, (CW + 1) * 32, smem, st>>>((const uint8_t*)x, nbytes, out);
+}
+
+extern "C" int ub_gen(int cfg, const void* x, int64_t nbytes, float* out, int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (cfg) {
+    case 0: run_gen<16, 4, 32768>(x, nbytes, out, grid, st); break;   // = stream_kernel geometry
+    case 1: run_gen<16, 6, 32768>(x, nbytes, out, grid, st); break;
+    case 2: run_gen<8, 4, 16384>(x, nbytes, out, grid, st); break;    // = tma_kernel geometry
+    case 3: run_gen<8, 8, 16384>(x, nbytes, out, grid, st); break;
+    case 4: run_gen<16, 3, 65536>(x, nbytes, out, grid, st); break;
+    case 5: run_gen<4, 8, 8192>(x, nbytes, out, grid, st); break;
+    default: return -1;
+  }
+  return (int)cudaGetLastError();
+}
+
 extern "C" int ub_run(int kind, int mode, const void* x, int64_t nbytes, float* out, int grid, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = ST * TB + 2 * ST * 8;

@@ -43,6 +43,20 @@ def main():
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / iters * 1000
                 res[f"{'tma' if kind == 0 else 'ldg'}_m{mode}_g{grid}"] = (round(us, 2), round(n * 2 / us / 1e3, 1))
+    lib.ub_gen.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    for cfg, grids in ((0, (148,)), (1, (148,)), (2, (148, 296)), (3, (148, 296)), (4, (148,)), (5, (296, 592, 888))):
+        for grid in grids:
+            for i in range(5):
+                lib.ub_gen(cfg, xs[i].data_ptr(), n * 2, out.data_ptr(), grid, st)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(50):
+                lib.ub_gen(cfg, xs[i % 5].data_ptr(), n * 2, out.data_ptr(), grid, st)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / 50 * 1000
+            res[f"gen{cfg}_g{grid}"] = (round(us, 2), round(n * 2 / us / 1e3, 1))
     print(json.dumps(res))
 
 
