@@ -28,29 +28,36 @@ struct RowOut {
   RowInfo* info;     // per-row hand-off / debug
 };
 
-// Per-slot history state.  offs[slot][b] = number of unique-table entries with
-// id < voff + min(kOffsBucket * b, vloc), b = 0..nb (nb = ceil(vloc / kOffsBucket)): the
-// table position of any STEP-aligned vocabulary boundary in O(1) (phase A's penalty ranges).
-constexpr int kOffsBucket = 512;
+// Per-slot history state.  pmask[slot] is the slot's penalty presence bitmap (the set of ids in
+// prompt u output — the support of the paper's penalty buffers f, kept as bits and
+// updated incrementally on append) in phase A's step-lane order: local element le, v = le / vec,
+// step k = v / 128, d = v % 128  ->  word k * 32 + (d % 32), bit (d / 32) * vec + le % vec.
+// Phase A bulk-copies the words of each tile next to the logits and masks those elements.
 struct HistState {
   SlotMeta* meta;
   UniqEntry* uniq;
   int32_t* tokens;
   int L;
-  int32_t* offs;  // [max_batch][nb + 1]
-  int nb;
+  uint32_t* pmask;  // [max_batch][spr * 32]
+  int spr;          // steps per row of the local slice
+  int vec;          // elements per 16-byte vector (8 bf16 / 4 f32)
   int voff, vloc;
 };
-__host__ __device__ inline int offs_nb(int vloc) { return (vloc + kOffsBucket - 1) / kOffsBucket; }
 
-// a new unique id `tok` entered the table: every boundary above it moves up by one
-__device__ __forceinline__ void offs_bump(const HistState& hs, int slot, int32_t tok, int tid, int nthr) {
-  int b0;
-  if (tok < hs.voff) b0 = 0;
-  else if (tok - hs.voff < hs.vloc) b0 = (tok - hs.voff) / kOffsBucket + 1;
-  else return;
-  int32_t* o = hs.offs + (int64_t)slot * (hs.nb + 1);
-  for (int b = b0 + tid; b <= hs.nb; b += nthr) o[b] += 1;
+__host__ __device__ inline void pmask_pos(int le, int vec, int* word, uint32_t* bit) {
+  const int v = le / vec, k = v / 128, d = v % 128;
+  *word = k * 32 + (d & 31);
+  *bit = 1u << ((d >> 5) * vec + le % vec);
+}
+
+// a token entered the slot's history: its presence bit (idempotent)
+__device__ __forceinline__ void pmask_set(const HistState& hs, int slot, int32_t tok) {
+  const int le = tok - hs.voff;
+  if (le < 0 || le >= hs.vloc) return;
+  int w;
+  uint32_t b;
+  pmask_pos(le, hs.vec, &w, &b);
+  atomicOr(hs.pmask + (int64_t)slot * hs.spr * 32 + w, b);
 }
 
 struct MergeSmem {
@@ -97,7 +104,7 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
       e.meta = 2u;
       u[less] = e;
     }
-    offs_bump(hs, slot, tok, lane, 32);
+    if (lane == 0) pmask_set(hs, slot, tok);
   }
   if (lane == 0) {
     hs.tokens[(int64_t)slot * hs.L + np + no] = tok;

@@ -40,8 +40,10 @@ struct sampler {
   int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
   float* d_scratch = nullptr;
-  int32_t* d_offs = nullptr;    // [max_batch][nb + 1] unique-table bucket offsets (HistState)
+  uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
   PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
+  RowHand* d_hand = nullptr;    // [max_batch] phase A -> B hand-off
+  PenEnt* d_pent = nullptr;     // [max_batch][max_history] penalised entries (hand-off)
   uint16_t* d_gkeys = nullptr;  // [max_batch][Vq/4] group keys (phase A -> phase B)
   uint64_t* d_trace = nullptr;
   int dbg = 0;                  // SAMPLER_DBG development switches (stream.cuh)  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
@@ -68,8 +70,9 @@ static HistState hist_state(const sampler* h) {
   s.uniq = h->d_uniq;
   s.tokens = h->d_hist;
   s.L = h->cfg.max_history;
-  s.offs = h->d_offs;
-  s.nb = offs_nb(h->cfg.vocab_local);
+  s.pmask = h->d_pmask;
+  s.spr = (int)(h->Vq / kStepVec);
+  s.vec = h->vec;
   s.voff = h->cfg.vocab_offset;
   s.vloc = h->cfg.vocab_local;
   return s;
@@ -192,7 +195,8 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
             al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
             al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
             al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
-            al((void**)&h->d_offs, sizeof(int32_t) * B * (offs_nb(c.vocab_local) + 1)) &&
+            al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&
+            al((void**)&h->d_hand, sizeof(RowHand) * B) && al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
             al((void**)&h->d_parts, sizeof(PartRec) * B * kCW * ((h->Vq / kStepVec + kTileSteps - 1) / kTileSteps + 1));
   if (!ok) {
     cudaGetLastError();
@@ -217,7 +221,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   if (cudaMemcpy(h->d_params, h->h_params.data(), sizeof(sampling_params) * B, cudaMemcpyHostToDevice) !=
           cudaSuccess ||
       cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
-      cudaMemset(h->d_offs, 0, sizeof(int32_t) * B * (offs_nb(c.vocab_local) + 1)) != cudaSuccess ||
+      cudaMemset(h->d_pmask, 0, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) != cudaSuccess ||
       cudaMemset(h->d_tickets, 0, sizeof(int32_t) * B) != cudaSuccess ||
       cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
       cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -258,8 +262,10 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_scratch);
   cudaFree(h->d_trace);
   cudaFree(h->d_gkeys);
-  cudaFree(h->d_offs);
+  cudaFree(h->d_pmask);
   cudaFree(h->d_parts);
+  cudaFree(h->d_hand);
+  cudaFree(h->d_pent);
   for (auto& e : h->tev)
     if (e) cudaEventDestroy(e);
   delete h;
@@ -308,17 +314,18 @@ static int upload_slot(sampler* h, int slot, const std::vector<int32_t>& prompt,
     CK(h, cudaMemcpy(h->d_uniq + (int64_t)slot * L, u.data(), sizeof(UniqEntry) * u.size(), cudaMemcpyHostToDevice));
   if (!toks.empty())
     CK(h, cudaMemcpy(h->d_hist + (int64_t)slot * L, toks.data(), sizeof(int32_t) * toks.size(), cudaMemcpyHostToDevice));
-  // bucket offsets of the sorted unique table (HistState::offs)
-  const int nb = offs_nb(h->cfg.vocab_local);
-  std::vector<int32_t> offs(nb + 1);
-  size_t j = 0;
-  for (int b = 0; b <= nb; ++b) {
-    const int64_t bound = (int64_t)h->cfg.vocab_offset + std::min<int64_t>((int64_t)kOffsBucket * b, h->cfg.vocab_local);
-    while (j < u.size() && u[j].id < bound) ++j;
-    offs[b] = (int32_t)j;
+  // penalty presence bitmap of the slot (HistState::pmask)
+  const int64_t nw = (h->Vq / kStepVec) * 32;
+  std::vector<uint32_t> pm(nw, 0u);
+  for (const UniqEntry& e : u) {
+    const int le = e.id - h->cfg.vocab_offset;
+    if (le < 0 || le >= h->cfg.vocab_local) continue;
+    int w;
+    uint32_t b;
+    pmask_pos(le, h->vec, &w, &b);
+    pm[w] |= b;
   }
-  CK(h, cudaMemcpy(h->d_offs + (int64_t)slot * (nb + 1), offs.data(), sizeof(int32_t) * (nb + 1),
-                   cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(h->d_pmask + (int64_t)slot * nw, pm.data(), sizeof(uint32_t) * nw, cudaMemcpyHostToDevice));
   CK(h, cudaMemcpy(h->d_meta + slot, &sm, sizeof(SlotMeta), cudaMemcpyHostToDevice));
   return SAMPLER_OK;
 }
@@ -467,8 +474,11 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.slots = slots;
   a.params_dev = params_dev;
   a.params_tab = h->d_params;
+  a.pen_mode = h->cfg.penalty_mode;
   a.hs = hist_state(h);
   a.parts = h->d_parts;
+  a.hand = h->d_hand;
+  a.pent = h->d_pent;
   a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
   a.dbg = h->dbg;
@@ -512,6 +522,8 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.pending_ok = 1;
   s.hs = hist_state(h);
   s.parts = h->d_parts;
+  s.hand = h->d_hand;
+  s.pent = h->d_pent;
   s.gkeys = h->d_gkeys;
   s.ro = ro;
   s.out_records = nullptr;

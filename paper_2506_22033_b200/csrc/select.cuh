@@ -45,6 +45,8 @@ struct SelectArgs {
   int kcand, pen_mode, mode, append, pending_ok;
   HistState hs;
   const PartRec* parts;    // phase A partial records [B][rpr][kCW]
+  const RowHand* hand;     // phase A hand-off [B]
+  const PenEnt* pent;      // [B][L]
   const uint16_t* gkeys;
   RowOut ro;
   uint8_t* out_records;  // mode 1: one candidate record per row
@@ -66,7 +68,9 @@ constexpr int kSOffScr = kSOffHdr + kMaxRecW * 48;                 // f[8] d[8] 
 constexpr int kSOffCtl = kSOffScr + 288;                           // ints [16]
 constexpr int kSOffGk = kSOffCtl + 64;                             // [kSelGR * kBT] uint4 group keys
 constexpr int kSOffSk = kSOffGk + kSelGR * kBT * 16;               // [kBT] u16 step keys
-constexpr int kSelectSmem = kSOffSk + kBT * 2;
+constexpr int kSOffHand = kSOffSk + kBT * 2;                        // RowHand
+constexpr int kSOffZp = kSOffHand + (int)sizeof(RowHand);          // [kSelPen] float penalised values
+constexpr int kSelectSmem = kSOffZp + kSelPen * 4;
 
 
 // Append `tok` to the slot's history (P:371 incremental update) from the smem copy of the sorted
@@ -96,7 +100,7 @@ __device__ __forceinline__ void block_append_smem(const HistState& hs, int slot,
       e.meta = 2u;
       u[less] = e;
     }
-    offs_bump(hs, slot, tok, tid, kBT);
+    if (tid == 0) pmask_set(hs, slot, tok);
   }
   if (tid == 0) {
     hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
@@ -209,46 +213,38 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   } while (0)
   STR(0);
 
-  // ---- prologue: nothing here depends on phase A
-  const int slot = a.slots ? a.slots[r] : r;
-  const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
-  const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
-  const RowCfg rc = decode_row(prm, a.V, a.kcand);
-  const int keff = rc.keff;
-  const SlotMeta smeta = a.hs.meta[slot];
-  const int nu = smeta.n_uniq;
-  const int nus = min(nu, kSelPen);
-  const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
-  const uint8_t* rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
-  float raw[kSelPR];
-  int lid[kSelPR];
-#pragma unroll
-  for (int q = 0; q < kSelPR; ++q) {
-    const int e = tid + q * kBT;
-    lid[q] = -1;
-    raw[q] = 0.f;
-    if (e < nus) {
-      const UniqEntry ue = utab[e];
-      s_ue[e] = ue;
-      const int l = ue.id - a.voff;
-      if (l >= 0 && l < a.vloc) {
-        lid[q] = l;
-        raw[q] = Dec<T>::load1(rowp, l);
-      }
-    }
-  }
   if (tid == 0) {
     ctl[0] = 0;
     ctl[1] = 0;
     ctl[2] = 0;
     ctl[5] = 0;
   }
-  // exact penalised values (binary32 ops), NaN for "not in this slice"
+  griddep_wait();  // phase A's hand-off, partial records and keys are visible from here on
+  // ---- RT1 (one round trip, nothing indexed by slot): the hand-off, the penalised entries, the
+  // partial records, the step keys and the group keys of row r
+  RowHand* s_hand = reinterpret_cast<RowHand*>(smem + kSOffHand);
+  if (tid < (int)(sizeof(RowHand) / 16))
+    reinterpret_cast<uint4*>(s_hand)[tid] = reinterpret_cast<const uint4*>(a.hand + r)[tid];
+  const int ncap = min(a.hs.L, kSelPen);  // entries loaded speculatively (nu is in the hand-off)
+  float* s_zp = reinterpret_cast<float*>(smem + kSOffZp);
+  {
+    uint4 x[kSelPR];  // every load in flight before the first use
+    const uint4* src = reinterpret_cast<const uint4*>(a.pent + (int64_t)r * a.hs.L);
 #pragma unroll
-  for (int q = 0; q < kSelPR; ++q)
-    raw[q] = (lid[q] >= 0) ? apply_penalty(raw[q], s_ue[tid + q * kBT].meta, prm, a.pen_mode) : NAN;
-  griddep_wait();  // phase A's records and group keys are visible from here on
-  // ---- RT1: the row's partial records, step keys and group keys (one round trip)
+    for (int q = 0; q < kSelPR; ++q)
+      if (tid + q * kBT < ncap) x[q] = src[tid + q * kBT];
+#pragma unroll
+    for (int q = 0; q < kSelPR; ++q) {
+      const int e = tid + q * kBT;
+      if (e < ncap) {
+        UniqEntry ue;
+        ue.id = (int32_t)x[q].x;
+        ue.meta = x[q].y;
+        s_ue[e] = ue;
+        s_zp[e] = __uint_as_float(x[q].z);
+      }
+    }
+  }
   const int64_t cfirst = ((int64_t)r * a.spr) / a.span;
   const int64_t clast = ((int64_t)(r + 1) * a.spr - 1) / a.span;
   const int nparts = (int)(clast - cfirst + 1) * kCW;
@@ -272,6 +268,35 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     s_gk[w] = (w < gwords) ? gk4[w] : make_uint4(0, 0, 0, 0);
   }
   for (int i = tid; i < kHistBins; i += kBT) hist[i] = 0u;
+  cbar();
+  const int slot = s_hand->slot;
+  const sampling_params prm = a.params_dev ? a.params_dev[r] : s_hand->prm;
+  const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
+  const RowCfg rc = decode_row(prm, a.V, a.kcand);
+  const int keff = rc.keff;
+  const SlotMeta smeta = s_hand->meta;
+  const int nu = smeta.n_uniq;
+  const int nus = min(nu, kSelPen);
+  const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
+  const uint8_t* rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
+  // the penalised entries: smem copy of the table (id order) for masking and the append, exact
+  // penalised values in registers (raw[q]; lid[q] < 0: not in this vocabulary slice)
+  float raw[kSelPR];
+  int lid[kSelPR];
+#pragma unroll
+  for (int q = 0; q < kSelPR; ++q) {
+    const int e = tid + q * kBT;
+    lid[q] = -1;
+    raw[q] = NAN;
+    if (e < nus) {
+      const int l = s_ue[e].id - a.voff;
+      if (l >= 0 && l < a.vloc) {
+        lid[q] = l;
+        raw[q] = s_zp[e];
+      }
+    }
+  }
+  STR(1);
   // ---- M = max of the stream partials and the exact penalised values;
   //      S = sum_parts s 2^((m - M) c) + sum_pen 2^((z' - M) c)   (fixed order: deterministic)
   float mloc = p0.m;
@@ -295,9 +320,28 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     if (!(zp < INFINITY)) fl |= kRecBad;
     else mloc = fmaxf(mloc, zp);
   }
-  const float M = block_max_f(mloc, ms.bs);
-  const bool bad = block_or_i((int)(fl & kRecBad), ms.bs) != 0;
-  STR(1);
+  // one barrier for max and flags together
+  {
+    const int w = tid >> 5;
+    float mw = warp_max(mloc);
+    const unsigned fw = __reduce_or_sync(kFull, fl);
+    if (lane == 0) {
+      ms.bs.f[w] = mw;
+      ms.bs.i[w] = (int)fw;
+    }
+    cbar();
+    mw = ms.bs.f[0];
+    unsigned fa = (unsigned)ms.bs.i[0];
+#pragma unroll
+    for (int j = 1; j < kBW; ++j) {
+      mw = fmaxf(mw, ms.bs.f[j]);
+      fa |= (unsigned)ms.bs.i[j];
+    }
+    mloc = mw;
+    fl = fa;
+  }
+  const float M = mloc;
+  const bool bad = (fl & kRecBad) != 0;
   double term = 0.0;
   if (M > -INFINITY && !bad) {
     if (p0.s != 0.0) term += p0.s * exp2(((double)p0.m - (double)M) * rc.c_d);

@@ -4,10 +4,11 @@
 // 128 16-byte vectors = 2 KB of one row) is cut into equal contiguous CTA spans:
 //   * producer warp: one 1-D bulk copy (cp.async.bulk, TMA engine, L2 evict-first) per step into a
 //     ring of kNS tiles of 16 steps (32 KB each), full / empty mbarriers;
-//   * 16 consumer warps: warp w takes step w of every tile (4 vectors = 32 bf16 / 16 f32 logits per
-//     lane); the row's penalised ids (the slot's incremental unique-token table, located in
-//     O(1) by its bucket offsets) are a CTA-wide smem bitmap built once per bitmap phase, and
-//     masked to -inf in registers with the padding tail; then per lane and step (a "group"):
+//     next to each run of logits, the same steps' words of the slot's penalty presence bitmap
+//     (HistState::pmask — the support of the paper's incremental penalty buffers);
+//   * 24 consumer warps: warp w takes step w of every tile (4 vectors = 32 bf16 / 16 f32 logits per
+//     lane); penalised ids and the padding tail are masked to -inf in registers (the penalised
+//     elements enter phase B as exact single values); then per lane and step (a "group"):
 //       - the group max by a NaN-propagating packed max tree (bf16x2 HMNMX2), its order-preserving
 //         16-bit key stored to gkeys[row][group] (phase B selects the top-k from these keys);
 //       - the exp-sum of P:149's softmax denominator, sum 2^((z - m_ref) * log2(e)/tau):
@@ -30,16 +31,32 @@ namespace smp {
 // ---- geometry of phase A (persistent CTAs, warp-specialised) ----------------------
 constexpr int kCW = 24;                    // consumer warps per CTA (one step of each tile each)
 constexpr int kTileSteps = kCW;            // steps per ring tile (24 x 2 KB = 48 KB)
-constexpr int kNS = 3;                     // ring tiles (144 KB of bulk copies in flight per SM)
-constexpr int kBmMax = 384;                // steps covered by one penalty-bitmap phase
+constexpr int kNS = 4;                     // ring tiles (192 KB of bulk copies in flight per SM)
 constexpr int kMaxSeg = 48;                // rows per CTA span (the host caps the span)
-constexpr int kStreamThreads = (kCW + 1) * 32;  // + one producer warp
+constexpr int kStreamThreads = (kCW + 2) * 32;  // + producer warp + penalty warp
 constexpr int kStepBytes = kStepVec * 16;
 constexpr int kSOffRing = 0;
-constexpr int kSOffBm = kSOffRing + kNS * kTileSteps * kStepBytes;
-constexpr int kSOffBar = kSOffBm + kBmMax * 32 * 4;
+constexpr int kSOffBm = kSOffRing + kNS * kTileSteps * kStepBytes;  // [kNS][kTileSteps][32] u32
+constexpr int kSOffBar = kSOffBm + kNS * kTileSteps * 128;
 constexpr int kSOffSeg = kSOffBar + 2 * kNS * 8;
 constexpr int kStreamSmem = kSOffSeg + kMaxSeg * 8;
+
+// Phase A -> phase B hand-off of one batch row, written by the CTA that holds the row's first step
+// (its penalty warp), so that phase B starts with one round trip and no slot indirection:
+// the slot, its history meta, the row's params and, per unique history entry (id order), the
+// exact penalised logit z' (R1-R3).
+struct __align__(16) RowHand {
+  int32_t slot;
+  int32_t pad[3];
+  SlotMeta meta;
+  sampling_params prm;
+};
+struct __align__(16) PenEnt {
+  int32_t id;
+  uint32_t meta;  // (count in output << 1) | in prompt
+  float zp;       // penalised logit (only for ids inside the local slice)
+  int32_t pad;
+};
 
 // one consumer warp's partial reduction of one row: max m and s = sum 2^((z - m) log2(e)/tau)
 struct __align__(16) PartRec {
@@ -62,8 +79,11 @@ struct StreamArgs {
   const int32_t* slots;
   const sampling_params* params_dev;  // nullable
   const sampling_params* params_tab;
+  int pen_mode;
   HistState hs;
   PartRec* parts;      // [B][rpr][kCW]
+  RowHand* hand;       // [B]
+  PenEnt* pent;        // [B][L]
   uint16_t* gkeys;     // [B][gk_stride(Vq)]: group keys | step keys
   uint64_t* trace;     // debug: per-CTA start / end timestamps (globaltimer ns, 64 per CTA), nullable
   int dbg;             // development switches (SAMPLER_DBG): bit0 no exp-sum, bit1 no keys, bit2 no mask
@@ -195,36 +215,6 @@ struct LaneSum {
   }
 };
 
-// Consumer-side prologue of one bitmap phase: CTA-relative steps [pa, pb) of the span that
-// starts at global step s0.  bm word (i - pa, lane), bit j*VEC + t <=> element t of vector
-// 128 k + lane + 32 j (k = the step's index in its row) is penalised: those elements are masked
-// to -inf in the stream (phase B applies their exact penalised values).
-template <int VEC>
-__device__ __forceinline__ void build_bitmap(const StreamArgs& a, int64_t s0, int pa, int pb, uint32_t* bm) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int i = tid; i < kBmMax * 32; i += kCW * 32) bm[i] = 0u;
-  cbar_n<kCW * 32>();
-  const int nvv = (a.vloc + VEC - 1) / VEC;
-  const int rA = (int)((s0 + pa) / a.spr), rB = (int)((s0 + pb - 1) / a.spr);
-  for (int r = rA + w; r <= rB; r += kCW) {
-    const int slot = a.slots ? a.slots[r] : r;
-    const int64_t rs = (int64_t)r * a.spr;
-    const int k0 = (int)(max(rs, s0 + pa) - rs), k1 = (int)(min(rs + a.spr, s0 + pb) - rs);  // row steps
-    const int32_t* offs = a.hs.offs + (int64_t)slot * (a.hs.nb + 1);
-    const int lo = offs[k0 * kStepVec * VEC / kOffsBucket];
-    const int hi = offs[(k1 * kStepVec >= nvv) ? a.hs.nb : k1 * kStepVec * VEC / kOffsBucket];
-    const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
-    const int ibase = (int)(rs - s0) - pa;  // bitmap step index of row step 0
-    for (int e = lo + lane; e < hi; e += 32) {
-      const int le = ut[e].id - a.voff;
-      const int v = le / VEC;
-      const int k = v / kStepVec, d = v - k * kStepVec;
-      atomicOr(&bm[(ibase + k) * 32 + (d & 31)], 1u << ((d >> 5) * VEC + (le & (VEC - 1))));
-    }
-  }
-  cbar_n<kCW * 32>();
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamArgs a) {
   constexpr int VEC = Dec<T>::N;
@@ -260,6 +250,56 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
   }
   __syncthreads();
 
+  if (w == kCW + 1) {
+    // ================= penalty warp: the hand-off of the rows that start in this span =================
+    const int64_t rfirst = (s0 + a.spr - 1) / a.spr;
+    for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
+      const int slot = a.slots ? a.slots[r] : (int)r;
+      const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
+      const SlotMeta sm = a.hs.meta[slot];
+      if (lane == 0) {
+        RowHand h;
+        h.slot = slot;
+        h.pad[0] = h.pad[1] = h.pad[2] = 0;
+        h.meta = sm;
+        h.prm = prm;
+        a.hand[r] = h;
+      }
+      const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
+      const uint8_t* rowp = lg + r * ldb;
+      // batches of 16 entries per lane: every table load, then every logit gather, in flight at once
+      constexpr int PB = 16;
+      for (int e0 = 0; e0 < sm.n_uniq; e0 += 32 * PB) {
+        UniqEntry ue[PB];
+        float raw[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          const int e = e0 + lane + 32 * q;
+          if (e < sm.n_uniq) ue[q] = ut[e];
+          else ue[q].id = -1;
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          const int le = ue[q].id - a.voff;
+          raw[q] = (ue[q].id >= 0 && le >= 0 && le < a.vloc) ? Dec<T>::load1(rowp, le) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          const int e = e0 + lane + 32 * q;
+          if (e >= sm.n_uniq) continue;
+          const int le = ue[q].id - a.voff;
+          PenEnt pe;
+          pe.id = ue[q].id;
+          pe.meta = ue[q].meta;
+          pe.zp = (le >= 0 && le < a.vloc) ? apply_penalty(raw[q], ue[q].meta, prm, a.pen_mode) : 0.f;
+          pe.pad = 0;
+            a.pent[r * a.hs.L + e] = pe;
+        }
+      }
+    }
+    if (a.trace && lane == 0) a.trace[blockIdx.x * 64 + 8] = gtimer();
+    return;
+  }
   if (w == kCW) {
     // ================= producer warp: 1-D bulk copies (TMA engine), one per step =================
     if (lane == 0) {
@@ -277,8 +317,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
             if (++kk == a.spr) { kk = 0; ++rr; }
           }
         }
-        mbar_arrive_expect_tx(full + sl, bytes);
+        mbar_arrive_expect_tx(full + sl, bytes + (uint32_t)n * 128u);
         uint8_t* dst = ring + sl * (kTileSteps * kStepBytes);
+        uint8_t* bdst = reinterpret_cast<uint8_t*>(bm) + sl * (kTileSteps * 128);
         // one bulk copy per run of consecutive steps of one row (contiguous in global memory)
         for (int j = 0; j < n;) {
           const int j0 = j, k0 = k;
@@ -289,6 +330,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
             ++k;
           } while (j < n && k < a.spr);
           bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
+          // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
+          const int slot = a.slots ? a.slots[r] : r;
+          bulk_g2s(bdst + j0 * 128, a.hs.pmask + ((int64_t)slot * a.spr + k0) * 32, (uint32_t)(j - j0) * 128u,
+                   full + sl, pol);
           if (k == a.spr) { k = 0; ++r; }
         }
       }
@@ -317,7 +362,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
       a.parts[((int64_t)r * a.rpr + (blockIdx.x - cfirst)) * kCW + lane] = pr;
     }
   }
-  build_bitmap<VEC>(a, s0, 0, min(nspan, kBmMax), bm);  // (begins and ends with a consumer barrier)
+  cbar_n<kCW * 32>();  // the span's row constants are in smem
 
   int cur = -1;  // row being accumulated
   LaneSum ls;
@@ -325,7 +370,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
   float c = 0.f, inv8 = 0.f;
   uint64_t c2 = 0;
   uint16_t* gkr = nullptr;
-  int pa = 0;  // bitmap phase start (CTA-relative step)
   auto flush = [&]() {
     const float m = warp_max(ls.mmax);
     double sv = (ls.acc != 0.0) ? ls.acc * (double)ex2f((ls.mref - m) * c) : 0.0;
@@ -344,10 +388,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
   int r = (int)((s0 + w) / a.spr), k = (int)(s0 + w - (int64_t)r * a.spr);
   for (int t = 0; t < ntiles; ++t) {
     const int i = t * kTileSteps + w;
-    if (t * kTileSteps - pa >= kBmMax) {  // next bitmap phase (uniform over the consumer warps)
-      pa = t * kTileSteps;
-      build_bitmap<VEC>(a, s0, pa, min(nspan, pa + kBmMax), bm);
-    }
     const int sl = t % kNS;
     if (i < nspan) {
       if (r != cur) {
@@ -364,7 +404,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
       uint4 cur4[kG];
       mbar_wait(full + sl, (uint32_t)((t / kNS) & 1));
       const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
-      uint32_t pm = bm[(i - pa) * 32 + lane];
+      uint32_t pm = bm[(sl * kTileSteps + w) * 32 + lane];
       if (vb + kStepVec <= nvv) {
 #pragma unroll
         for (int j = 0; j < kG; ++j) cur4[j] = tile[lane + 32 * j];
@@ -379,6 +419,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + sl);  // this warp's part of the slot is consumed
+      if (a.dbg & 8) {  // (development: the pipeline skeleton only)
+        ls.acc += (double)__uint_as_float(cur4[0].x ^ cur4[1].y ^ cur4[2].z ^ cur4[3].w ^ pm);
+        k += kTileSteps;
+        while (k >= a.spr) {
+          k -= a.spr;
+          ++r;
+        }
+        continue;
+      }
       if (pm && !(a.dbg & 4)) {
 #pragma unroll
         for (int j = 0; j < kG; ++j) {

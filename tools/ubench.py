@@ -57,6 +57,19 @@ def main():
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / 50 * 1000
             res[f"gen{cfg}_g{grid}"] = (round(us, 2), round(n * 2 / us / 1e3, 1))
+    lib.ub_xu.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    for kind in (0, 1):
+        grid, iters = 148 * 4, 2000
+        lib.ub_xu(kind, out.data_ptr(), grid, iters, st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.ub_xu(kind, out.data_ptr(), grid, iters, st)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1000
+        n_exp = grid * 512 * iters * 8
+        res[f"xu{kind}"] = (round(us, 1), "exp/clk/SM @1965MHz", round(n_exp / (us * 1e-6) / 148 / 1.965e9, 2))
     print(json.dumps(res))
 
 
