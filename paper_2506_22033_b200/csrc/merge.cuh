@@ -192,6 +192,7 @@ __device__ __noinline__ int warp_decide(const MergeSmem& ms, int n, float M, dou
           double run = 0.0;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
+            if (32 * q >= lim || n2 != UNK) break;  // (uniform)
             const int i = lane + 32 * q;
             const double cq = run + warp_incl_scan_d((i < lim) ? w[q] : 0.0, lane);
             const unsigned hit = __ballot_sync(kFull, (i < lim) && (cq >= target));
@@ -248,11 +249,16 @@ __device__ __noinline__ int warp_decide(const MergeSmem& ms, int n, float M, dou
         const double u = pre ? u_pre : philox_uniform(seed, p.request_id, step);
         const double target = u * W;
         DTR(12);
+        if (n3 <= 32) {
 #pragma unroll 4
-        for (int j = 0; j < n3; ++j) {
-          const int idj = comp_id(top[j]);
+          for (int j = 0; j < n3; ++j) rk[0] += (comp_id(top[j]) < id[0]) ? 1 : 0;
+        } else {
+#pragma unroll 4
+          for (int j = 0; j < n3; ++j) {
+            const int idj = comp_id(top[j]);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) rk[q] += (idj < id[q]) ? 1 : 0;
+            for (int q = 0; q < Q; ++q) rk[q] += (idj < id[q]) ? 1 : 0;
+          }
         }
         double* wid = reinterpret_cast<double*>(ms.byid);
 #pragma unroll

@@ -126,8 +126,10 @@ static bool row_may_pend(const sampling_params& p, int V, int kcand) {
 extern "C" {
 
 const char* sampler_version(void) {
-  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a), 16-byte LDG streaming pass with "
-         "per-vector max keys and lane-max bound, per-row merge, exact multi-pass fallback, Philox4x32-10";
+  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a); phase A: persistent warp-specialised "
+         "stream (1-D bulk-copy ring, penalty presence bitmap, packed bf16 exp-sum, group/step keys); "
+         "phase B: per-row step-key bound, group re-read, exact top-k, candidate-parallel decision, "
+         "Philox4x32-10; exact multi-pass fallback";
 }
 
 const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }

@@ -184,6 +184,153 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
   return floor;
 }
 
+
+// Final decision for one row by the whole block, candidate-parallel (R6-R11; the same
+// rules as merge.cuh warp_decide): candidate i = top[i] (pi order, weight wv[i] = exp((z'-M)/tau)
+// in float64) is owned by thread i.  Every prefix sum is a plain loop in a fixed order (pi order
+// for top-k/top-p, ascending id for the draw), so the arithmetic is the oracle's sequential sums
+// and no warp scan or shuffle sits on the critical path.  Returns the token (-1: not OK).
+__device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
+                                         uint64_t F, bool bad, const RowCfg& rc, const sampling_params& p,
+                                         double u, int row, const RowOut& ro, bool pending_ok) {
+  constexpr int UNK = 0x7FFFFFFF;
+  const int tid = threadIdx.x;
+  const uint64_t* top = ms.top;
+  const double* wv = ms.wv;
+  // ctl[6] n2 (top-p), ctl[7] nm (min-p), ctl[8] pick id, ctl[9] n_exact
+  if (tid == 0) {
+    ctl[6] = UNK;
+    ctl[7] = UNK;
+    ctl[8] = UNK;
+    ctl[9] = 0;
+  }
+  cbar();
+  int status = SAMPLER_ROW_OK;
+  if (bad) status = SAMPLER_ROW_NONFINITE;
+  else if (n == 0 || !(M > -INFINITY)) status = SAMPLER_ROW_ALL_NEG_INF;
+  // n_exact = |{i : top[i] >= F}| (a prefix: top is sorted descending)
+  const bool own = tid < n;
+  const uint64_t ci = own ? top[tid] : 0ull;
+  const double wi = own ? wv[tid] : 0.0;
+  if (own && ci >= F && (tid + 1 == n || top[tid + 1] < F)) ctl[9] = tid + 1;
+  const bool complete = (F == 0);
+  double cum = 0.0;  // inclusive pi-order prefix of the weights
+  if (own && status == SAMPLER_ROW_OK && !rc.greedy)
+    for (int j = 0; j <= tid; ++j) cum += wv[j];
+  cbar();
+  const int n_exact = ctl[9];
+  int n3 = -1;
+  int32_t tok = -1;
+  double lp = NAN, flp = NAN, W = 0.0;
+  uint64_t cutoff = 0;
+  if (status == SAMPLER_ROW_OK) {
+    if (rc.greedy) {
+      n3 = (n_exact >= 1) ? 1 : -1;
+    } else {
+      int n1 = UNK;
+      if (rc.topk_on) {
+        if (rc.k <= n_exact) n1 = rc.k;
+        else if (complete) n1 = n;
+      } else if (complete) {
+        n1 = n;
+      }
+      int cand = n1;
+      bool ok = true;
+      double* cums = reinterpret_cast<double*>(ms.pool);  // pi-order prefix sums (the pool is done)
+      if (own) cums[tid] = cum;
+      cbar();
+      if (rc.top_p < 1.0f) {
+        double W1 = 0.0;
+        bool w1k = false;
+        if (n1 != UNK) {
+          W1 = cums[n1 - 1];
+          w1k = true;
+        } else if (!rc.topk_on) {
+          W1 = S;
+          w1k = true;
+        }
+        if (!w1k) {
+          ok = false;
+        } else {
+          const double target = (double)rc.top_p * W1;
+          const int lim = (n1 != UNK && n1 < n_exact) ? n1 : n_exact;
+          if (tid < lim && cum >= target && (tid == 0 || cums[tid - 1] < target)) ctl[6] = tid + 1;
+          cbar();
+          int n2 = ctl[6];
+          if (n2 == UNK && n1 != UNK && n1 <= n_exact) n2 = n1;  // rounding shortfall
+          if (n2 != UNK) cand = cand < n2 ? cand : n2;
+        }
+      }
+      if (ok && rc.min_p > 0.0f) {
+        if (tid < n_exact && wi < (double)rc.min_p && (tid == 0 || wv[tid - 1] >= (double)rc.min_p)) ctl[7] = tid;
+        cbar();
+        int nm = ctl[7];
+        if (nm == UNK && complete) nm = n;
+        if (nm != UNK) cand = cand < nm ? cand : nm;
+      }
+      if (ok && cand != UNK && cand <= n_exact && cand >= 1) n3 = cand;
+      if (n3 >= 1) W = cums[n3 - 1];
+    }
+    if (n3 < 0) {
+      status = kRowPending;
+    } else {
+      cutoff = top[n3 - 1];
+      if (rc.greedy) {
+        tok = comp_id(top[0]);
+        W = 1.0;
+        lp = ((double)comp_val(top[0]) - (double)M) - logS;
+        flp = 0.0;
+      } else {
+        // the draw: ascending token id over the kept set K3 = top[0..n3), first cumulative > u W
+        const double target = u * W;
+        const int idi = own ? comp_id(ci) : 0;
+        if (tid < n3) {
+          double c_in = 0.0;
+          for (int j = 0; j < n3; ++j)
+            if (comp_id(top[j]) <= idi) c_in += wv[j];
+          if (c_in > target) atomicMin(&ctl[8], idi);
+        }
+        cbar();
+        int pick = ctl[8];
+        if (pick == UNK) {  // u W at the top of the mass: the last kept id
+          if (tid < n3) atomicMax(&ctl[10], idi);
+          cbar();
+          pick = ctl[10];
+        }
+        tok = pick;
+        if (tid < n3 && idi == pick) {
+          lp = ((double)comp_val(ci) - (double)M) / (double)rc.tau - logS;
+          flp = log(wi / W);
+          ro.logprobs[row] = (float)lp;
+          if (ro.flogprobs) ro.flogprobs[row] = (float)flp;
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    RowInfo ri;
+    ri.M = M;
+    ri.status = status;
+    ri.S = S;
+    ri.W = W;
+    ri.cutoff = cutoff;
+    ri.token = tok;
+    ri.greedy = rc.greedy;
+    ro.info[row] = ri;
+    const bool pend = status == kRowPending;
+    if (!pend || !pending_ok) {
+      const int st = pend ? SAMPLER_ROW_UNRESOLVED : status;
+      ro.tokens[row] = (st == SAMPLER_ROW_OK) ? tok : -1;
+      if (st != SAMPLER_ROW_OK || rc.greedy) {
+        ro.logprobs[row] = (st == SAMPLER_ROW_OK) ? (float)lp : NAN;
+        if (ro.flogprobs) ro.flogprobs[row] = (st == SAMPLER_ROW_OK) ? (float)flp : NAN;
+      }
+      if (ro.status) ro.status[row] = st;
+    }
+  }
+  return (status == SAMPLER_ROW_OK) ? tok : -1;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a) {
   constexpr int VEC = Dec<T>::N;
@@ -375,15 +522,26 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   uint32_t lo_k = kKey16NegInf + 1;
   bool need_hist = rowok;
   if (rowok && nsv >= keff && nsv <= kBT) {
-    const uint32_t x = (tid < nsv) ? (uint32_t)s_sk[tid] : 0u;
-    if (x > kKey16NegInf) {
-      int gt = 0, ge = 0;
-      for (int j = 0; j < nsv; ++j) {
-        const uint32_t y = s_sk[j];
-        gt += y > x;
-        ge += y >= x;
+    if (tid < 32) {
+      // warp radix select, MSB first: the largest x with |{step keys >= x}| >= K is the K-th
+      // largest step key (8 keys per lane at most: nsv <= 256)
+      uint32_t key[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = lane + 32 * i;
+        const uint32_t y = (j < nsv) ? (uint32_t)s_sk[j] : 0u;
+        key[i] = (y > kKey16NegInf) ? y : 0u;
       }
-      if (gt < keff && ge >= keff) ctl[0] = (int)x;  // every such thread writes the same x
+      uint32_t pre = 0;
+#pragma unroll 1
+      for (int b = 15; b >= 0; --b) {
+        const uint32_t cand = pre | (1u << b);
+        int cnt = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cnt += __popc(__ballot_sync(kFull, key[i] >= cand));
+        if (cnt >= keff) pre = cand;
+      }
+      if (lane == 0 && pre > kKey16NegInf) ctl[0] = (int)pre;  // (fewer than K finite keys: 0)
     }
     cbar();
     if (ctl[0] != 0) {
@@ -576,16 +734,11 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     }
     return;
   }
-  // ---- decision (warp 0)
-  if (tid < 32) {
-    const double u = philox_uniform(seed, prm.request_id, a.step);
-    const int t = warp_decide(ms, n, M, S, F, bad, rc, prm, seed, a.step, r, a.ro, a.pending_ok != 0, tr, true,
-                              logS, u);
-    if (lane == 0) ctl[3] = t;
-  }
+  // ---- decision (whole block, candidate-parallel)
+  if (tid == 0) ctl[10] = -1;
+  const double u = philox_uniform(seed, prm.request_id, a.step);
+  const int32_t tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0);
   STR(6);
-  cbar();
-  const int32_t tok = ctl[3];
   if (!a.append || tok < 0) return;
   if (nu > kSelPen) {
     if (tid < 32) warp_append_token(a.hs, slot, tok, lane);

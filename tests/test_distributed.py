@@ -1,0 +1,106 @@
+"""Host-side logic of the N>1 paths, on CPU with the gloo backend, world_size 2.
+
+* vocab sharding (TP lm_head style): the shard bounds tile [0, V) and every rank
+  receives every rank's candidate record, in rank order, from ONE all_gather_into_tensor —
+  checked through paper_2506_22033_b200.distributed.sample_vocab_sharded with a stand-in sampler
+  object (the CUDA kernels behind sample_local / merge are covered by the -m gpu tests, including
+  the sharded == unsharded parity with an in-process gather);
+* batch-row sharding (DP style): the row bounds tile [0, B) with no collective on the data path;
+* bench.py's max-over-ranks reduction of the timed region.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2506_22033_b200.distributed import batch_row_bounds, sample_vocab_sharded, vocab_shard_bounds
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("V", [32000, 128256, 129280, 152064, 7, 8])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_vocab_shard_bounds_tile_the_vocabulary(V, world):
+    prev = 0
+    for r in range(world):
+        lo, hi = vocab_shard_bounds(V, world, r)
+        assert lo == prev and hi >= lo
+        if hi < V:
+            assert (hi - lo) % 8 == 0  # 16-byte bf16 rows in every shard but the last
+        prev = hi
+    assert prev == V
+
+
+@pytest.mark.parametrize("B", [1, 3, 256, 1024])
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_batch_row_bounds_tile_the_batch(B, world):
+    prev = 0
+    for r in range(world):
+        lo, hi = batch_row_bounds(B, world, r)
+        assert lo == prev
+        prev = hi
+    assert prev == B
+
+
+class _StandInSampler:
+    """Plays the C-ABI handle's part in the exchange: record = (rank, row, byte index) pattern."""
+
+    def __init__(self, rank, rec_bytes_per_row):
+        self.rank, self.rb = rank, rec_bytes_per_row
+        self.merged = None
+
+    def record_bytes(self, B):
+        return self.rb * B
+
+    def sample_local(self, logits_slice, rec, slots=None, params=None):
+        B = logits_slice.shape[0]
+        v = torch.arange(self.rb * B, dtype=torch.int64)
+        rec.copy_(((v + 31 * self.rank + 7) % 251).to(torch.uint8))
+
+    def merge(self, gathered, world, B, step, slots=None, params=None, seeds=None, append=False):
+        self.merged = (gathered.clone(), world, B, step)
+        return {"tokens": torch.zeros(B, dtype=torch.int32)}
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, V = 5, 1000
+        lo, hi = vocab_shard_bounds(V, world, rank)
+        s = _StandInSampler(rank, rec_bytes_per_row=48 + 8 * 40)
+        out = sample_vocab_sharded(s, torch.zeros(B, hi - lo), step=3)
+        g, w, b, step = s.merged
+        ok = w == world and b == B and step == 3 and "tokens" in out
+        rb = s.record_bytes(B)
+        for r in range(world):
+            v = torch.arange(rb, dtype=torch.int64)
+            ok = ok and torch.equal(g[r * rb:(r + 1) * rb], ((v + 31 * r + 7) % 251).to(torch.uint8))
+        # bench.py: time of the slowest rank
+        t = torch.tensor([1.0 + rank])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ok = ok and float(t.item()) == float(world)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_vocab_sharded_exchange_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}

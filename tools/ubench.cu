@@ -234,6 +234,33 @@ extern "C" int ub_xu(int kind, float* out, int grid, int iters, void* stream) {
   return (int)cudaGetLastError();
 }
 
+
+// fp64 vs fp32: dependent-chain latency (1 warp per SM) and math-library exp/log chains
+template <int KIND>
+__global__ void chain_kernel(float* out, int iters) {
+  double d = 1.0 + threadIdx.x * 1e-9;
+  float f = 1.0f + threadIdx.x * 1e-7f;
+  for (int i = 0; i < iters; ++i) {
+    if (KIND == 0) d = d * 0.9999999 + 1e-9;           // DFMA chain
+    else if (KIND == 1) f = f * 0.9999999f + 1e-7f;    // FFMA chain
+    else if (KIND == 2) d = exp(-d) + 0.5;             // double exp chain
+    else if (KIND == 3) d = log(d + 1.0);              // double log chain
+    else if (KIND == 4) f = __expf(-f) + 0.5f;         // float fast exp chain
+  }
+  if (d == 12345.0 || f == 12345.f) out[0] = (float)d + f;
+}
+extern "C" int ub_chain(int kind, float* out, int iters, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (kind) {
+    case 0: chain_kernel<0><<<148, 32, 0, st>>>(out, iters); break;
+    case 1: chain_kernel<1><<<148, 32, 0, st>>>(out, iters); break;
+    case 2: chain_kernel<2><<<148, 32, 0, st>>>(out, iters); break;
+    case 3: chain_kernel<3><<<148, 32, 0, st>>>(out, iters); break;
+    default: chain_kernel<4><<<148, 32, 0, st>>>(out, iters); break;
+  }
+  return (int)cudaGetLastError();
+}
+
 extern "C" int ub_run(int kind, int mode, const void* x, int64_t nbytes, float* out, int grid, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = ST * TB + 2 * ST * 8;

@@ -70,6 +70,18 @@ def main():
         us = e0.elapsed_time(e1) * 1000
         n_exp = grid * 512 * iters * 8
         res[f"xu{kind}"] = (round(us, 1), "exp/clk/SM @1965MHz", round(n_exp / (us * 1e-6) / 148 / 1.965e9, 2))
+    lib.ub_chain.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    for kind in range(5):
+        iters = 20000
+        lib.ub_chain(kind, out.data_ptr(), iters, st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.ub_chain(kind, out.data_ptr(), iters, st)
+        e1.record()
+        torch.cuda.synchronize()
+        ns = e0.elapsed_time(e1) * 1e6 / iters
+        res[f"chain{kind}_ns_per_link"] = round(ns, 2)
     print(json.dumps(res))
 
 
