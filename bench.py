@@ -246,6 +246,8 @@ def main():
     # (set = step mod NSET), so each history grows by at most GROW tokens over the run.
     GROW = 256
     nset = max(1, -(-(total_steps + a.e2e_steps + 8) // GROW))
+    if nset % NBUF == 0:  # a slot set must not always meet the same logits buffer
+        nset += 1
     L = max(len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)) + GROW + 64
     if vocab_mode:
         from paper_2506_22033_b200.distributed import vocab_shard_bounds

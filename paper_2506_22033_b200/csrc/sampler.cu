@@ -198,7 +198,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
             al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
             al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
             al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&
-            al((void**)&h->d_hand, sizeof(RowHand) * B) && al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
+            al((void**)&h->d_hand, sizeof(RowHand) * B) &&  al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
             al((void**)&h->d_parts, sizeof(PartRec) * B * kCW * ((h->Vq / kStepVec + kTileSteps - 1) / kTileSteps + 1));
   if (!ok) {
     cudaGetLastError();
@@ -525,6 +525,7 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.hs = hist_state(h);
   s.parts = h->d_parts;
   s.hand = h->d_hand;
+  s.dbg = h->dbg;
   s.pent = h->d_pent;
   s.gkeys = h->d_gkeys;
   s.ro = ro;

@@ -46,6 +46,7 @@ struct SelectArgs {
   HistState hs;
   const PartRec* parts;    // phase A partial records [B][rpr][kCW]
   const RowHand* hand;     // phase A hand-off [B]
+  int dbg;
   const PenEnt* pent;      // [B][L]
   const uint16_t* gkeys;
   RowOut ro;
@@ -114,6 +115,12 @@ __device__ __forceinline__ void block_append_smem(const HistState& hs, int slot,
 // Degenerate rows (more candidates >= T than the pool holds: massive ties, or an unbounded T):
 // the whole collection again in bounded chunks, shrinking the pool to its exact top-K (raising a
 // floor below which nothing is kept) whenever it fills.  Returns the floor.
+// float64 exp2 / exp / log as calls: one copy of the math-library code on the per-row path
+// (each CTA walks its code once, so inlined copies are instruction-fetch misses)
+__device__ __noinline__ double dexp2_call(double x) { return exp2(x); }
+__device__ __noinline__ double dexp_call(double x) { return exp(x); }
+__device__ __noinline__ double dlog_call(double x) { return log(x); }
+
 template <typename T>
 __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const uint8_t* rowp,
                                                     const UniqEntry* utab, const UniqEntry* s_ue, int nu, int nus,
@@ -192,8 +199,13 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
 // and no warp scan or shuffle sits on the critical path.  Returns the token (-1: not OK).
 __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
                                          uint64_t F, bool bad, const RowCfg& rc, const sampling_params& p,
-                                         double u, int row, const RowOut& ro, bool pending_ok) {
+                                         double u, int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {
   constexpr int UNK = 0x7FFFFFFF;
+#define BTR(k)                                    \
+  do {                                            \
+    if (tr && threadIdx.x == 0) tr[k] = gtimer(); \
+  } while (0)
+  BTR(8);
   const int tid = threadIdx.x;
   const uint64_t* top = ms.top;
   const double* wv = ms.wv;
@@ -218,6 +230,7 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
   if (own && status == SAMPLER_ROW_OK && !rc.greedy)
     for (int j = 0; j <= tid; ++j) cum += wv[j];
   cbar();
+  BTR(9);
   const int n_exact = ctl[9];
   int n3 = -1;
   int32_t tok = -1;
@@ -271,6 +284,7 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
       if (ok && cand != UNK && cand <= n_exact && cand >= 1) n3 = cand;
       if (n3 >= 1) W = cums[n3 - 1];
     }
+    BTR(10);
     if (n3 < 0) {
       status = kRowPending;
     } else {
@@ -291,6 +305,7 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
           if (c_in > target) atomicMin(&ctl[8], idi);
         }
         cbar();
+        BTR(11);
         int pick = ctl[8];
         if (pick == UNK) {  // u W at the top of the mass: the last kept id
           if (tid < n3) atomicMax(&ctl[10], idi);
@@ -300,13 +315,14 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
         tok = pick;
         if (tid < n3 && idi == pick) {
           lp = ((double)comp_val(ci) - (double)M) / (double)rc.tau - logS;
-          flp = log(wi / W);
+          flp = dlog_call(wi / W);
           ro.logprobs[row] = (float)lp;
           if (ro.flogprobs) ro.flogprobs[row] = (float)flp;
         }
       }
     }
   }
+  BTR(12);
   if (tid == 0) {
     RowInfo ri;
     ri.M = M;
@@ -328,6 +344,8 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
       if (ro.status) ro.status[row] = st;
     }
   }
+  BTR(13);
+#undef BTR
   return (status == SAMPLER_ROW_OK) ? tok : -1;
 }
 
@@ -426,23 +444,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   const int nus = min(nu, kSelPen);
   const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
   const uint8_t* rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
-  // the penalised entries: smem copy of the table (id order) for masking and the append, exact
-  // penalised values in registers (raw[q]; lid[q] < 0: not in this vocabulary slice)
-  float raw[kSelPR];
-  int lid[kSelPR];
-#pragma unroll
-  for (int q = 0; q < kSelPR; ++q) {
-    const int e = tid + q * kBT;
-    lid[q] = -1;
-    raw[q] = NAN;
-    if (e < nus) {
-      const int l = s_ue[e].id - a.voff;
-      if (l >= 0 && l < a.vloc) {
-        lid[q] = l;
-        raw[q] = s_zp[e];
-      }
-    }
-  }
+  // the penalised entries: smem copy of the table (id order) for masking and the append, and the
+  // exact penalised values s_zp (entries outside this vocabulary slice are skipped by id)
   STR(1);
   // ---- M = max of the stream partials and the exact penalised values;
   //      S = sum_parts s 2^((m - M) c) + sum_pen 2^((z' - M) c)   (fixed order: deterministic)
@@ -453,12 +456,14 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     mloc = fmaxf(mloc, pr.m);
     fl |= pr.bad;
   }
-#pragma unroll
-  for (int q = 0; q < kSelPR; ++q)
-    if (lid[q] >= 0) {
-      if (!(raw[q] < INFINITY)) fl |= kRecBad;  // NaN / +inf logit (or penalised value)
-      else mloc = fmaxf(mloc, raw[q]);
-    }
+#pragma unroll 1
+  for (int e = tid; e < nus; e += kBT) {
+    const int l = s_ue[e].id - a.voff;
+    if (l < 0 || l >= a.vloc) continue;
+    const float zp = s_zp[e];
+    if (!(zp < INFINITY)) fl |= kRecBad;  // NaN / +inf logit (or penalised value)
+    else mloc = fmaxf(mloc, zp);
+  }
   for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
     const UniqEntry ue = utab[e];
     const int l = ue.id - a.voff;
@@ -491,25 +496,35 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   const bool bad = (fl & kRecBad) != 0;
   double term = 0.0;
   if (M > -INFINITY && !bad) {
-    if (p0.s != 0.0) term += p0.s * exp2(((double)p0.m - (double)M) * rc.c_d);
+    if (p0.s != 0.0) term += p0.s * dexp2_call(((double)p0.m - (double)M) * rc.c_d);
+#pragma unroll 1
     for (int o = tid + kBT; o < nparts; o += kBT) {
       const PartRec pr = prow[o];
-      if (pr.s != 0.0) term += pr.s * exp2(((double)pr.m - (double)M) * rc.c_d);
+      if (pr.s != 0.0) term += pr.s * dexp2_call(((double)pr.m - (double)M) * rc.c_d);
     }
-#pragma unroll
-    for (int q = 0; q < kSelPR; ++q)
-      if (lid[q] >= 0 && raw[q] > -INFINITY) term += exp2(((double)raw[q] - (double)M) * rc.c_d);
+#pragma unroll 1
+    for (int e = tid; e < nus; e += kBT) {
+      const int l = s_ue[e].id - a.voff;
+      const float zp = s_zp[e];
+      if (l >= 0 && l < a.vloc && zp > -INFINITY) term += dexp2_call(((double)zp - (double)M) * rc.c_d);
+    }
+#pragma unroll 1
     for (int e = kSelPen + tid; e < nu; e += kBT) {
       const UniqEntry ue = utab[e];
       const int l = ue.id - a.voff;
       if (l < 0 || l >= a.vloc) continue;
       const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
-      if (zp > -INFINITY) term += exp2(((double)zp - (double)M) * rc.c_d);
+      if (zp > -INFINITY) term += dexp2_call(((double)zp - (double)M) * rc.c_d);
     }
   }
   const double S = block_sum_d(term, ms.bs);
-  const double logS = log(S);
+  const double logS = dlog_call(S);
   STR(2);
+  const bool rowok = !bad && M > -INFINITY;
+  uint32_t lo_k = kKey16NegInf + 1;
+  float Tv = 0.f;
+  uint64_t floor = 0;
+  {
   // ---- bound: T = the K-th largest step key (each step key = the max of 1024 / 512 elements
   // rounded down, so K distinct elements are >= val(T)); every element >= val(T) lies in a
   // group with key >= T or is penalised.  One rank count per step key (smem broadcast).
@@ -517,9 +532,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   // 16-bit key among the group keys and the penalised elements, by one histogram pass over the
   // kHistBins key steps below key(M) (one bin per key value: exact); a row whose K-th key lies
   // below that window takes every finite element (the collection then shrinks in bounded rounds).
-  const bool rowok = !bad && M > -INFINITY;
   const uint32_t kmax = rowok ? key16_down(M) : 0u;
-  uint32_t lo_k = kKey16NegInf + 1;
   bool need_hist = rowok;
   if (rowok && nsv >= keff && nsv <= kBT) {
     if (tid < 32) {
@@ -554,9 +567,12 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
       const uint32_t d = kmax - key;
       if (key > kKey16NegInf && d < (uint32_t)kHistBins) atomicAdd(&hist[d], 1u);
     };
-#pragma unroll
-    for (int q = 0; q < kSelPR; ++q)
-      if (lid[q] >= 0 && raw[q] > -INFINITY && raw[q] < INFINITY) add_key(key16_down(raw[q]));
+#pragma unroll 1
+    for (int e = tid; e < nus; e += kBT) {
+      const int l = s_ue[e].id - a.voff;
+      const float zp = s_zp[e];
+      if (l >= 0 && l < a.vloc && zp > -INFINITY && zp < INFINITY) add_key(key16_down(zp));
+    }
     for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
       const UniqEntry ue = utab[e];
       const int l = ue.id - a.voff;
@@ -594,17 +610,18 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     cbar();
     if (ctl[0] != 0) lo_k = (uint32_t)ctl[0];
   }
-  const float Tv = key16_val(lo_k);
+  Tv = key16_val(lo_k);
   // ---- collect: penalised elements (exact), then the qualifying groups
   auto push = [&](uint64_t c) {
     const int at = atomicAdd(&ctl[1], 1);
     if (at < kPool) ms.pool[at] = c;
   };
-#pragma unroll
-  for (int q = 0; q < kSelPR; ++q) {
-    if (lid[q] < 0) continue;
-    const float zp = raw[q];
-    if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, a.voff + lid[q]));
+#pragma unroll 1
+  for (int e = tid; e < nus; e += kBT) {
+    const int l = s_ue[e].id - a.voff;
+    if (l < 0 || l >= a.vloc) continue;
+    const float zp = s_zp[e];
+    if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, s_ue[e].id));
   }
   for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
     const UniqEntry ue = utab[e];
@@ -687,9 +704,9 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
   }
   cbar();
   slow = slow || ctl[1] > kPool;  // uniform: after the barrier
-  uint64_t floor = 0;
   if (slow) floor = select_collect_slow<T>(a, rowp, utab, s_ue, nu, nus, prm, Tv, lo_k, nvv, gwords, keff, ms, ctl, ql);
   cbar();
+  }
   STR(4);
   // ---- exact top-K of the pool by rank counting
   // (each placed candidate's weight w = exp((z - M)/tau) in float64 is computed here, in
@@ -706,7 +723,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     for (; j < nc && rank < keff; ++j) rank += ms.pool[j] > c ? 1 : 0;
     if (rank < keff) {
       ms.top[rank] = c;
-      ms.wv[rank] = rc.greedy ? 0.0 : exp(((double)comp_val(c) - (double)M) * inv_tau);
+      ms.wv[rank] = rc.greedy ? 0.0 : dexp_call(((double)comp_val(c) - (double)M) * inv_tau);
     }
   }
   cbar();
@@ -735,9 +752,11 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a)
     return;
   }
   // ---- decision (whole block, candidate-parallel)
+  STR(20);
   if (tid == 0) ctl[10] = -1;
   const double u = philox_uniform(seed, prm.request_id, a.step);
-  const int32_t tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0);
+  STR(21);
+  const int32_t tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
   STR(6);
   if (!a.append || tok < 0) return;
   if (nu > kSelPen) {

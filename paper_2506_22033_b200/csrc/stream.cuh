@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamA
       }
       const int vb = k * kStepVec;
       uint4 cur4[kG];
+      __syncwarp();  // converged before the spin-wait (a diverged lane must not starve behind it)
       mbar_wait(full + sl, (uint32_t)((t / kNS) & 1));
       const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
       uint32_t pm = bm[(sl * kTileSteps + w) * 32 + lane];
