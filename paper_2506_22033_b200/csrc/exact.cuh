@@ -251,7 +251,7 @@ __device__ uint64_t radix_in_bucket(ExSmem& s, const BucketCtx& bc, int b, uint6
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const ExactArgs a) {
+__global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_constant__ ExactArgs a) {
   const int r = blockIdx.x;
   if (a.ro.info[r].status != kRowPending) return;
   extern __shared__ __align__(128) uint8_t smem[];

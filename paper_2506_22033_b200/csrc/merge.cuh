@@ -498,7 +498,7 @@ struct MergeArgs {
 };
 constexpr int kMergeKernelSmem = kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8 + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12 + 512;
 
-__global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const MergeArgs m) {
+__global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constant__ MergeArgs m) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int r = blockIdx.x;
   MergeSmem ms;

@@ -197,7 +197,7 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
 // in float64) is owned by thread i.  Every prefix sum is a plain loop in a fixed order (pi order
 // for top-k/top-p, ascending id for the draw), so the arithmetic is the oracle's sequential sums
 // and no warp scan or shuffle sits on the critical path.  Returns the token (-1: not OK).
-__device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
+__device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
                                          uint64_t F, bool bad, const RowCfg& rc, const sampling_params& p,
                                          double u, int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {
   constexpr int UNK = 0x7FFFFFFF;
@@ -350,7 +350,7 @@ __device__ __noinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, f
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const SelectArgs a) {
+__global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_constant__ SelectArgs a) {
   constexpr int VEC = Dec<T>::N;
   constexpr int ESZ = (int)sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];

@@ -216,7 +216,7 @@ struct LaneSum {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const StreamArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int VEC = Dec<T>::N;
   constexpr int ESZ = (int)sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
