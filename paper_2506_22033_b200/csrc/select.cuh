@@ -472,7 +472,10 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     if (!(zp < INFINITY)) fl |= kRecBad;
     else mloc = fmaxf(mloc, zp);
   }
-  // one barrier for max and flags together
+  // one barrier for max and flags together; meanwhile the last warp finds the bound T = the K-th
+  // largest step key (each step key = the max of 1024 / 512 elements rounded down, so K distinct
+  // elements are >= val(T); every element >= val(T) lies in a group with key >= T or is
+  // penalised): warp radix select, MSB first — the largest x with |{step keys >= x}| >= K
   {
     const int w = tid >> 5;
     float mw = warp_max(mloc);
@@ -481,64 +484,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       ms.bs.f[w] = mw;
       ms.bs.i[w] = (int)fw;
     }
-    cbar();
-    mw = ms.bs.f[0];
-    unsigned fa = (unsigned)ms.bs.i[0];
-#pragma unroll
-    for (int j = 1; j < kBW; ++j) {
-      mw = fmaxf(mw, ms.bs.f[j]);
-      fa |= (unsigned)ms.bs.i[j];
-    }
-    mloc = mw;
-    fl = fa;
-  }
-  const float M = mloc;
-  const bool bad = (fl & kRecBad) != 0;
-  double term = 0.0;
-  if (M > -INFINITY && !bad) {
-    if (p0.s != 0.0) term += p0.s * dexp2_call(((double)p0.m - (double)M) * rc.c_d);
-#pragma unroll 1
-    for (int o = tid + kBT; o < nparts; o += kBT) {
-      const PartRec pr = prow[o];
-      if (pr.s != 0.0) term += pr.s * dexp2_call(((double)pr.m - (double)M) * rc.c_d);
-    }
-#pragma unroll 1
-    for (int e = tid; e < nus; e += kBT) {
-      const int l = s_ue[e].id - a.voff;
-      const float zp = s_zp[e];
-      if (l >= 0 && l < a.vloc && zp > -INFINITY) term += dexp2_call(((double)zp - (double)M) * rc.c_d);
-    }
-#pragma unroll 1
-    for (int e = kSelPen + tid; e < nu; e += kBT) {
-      const UniqEntry ue = utab[e];
-      const int l = ue.id - a.voff;
-      if (l < 0 || l >= a.vloc) continue;
-      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
-      if (zp > -INFINITY) term += dexp2_call(((double)zp - (double)M) * rc.c_d);
-    }
-  }
-  const double S = block_sum_d(term, ms.bs);
-  const double logS = dlog_call(S);
-  STR(2);
-  const bool rowok = !bad && M > -INFINITY;
-  uint32_t lo_k = kKey16NegInf + 1;
-  float Tv = 0.f;
-  uint64_t floor = 0;
-  {
-  // ---- bound: T = the K-th largest step key (each step key = the max of 1024 / 512 elements
-  // rounded down, so K distinct elements are >= val(T)); every element >= val(T) lies in a
-  // group with key >= T or is penalised.  One rank count per step key (smem broadcast).
-  // Fallback (fewer than K finite step keys, or more steps than threads): T = the K-th largest
-  // 16-bit key among the group keys and the penalised elements, by one histogram pass over the
-  // kHistBins key steps below key(M) (one bin per key value: exact); a row whose K-th key lies
-  // below that window takes every finite element (the collection then shrinks in bounded rounds).
-  const uint32_t kmax = rowok ? key16_down(M) : 0u;
-  bool need_hist = rowok;
-  if (rowok && nsv >= keff && nsv <= kBT) {
-    if (tid < 32) {
-      // warp radix select, MSB first: the largest x with |{step keys >= x}| >= K is the K-th
-      // largest step key (8 keys per lane at most: nsv <= 256)
-      uint32_t key[8];
+    if (w == kBW - 1 && nsv >= keff && nsv <= kBT) {
+      uint32_t key[8];  // 8 keys per lane at most: nsv <= 256
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int j = lane + 32 * i;
@@ -557,6 +504,60 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       if (lane == 0 && pre > kKey16NegInf) ctl[0] = (int)pre;  // (fewer than K finite keys: 0)
     }
     cbar();
+    mw = ms.bs.f[0];
+    unsigned fa = (unsigned)ms.bs.i[0];
+#pragma unroll
+    for (int j = 1; j < kBW; ++j) {
+      mw = fmaxf(mw, ms.bs.f[j]);
+      fa |= (unsigned)ms.bs.i[j];
+    }
+    mloc = mw;
+    fl = fa;
+  }
+  const float M = mloc;
+  const bool bad = (fl & kRecBad) != 0;
+  STR(2);
+  double term = 0.0;
+  auto s_terms = [&]() -> double {
+    double t = 0.0;
+    if (!(M > -INFINITY) || bad) return t;
+    if (p0.s != 0.0) t += p0.s * dexp2_call(((double)p0.m - (double)M) * rc.c_d);
+#pragma unroll 1
+    for (int o = tid + kBT; o < nparts; o += kBT) {
+      const PartRec pr = prow[o];
+      if (pr.s != 0.0) t += pr.s * dexp2_call(((double)pr.m - (double)M) * rc.c_d);
+    }
+#pragma unroll 1
+    for (int e = tid; e < nus; e += kBT) {
+      const int l = s_ue[e].id - a.voff;
+      const float zp = s_zp[e];
+      if (l >= 0 && l < a.vloc && zp > -INFINITY) t += dexp2_call(((double)zp - (double)M) * rc.c_d);
+    }
+#pragma unroll 1
+    for (int e = kSelPen + tid; e < nu; e += kBT) {
+      const UniqEntry ue = utab[e];
+      const int l = ue.id - a.voff;
+      if (l < 0 || l >= a.vloc) continue;
+      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+      if (zp > -INFINITY) t += dexp2_call(((double)zp - (double)M) * rc.c_d);
+    }
+    return t;
+  };
+  const bool rowok = !bad && M > -INFINITY;
+  uint32_t lo_k = kKey16NegInf + 1;
+  float Tv = 0.f;
+  uint64_t floor = 0;
+  {
+  // ---- bound: T = the K-th largest step key (each step key = the max of 1024 / 512 elements
+  // rounded down, so K distinct elements are >= val(T)); every element >= val(T) lies in a
+  // group with key >= T or is penalised.  One rank count per step key (smem broadcast).
+  // Fallback (fewer than K finite step keys, or more steps than threads): T = the K-th largest
+  // 16-bit key among the group keys and the penalised elements, by one histogram pass over the
+  // kHistBins key steps below key(M) (one bin per key value: exact); a row whose K-th key lies
+  // below that window takes every finite element (the collection then shrinks in bounded rounds).
+  const uint32_t kmax = rowok ? key16_down(M) : 0u;
+  bool need_hist = rowok;
+  if (rowok && nsv >= keff && nsv <= kBT) {
     if (ctl[0] != 0) {
       lo_k = (uint32_t)ctl[0];
       need_hist = false;
@@ -611,7 +612,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     if (ctl[0] != 0) lo_k = (uint32_t)ctl[0];
   }
   Tv = key16_val(lo_k);
-  // ---- collect: penalised elements (exact), then the qualifying groups
+  // ---- collect: penalised elements (exact), then the qualifying groups (their re-read overlaps
+  // the float64 softmax terms S = sum_parts s 2^((m - M) c) + sum_pen 2^((z' - M) c))
   auto push = [&](uint64_t c) {
     const int at = atomicAdd(&ctl[1], 1);
     if (at < kPool) ms.pool[at] = c;
@@ -673,6 +675,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     const bool act = it < nq * kG && v < nvv;
     uint4 u4 = act ? ldg_stream(rowp + (int64_t)v * 16) : make_uint4(Dec<T>::kNegInfWord, Dec<T>::kNegInfWord,
                                                                        Dec<T>::kNegInfWord, Dec<T>::kNegInfWord);
+    if (it0 == 0) term = s_terms();  // the float64 softmax terms, while the re-read is in flight
     uint32_t msk = listed_mask<VEC>(s_ue, ns, a.voff + v * VEC);
 #pragma unroll
     for (int t = 0; t < VEC; ++t)
@@ -702,11 +705,13 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
         ++at;
       }
   }
+  if (nq * kG == 0) term = s_terms();
   cbar();
   slow = slow || ctl[1] > kPool;  // uniform: after the barrier
   if (slow) floor = select_collect_slow<T>(a, rowp, utab, s_ue, nu, nus, prm, Tv, lo_k, nvv, gwords, keff, ms, ctl, ql);
-  cbar();
   }
+  const double S = block_sum_d(term, ms.bs);  // (its barriers also close the collection)
+  const double logS = dlog_call(S);
   STR(4);
   // ---- exact top-K of the pool by rank counting
   // (each placed candidate's weight w = exp((z - M)/tau) in float64 is computed here, in

@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   __syncthreads();
 
   if (w == kCW + 1) {
+    if (a.dbg & 512) return;  // (development: no hand-off)
     // ================= penalty warp: the hand-off of the rows that start in this span =================
     const int64_t rfirst = (s0 + a.spr - 1) / a.spr;
     for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
@@ -317,7 +318,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
             if (++kk == a.spr) { kk = 0; ++rr; }
           }
         }
-        mbar_arrive_expect_tx(full + sl, bytes + (uint32_t)n * 128u);
+        const bool bmcopy = !(a.dbg & 256);
+        mbar_arrive_expect_tx(full + sl, bytes + (bmcopy ? (uint32_t)n * 128u : 0u));
         uint8_t* dst = ring + sl * (kTileSteps * kStepBytes);
         uint8_t* bdst = reinterpret_cast<uint8_t*>(bm) + sl * (kTileSteps * 128);
         // one bulk copy per run of consecutive steps of one row (contiguous in global memory)
@@ -331,9 +333,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
           } while (j < n && k < a.spr);
           bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
           // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
-          const int slot = a.slots ? a.slots[r] : r;
-          bulk_g2s(bdst + j0 * 128, a.hs.pmask + ((int64_t)slot * a.spr + k0) * 32, (uint32_t)(j - j0) * 128u,
-                   full + sl, pol);
+          if (bmcopy) {
+            const int slot = a.slots ? a.slots[r] : r;
+            bulk_g2s(bdst + j0 * 128, a.hs.pmask + ((int64_t)slot * a.spr + k0) * 32, (uint32_t)(j - j0) * 128u,
+                     full + sl, pol);
+          }
           if (k == a.spr) { k = 0; ++r; }
         }
       }
