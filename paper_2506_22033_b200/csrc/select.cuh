@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     for (int e = tid; e < nus; e += kBT) {
       const int l = s_ue[e].id - a.voff;
       const float zp = s_zp[e];
-      if (l >= 0 && l < a.vloc && zp > -INFINITY) t += dexp2_call(((double)zp - (double)M) * rc.c_d);
+      // (binary32 MUFU exp2, like the stream's own terms: relative error ~2^-22 per term)
+      if (l >= 0 && l < a.vloc && zp > -INFINITY) t += (double)ex2f((float)(((double)zp - (double)M) * rc.c_d));
     }
 #pragma unroll 1
     for (int e = kSelPen + tid; e < nu; e += kBT) {
@@ -728,7 +729,9 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     for (; j < nc && rank < keff; ++j) rank += ms.pool[j] > c ? 1 : 0;
     if (rank < keff) {
       ms.top[rank] = c;
-      ms.wv[rank] = rc.greedy ? 0.0 : dexp_call(((double)comp_val(c) - (double)M) * inv_tau);
+      // w = exp((z' - M)/tau) = 2^((z' - M) log2(e)/tau): MUFU exp2 (relative error ~2^-22), the
+      // argument rounded once to binary32
+      ms.wv[rank] = rc.greedy ? 0.0 : (double)ex2f((float)(((double)comp_val(c) - (double)M) * rc.c_d));
     }
   }
   cbar();
