@@ -139,20 +139,34 @@ struct GroupMath<__nv_bfloat16> {
     return fmax_nan(__low2float(r), __high2float(r));
   }
   static __device__ __forceinline__ float esum(const uint4 (&u)[kG], float nm, uint64_t c2) {
+    float tmax;
+    return esum_tmax(u, nm, c2, tmax);
+  }
+  // the exp-sum and, from the same differences t = z - m_ref (exact for bf16 operands), the
+  // NaN-propagating max of t on the FP32 ALU (keeps the packed bf16 max off the MUFU/XU pipe)
+  static __device__ __forceinline__ float esum_tmax(const uint4 (&u)[kG], float nm, uint64_t c2, float& tmax) {
     uint64_t e[2 * kG];
+    float tm[kG];
 #pragma unroll
     for (int j = 0; j < kG; ++j) {
       const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
       uint64_t p[4];
+      float m4[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
+        const uint64_t t2 = bf16x2_sub(w[i], nm);
+        float ta, tb;
+        f2_unpack(t2, ta, tb);
+        m4[i] = fmax_nan(ta, tb);
         float a, b;
-        f2_unpack(f2_mul(bf16x2_sub(w[i], nm), c2), a, b);
+        f2_unpack(f2_mul(t2, c2), a, b);
         p[i] = f2_pack(ex2f(a), ex2f(b));
       }
+      tm[j] = fmax_nan(fmax_nan(m4[0], m4[1]), fmax_nan(m4[2], m4[3]));
       e[2 * j] = f2_add(p[0], p[1]);
       e[2 * j + 1] = f2_add(p[2], p[3]);
     }
+    tmax = fmax_nan(fmax_nan(tm[0], tm[1]), fmax_nan(tm[2], tm[3]));
 #pragma unroll
     for (int s = 1; s < 2 * kG; s <<= 1)
 #pragma unroll
@@ -169,6 +183,10 @@ struct GroupMath<float> {
 #pragma unroll
     for (int j = 0; j < kG; ++j) m = fmax_nan(m, Dec<float>::vmax(u[j]));
     return m;
+  }
+  static __device__ __forceinline__ float esum_tmax(const uint4 (&u)[kG], float nm, uint64_t c2, float& tmax) {
+    tmax = gmax(u) + nm;  // (unused for binary32 logits: the max is taken on the raw values)
+    return esum(u, nm, c2);
   }
   static __device__ __forceinline__ float esum(const uint4 (&u)[kG], float nm, uint64_t c2) {
     const uint64_t nm2 = f2_pack(nm, nm);
@@ -442,8 +460,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       }
       // the exp-sum is taken against the current reference speculatively (independent of the
       // max tree, so the two chains overlap); a group that needs a new reference (rare) redoes it
-      float es = (a.dbg & 1) ? __uint_as_float(cur4[0].x ^ cur4[1].y ^ cur4[2].z ^ cur4[3].w) : GroupMath<T>::esum(cur4, ls.nm, c2);
-      const float gm = GroupMath<T>::gmax(cur4);
+      float es, gm;
+      if (VEC == 8 && ls.mref > -INFINITY) {  // bf16: the group max from the exact differences
+        float tmax;
+        es = GroupMath<T>::esum_tmax(cur4, ls.nm, c2, tmax);
+        gm = tmax + ls.mref;  // exact: tmax = z* - m_ref exactly
+      } else {
+        es = GroupMath<T>::esum(cur4, ls.nm, c2);
+        gm = GroupMath<T>::gmax(cur4);
+      }
       ls.bad |= !(gm < INFINITY) ? 1 : 0;  // NaN or +inf in the group
       if (!(a.dbg & 2)) {
         const uint32_t key = key16_down(gm);
