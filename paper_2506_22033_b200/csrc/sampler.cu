@@ -60,7 +60,11 @@ struct sampler {
 // event after the k-th kernel of a call (k = 0: before the first)
 static void tmark(sampler* h, int k, cudaStream_t st) {
   if (!h->timing) return;
-  cudaEventRecord(h->tev[k], st);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  // under graph capture the marks must be external event nodes to be readable after a replay
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(h->tev[k], st, cudaEventRecordExternal);
+  else cudaEventRecord(h->tev[k], st);
   h->tev_n = k;
 }
 
