@@ -454,7 +454,8 @@ static LaunchPlan plan(const sampler* h, int32_t B) {
   LaunchPlan p;
   p.spr = (int)(h->Vq / kStepVec);
   p.nsteps = (int64_t)B * p.spr;
-  int64_t span = (p.nsteps + h->sm_count - 1) / h->sm_count;
+  const int64_t nctas = (int64_t)h->sm_count * kStreamCtasPerSm;
+  int64_t span = (p.nsteps + nctas - 1) / nctas;
   span = std::max<int64_t>(span, kTileSteps);
   span = std::min<int64_t>(span, (int64_t)(kMaxSeg - 2) * p.spr);
   p.span = (int)span;

@@ -30,6 +30,7 @@ namespace smp {
 
 // ---- geometry of phase A (persistent CTAs, warp-specialised) ----------------------
 constexpr int kCW = 24;                    // consumer warps per CTA (one step of each tile each)
+constexpr int kStreamCtasPerSm = 1;        // CTAs (independent pipelines) per SM
 constexpr int kTileSteps = kCW;            // steps per ring tile (24 x 2 KB = 48 KB)
 constexpr int kNS = 4;                     // ring tiles (192 KB of bulk copies in flight per SM)
 constexpr int kMaxSeg = 48;                // rows per CTA span (the host caps the span)
@@ -234,7 +235,7 @@ struct LaneSum {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_constant__ StreamArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int VEC = Dec<T>::N;
   constexpr int ESZ = (int)sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
@@ -323,10 +324,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
     // ================= producer warp: 1-D bulk copies (TMA engine), one per step =================
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
+      uint64_t pwait = 0;
       int r = (int)(s0 / a.spr), k = (int)(s0 - (int64_t)r * a.spr);
       for (int t = 0; t < ntiles; ++t) {
         const int sl = t % kNS;
+        const uint64_t tp0 = a.trace ? gtimer() : 0;
         if (t >= kNS) mbar_wait(empty + sl, (uint32_t)((t / kNS - 1) & 1));
+        if (a.trace) pwait += gtimer() - tp0;
         const int n = min(kTileSteps, nspan - t * kTileSteps);
         uint32_t bytes = 0;
         {
@@ -349,7 +353,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
             ++j;
             ++k;
           } while (j < n && k < a.spr);
-          bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
+          if (a.dbg & 1024)
+            bulk_g2s_nohint(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl);
+          else
+            bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
           // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
           if (bmcopy) {
             const int slot = a.slots ? a.slots[r] : r;
@@ -358,6 +365,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
           }
           if (k == a.spr) { k = 0; ++r; }
         }
+      }
+      if (a.trace) {
+        a.trace[blockIdx.x * 64 + 9] = pwait;
+        a.trace[blockIdx.x * 64 + 10] = gtimer();
       }
     }
     return;
@@ -386,6 +397,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   }
   cbar_n<kCW * 32>();  // the span's row constants are in smem
 
+  uint64_t wait_ns = 0;  // (trace: time this warp spent waiting for its tiles)
   int cur = -1;  // row being accumulated
   LaneSum ls;
   ls.reset();
@@ -425,7 +437,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       const int vb = k * kStepVec;
       uint4 cur4[kG];
       __syncwarp();  // converged before the spin-wait (a diverged lane must not starve behind it)
+      const uint64_t tw0 = a.trace ? gtimer() : 0;
       mbar_wait(full + sl, (uint32_t)((t / kNS) & 1));
+      if (a.trace) wait_ns += gtimer() - tw0;
       const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
       uint32_t pm = bm[(sl * kTileSteps + w) * 32 + lane];
       if (vb + kStepVec <= nvv) {
@@ -494,6 +508,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
     }
   }
   if (cur >= 0) flush();
+  if (a.trace && lane == 0) a.trace[blockIdx.x * 64 + 16 + w] = wait_ns;  // (kCW <= 48)
   if (a.trace && tid == 0) a.trace[blockIdx.x * 64 + 7] = gtimer();
 }
 

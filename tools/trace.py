@@ -34,7 +34,7 @@ def main():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     vec = 8 if wl.dtype == "bf16" else 4
     spr = -(-(-(-wl.V // vec)) // 128)
-    nA = 64 * (wl.B * spr // 24 + 1)
+    nA = 64 * (wl.B * spr // int(os.environ.get("TILE_STEPS", "24")) + 1)
     n = nA + 32 * wl.B
     buf = (ctypes.c_uint64 * n)()
     rc = smod._lib.sampler_debug_trace(s.h, buf, n)
@@ -53,6 +53,9 @@ def main():
     print("late CTAs", int(late.sum()), "their SMs", sorted(set(sm[late].tolist()))[:40])
     print("per-CTA (start,end) us of late:", [(round((st[used][i]-t0)/1e3,1), round((en[used][i]-t0)/1e3,1)) for i in np.where(late)[0][:10]])
     print("phaseA end  ", pr(en[used] - t0))
+    cw = A[used, 16:16 + int(os.environ.get("CW", "24"))]
+    print("consumer wait ns per warp: p50=%.0f max=%.0f  (per CTA mean of warps p50=%.0f)" % (np.median(cw), cw.max(), np.median(cw.mean(axis=1))))
+    print("producer empty-wait ns p50=%.0f max=%.0f ; producer done p50=%.0f" % (np.median(A[used, 9]), A[used, 9].max(), np.median(A[used, 10] - t0)))
     pw = A[used, 8]
     print("penalty warp end", pr(pw[pw > 0] - t0))
     Bt = t[nA:].reshape(wl.B, 32)
