@@ -456,45 +456,44 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + sl);  // this warp's part of the slot is consumed
-      if (a.dbg & 8) {  // (development: the pipeline skeleton only)
-        ls.acc += (double)__uint_as_float(cur4[0].x ^ cur4[1].y ^ cur4[2].z ^ cur4[3].w ^ pm);
-        k += kTileSteps;
-        while (k >= a.spr) {
-          k -= a.spr;
-          ++r;
-        }
-        continue;
-      }
-      if (pm && !(a.dbg & 4)) {
+      if (pm) {
 #pragma unroll
         for (int j = 0; j < kG; ++j) {
           const uint32_t b = (pm >> (j * VEC)) & ((1u << VEC) - 1u);
           if (b) cur4[j] = Dec<T>::mask(cur4[j], b);
         }
       }
-      // the exp-sum is taken against the current reference speculatively (independent of the
-      // max tree, so the two chains overlap); a group that needs a new reference (rare) redoes it
-      float es, gm;
-      if (VEC == 8 && ls.mref > -INFINITY) {  // bf16: the group max from the exact differences
-        float tmax;
-        es = GroupMath<T>::esum_tmax(cur4, ls.nm, c2, tmax);
-        gm = tmax + ls.mref;  // exact: tmax = z* - m_ref exactly
-      } else {
-        es = GroupMath<T>::esum(cur4, ls.nm, c2);
-        gm = GroupMath<T>::gmax(cur4);
+      // The lane's first finite group takes its max as the reference (the only place the max is
+      // taken separately); afterwards one exp-sum pass per group also yields the group max (bf16:
+      // from the exact differences t = z - m_ref).  A group exceeding the reference by > 8 / c
+      // (rare) rebases and runs the same pass again — one copy of the pass in the loop.
+      float gm = -INFINITY, es = 0.f;
+      if (!(ls.mref > -INFINITY)) {
+        const float g0 = GroupMath<T>::gmax(cur4);
+        if (g0 > -INFINITY) ls.rebase(g0, c, inv8);
+        gm = g0;  // (stays -inf / NaN when the group has no finite element)
+      }
+      if (ls.mref > -INFINITY) {
+        for (;;) {
+          float tmax;
+          es = GroupMath<T>::esum_tmax(cur4, ls.nm, c2, tmax);
+          gm = (VEC == 8) ? tmax + ls.mref : GroupMath<T>::gmax(cur4);  // bf16: exact
+          if (!(gm > ls.thr)) break;
+          ls.rebase(gm, c, inv8);
+        }
       }
       ls.bad |= !(gm < INFINITY) ? 1 : 0;  // NaN or +inf in the group
-      if (!(a.dbg & 2)) {
-        const uint32_t key = key16_down(gm);
-        gkr[k * 32 + lane] = (uint16_t)key;
-        const uint32_t skey = __reduce_max_sync(kFull, key);
-        if (lane == 0) gkr[a.Vq / kG + k] = (uint16_t)skey;
+      uint32_t key;
+      if (VEC == 8) {  // bf16 logits: gm is a bf16 value, its key is its bits, order-flipped
+        const uint32_t h = __float_as_uint(gm + 0.0f) >> 16;  // (-0 -> +0)
+        key = (gm != gm) ? 0xFF80u : h ^ ((h & 0x8000u) ? 0xFFFFu : 0x8000u);  // NaN: the +inf key
+      } else {
+        key = key16_down(gm);
       }
+      gkr[k * 32 + lane] = (uint16_t)key;
+      const uint32_t skey = __reduce_max_sync(kFull, key);
+      if (lane == 0) gkr[a.Vq / kG + k] = (uint16_t)skey;
       if (gm > -INFINITY) {
-        if (gm > ls.thr) {
-          ls.rebase(gm, c, inv8);
-          if (!(a.dbg & 1)) es = GroupMath<T>::esum(cur4, ls.nm, c2);
-        }
         ls.acc += (double)es;
         ls.mmax = fmaxf(ls.mmax, gm);
       }
