@@ -226,10 +226,12 @@ __device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n
   const double wi = own ? wv[tid] : 0.0;
   if (own && ci >= F && (tid + 1 == n || top[tid + 1] < F)) ctl[9] = tid + 1;
   const bool complete = (F == 0);
-  double cum = 0.0;  // inclusive pi-order prefix of the weights
-  if (own && status == SAMPLER_ROW_OK && !rc.greedy)
-    for (int j = 0; j <= tid; ++j) cum += wv[j];
+  // inclusive pi-order prefix of the weights: warp scans + the totals of the warps before
+  const int lane = tid & 31, wq = tid >> 5;
+  double cum = warp_incl_scan_d((own && status == SAMPLER_ROW_OK && !rc.greedy) ? wi : 0.0, lane);
+  if (lane == 31) ms.bs.d[wq] = cum;
   cbar();
+  for (int j = 0; j < wq; ++j) cum += ms.bs.d[j];
   BTR(9);
   const int n_exact = ctl[9];
   int n3 = -1;
@@ -297,21 +299,31 @@ __device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n
       } else {
         // the draw: ascending token id over the kept set K3 = top[0..n3), first cumulative > u W
         const double target = u * W;
+        // id order: every kept candidate's rank by id (independent compares), its weight placed
+        // at that rank, one scan, the first rank whose cumulative mass exceeds u W
         const int idi = own ? comp_id(ci) : 0;
+        double* wid = reinterpret_cast<double*>(ms.byid);     // [n3] weights in id order
+        int* idord = reinterpret_cast<int*>(ms.pool + 1024);  // [n3] ids in id order
         if (tid < n3) {
-          double c_in = 0.0;
-          for (int j = 0; j < n3; ++j)
-            if (comp_id(top[j]) <= idi) c_in += wv[j];
-          if (c_in > target) atomicMin(&ctl[8], idi);
+          int rk = 0;
+          for (int j = 0; j < n3; ++j) rk += (comp_id(top[j]) < idi) ? 1 : 0;
+          wid[rk] = wi;
+          idord[rk] = idi;
         }
+        cbar();
+        double ci_ = warp_incl_scan_d((tid < n3) ? wid[tid] : 0.0, lane);
+        if (lane == 31) ms.bs.d[wq] = ci_;
+        cbar();
+        double off = 0.0;
+        for (int j = 0; j < wq; ++j) off += ms.bs.d[j];
+        const double prev = __shfl_up_sync(kFull, ci_, 1);
+        ci_ += off;
+        const double cprev = (lane == 0) ? off : prev + off;
+        if (tid < n3 && ci_ > target && !(cprev > target)) ctl[8] = idord[tid];
         cbar();
         BTR(11);
         int pick = ctl[8];
-        if (pick == UNK) {  // u W at the top of the mass: the last kept id
-          if (tid < n3) atomicMax(&ctl[10], idi);
-          cbar();
-          pick = ctl[10];
-        }
+        if (pick == UNK) pick = idord[n3 - 1];  // u W at the top of the mass: the last kept id
         tok = pick;
         if (tid < n3 && idi == pick) {
           lp = ((double)comp_val(ci) - (double)M) / (double)rc.tau - logS;
