@@ -59,6 +59,15 @@ __device__ __forceinline__ int bucket_of(float z, float M, float c_hi, float c_l
 }
 
 __device__ __forceinline__ uint64_t fixmass(float w) { return (uint64_t)__float2ull_rn(w * (float)kFix); }
+// 64-bit shared-memory add as two native 32-bit atomics with the carry (sm_100 has no native
+// 64-bit shared add: it would be a CAS spin loop); integer, so still order-independent
+__device__ __forceinline__ void smem_add_u64(uint64_t* p, uint64_t v) {
+  uint32_t* p32 = reinterpret_cast<uint32_t*>(p);
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(p32, lo);
+  const uint32_t up = hi + ((uint32_t)(old + lo) < old ? 1u : 0u);
+  if (up) atomicAdd(p32 + 1, up);
+}
 
 // block-wide reductions (512 threads)
 __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, ExSmem& s) {
@@ -219,8 +228,7 @@ __device__ uint64_t radix_in_bucket(ExSmem& s, const BucketCtx& bc, int b, uint6
       const int dig = (int)((c >> d) & 255);
       if (MASS) {
         const float t = z - bc.M;
-        atomicAdd((unsigned long long*)&s.rmass[dig],
-                  (unsigned long long)fixmass(ex2f(fmaf(t, bc.c_hi, t * bc.c_lo))));
+        smem_add_u64(&s.rmass[dig], fixmass(ex2f(fmaf(t, bc.c_hi, t * bc.c_lo))));
       } else {
         atomicAdd(&s.rcnt[dig], 1u);
       }
@@ -275,15 +283,35 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   // ---- pass 0: z' row
   float* zs = a.scratch + (int64_t)r * a.Vp;
   const uint8_t* lrow = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * sizeof(T);
-  for (int i = tid; i < a.Vp; i += kExThreads) {
-    float z;
-    if (i >= a.vloc)
-      z = -INFINITY;
-    else if (sizeof(T) == 2)
-      z = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(lrow)[i] << 16);
-    else
-      z = reinterpret_cast<const float*>(lrow)[i];
-    zs[i] = z;
+  {
+    // 16-byte loads (8 bf16 / 4 f32 per vector; rows are 16-byte aligned, ld * elem % 16 == 0)
+    constexpr int VEC = 16 / (int)sizeof(T);
+    const int nvec = a.Vp / VEC;
+#pragma unroll 4
+    for (int v = tid; v < nvec; v += kExThreads) {
+      const uint4 u = (v * VEC < a.vloc) ? *reinterpret_cast<const uint4*>(lrow + (int64_t)v * 16)
+                                         : make_uint4(0u, 0u, 0u, 0u);
+      float z[VEC];
+      if (sizeof(T) == 2) {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          z[2 * q] = __uint_as_float(w[q] << 16);
+          z[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+        }
+      } else {
+        z[0] = __uint_as_float(u.x);
+        z[1] = __uint_as_float(u.y);
+        z[2] = __uint_as_float(u.z);
+        z[3 % VEC] = __uint_as_float(u.w);
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (v * VEC + e >= a.vloc) z[e] = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4)
+        *reinterpret_cast<float4*>(zs + v * VEC + e) = make_float4(z[e], z[e + 1], z[e + 2], z[e + 3]);
+    }
   }
   __syncthreads();
   {
@@ -331,7 +359,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
         const float y = -x * 64.0f;
         const int b = y >= (float)(kNB - 1) ? kNB - 1 : (y > 0.0f ? (int)y : 0);
         atomicAdd(&s.cnt[b], 1u);
-        atomicAdd((unsigned long long*)&s.mass[b], (unsigned long long)fixmass(ex2f(x)));
+        smem_add_u64(&s.mass[b], fixmass(ex2f(x)));
         ++nfin_loc;
       }
     }
