@@ -190,6 +190,7 @@ __device__ void gather_bucket(ExSmem& s, const BucketCtx& bc, int b, int nb) {
   if (threadIdx.x == 0) s.ints[1] = 0;
   __syncthreads();
   const float4* z4 = reinterpret_cast<const float4*>(bc.zs);
+#pragma unroll 4
   for (int i = threadIdx.x; i < bc.Vp / 4; i += kExThreads) {
     const float4 q = z4[i];
     const float zz[4] = {q.x, q.y, q.z, q.w};
@@ -219,6 +220,7 @@ __device__ uint64_t radix_in_bucket(ExSmem& s, const BucketCtx& bc, int b, uint6
       s.rmass[i] = 0;
     }
     __syncthreads();
+#pragma unroll 4
     for (int i = threadIdx.x; i < bc.Vp; i += kExThreads) {
       const float z = bc.zs[i];
       if (!(z > -INFINITY) || bucket_of(z, bc.M, bc.c_hi, bc.c_lo) != b) continue;
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   __syncthreads();
   int nfin_loc = 0;
   const float4* z4 = reinterpret_cast<const float4*>(zs);
+#pragma unroll 4
   for (int i = tid; i < a.Vp / 4; i += kExThreads) {
     const float4 q = z4[i];
     const float zz[4] = {q.x, q.y, q.z, q.w};
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
       } else {
         // partial mass inside bk via a pass
         double loc = 0.0;
+#pragma unroll 4
         for (int i = tid; i < a.Vp; i += kExThreads) {
           const float z = zs[i];
           if (z > -INFINITY && bucket_of(z, M, rc.c_hi, rc.c_lo) == bk && make_comp(z, a.voff + i) >= Ck) {
@@ -505,15 +509,22 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   C3 = Cm > C3 ? Cm : C3;
 
   // ---- pass 2: draw in ascending id order over K3 = {composite >= C3}
-  const int per = (a.Vp + kExThreads - 1) / kExThreads;
-  const int j0 = tid * per, j1 = min(a.Vp, j0 + per);
+  // (each thread owns a contiguous, 16-byte aligned id range: Vp is a multiple of 4)
+  const int per = ((a.Vp + kExThreads - 1) / kExThreads + 3) / 4 * 4;
+  const int j0 = min(a.Vp, tid * per), j1 = min(a.Vp, j0 + per);
   double loc = 0.0;
-  for (int j = j0; j < j1; ++j) {
-    const float z = zs[j];
-    if (z > -INFINITY && make_comp(z, a.voff + j) >= C3) {
-      const float t = z - M;
-      loc += (double)ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
-    }
+#pragma unroll 2
+  for (int j = j0; j < j1; j += 4) {
+    const float4 q = *reinterpret_cast<const float4*>(zs + j);
+    const float zz[4] = {q.x, q.y, q.z, q.w};
+    float l4 = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (zz[e] > -INFINITY && make_comp(zz[e], a.voff + j + e) >= C3) {
+        const float t = zz[e] - M;
+        l4 += ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
+      }
+    loc += (double)l4;
   }
   double W;
   const double ex = block_excl_scan_d(loc, &W, s);
@@ -523,17 +534,35 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   if (tid == 0) s.ints[4] = 0x7FFFFFFF;
   __syncthreads();
   if (ex <= target && target < ex + loc) {
+    // the same arithmetic as the chunk sum above: float sums of 4, then float64
     double run = ex;
-    for (int j = j0; j < j1; ++j) {
-      const float z = zs[j];
-      if (z > -INFINITY && make_comp(z, a.voff + j) >= C3) {
-        const float t = z - M;
-        run += (double)ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
-        if (run > target) {
-          atomicMin(&s.ints[4], j);
-          break;
+    for (int j = j0; j < j1; j += 4) {
+      float w4[4], l4 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float z = zs[j + e];
+        w4[e] = 0.f;
+        if (z > -INFINITY && make_comp(z, a.voff + j + e) >= C3) {
+          const float t = z - M;
+          w4[e] = ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
         }
+        l4 += w4[e];
       }
+      if (run + (double)l4 > target) {
+        float cf = 0.f;
+        int pick = j + 3;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          cf += w4[e];
+          if (w4[e] > 0.f && run + (double)cf > target) {
+            pick = j + e;
+            break;
+          }
+        }
+        atomicMin(&s.ints[4], pick);
+        break;
+      }
+      run += (double)l4;
     }
   }
   __syncthreads();
