@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       for (int t = 0; t < ntiles; ++t) {
         const int sl = t % kNS;
         const uint64_t tp0 = a.trace ? gtimer() : 0;
-        if (t >= kNS) mbar_wait(empty + sl, (uint32_t)((t / kNS - 1) & 1));
+        if (t >= kNS) mbar_wait_sleep(empty + sl, (uint32_t)((t / kNS - 1) & 1));
         if (a.trace) pwait += gtimer() - tp0;
         const int n = min(kTileSteps, nspan - t * kTileSteps);
         uint32_t bytes = 0;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       uint4 cur4[kG];
       __syncwarp();  // converged before the spin-wait (a diverged lane must not starve behind it)
       const uint64_t tw0 = a.trace ? gtimer() : 0;
-      mbar_wait(full + sl, (uint32_t)((t / kNS) & 1));
+      mbar_wait_sleep(full + sl, (uint32_t)((t / kNS) & 1));
       if (a.trace) wait_ns += gtimer() - tw0;
       const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
       uint32_t pm = bm[(sl * kTileSteps + w) * 32 + lane];
