@@ -496,6 +496,10 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       ms.bs.f[w] = mw;
       ms.bs.i[w] = (int)fw;
     }
+    if (w == kBW - 2 && lane == 0) {  // the draw's uniform, off the critical path
+      const double uu = philox_uniform(seed, prm.request_id, a.step);
+      *reinterpret_cast<double*>(ctl + 14) = uu;
+    }
     if (w == kBW - 1 && nsv >= keff && nsv <= kBT) {
       uint32_t key[8];  // 8 keys per lane at most: nsv <= 256
 #pragma unroll
@@ -680,7 +684,6 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   STR(3);
   bool slow = ctl[2] > kSelQ;
   const int nq = slow ? 0 : ctl[2];
-  const int ns = nus;
   for (int it0 = 0; it0 < nq * kG; it0 += kBT) {  // uniform per warp: aggregated pushes
     const int it = it0 + tid;
     const uint32_t g = (it < nq * kG) ? ql[it >> 2] : 0u;
@@ -688,16 +691,15 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     const bool act = it < nq * kG && v < nvv;
     uint4 u4 = act ? ldg_stream(rowp + (int64_t)v * 16) : make_uint4(Dec<T>::kNegInfWord, Dec<T>::kNegInfWord,
                                                                        Dec<T>::kNegInfWord, Dec<T>::kNegInfWord);
+    // the vector's penalised elements from the slot's presence bitmap (HistState::pmask), loaded
+    // alongside the logits
+    const int vk = v / kStepVec, vd = v - vk * kStepVec;
+    const uint32_t pmw = act ? a.hs.pmask[((int64_t)slot * a.hs.spr + vk) * 32 + (vd & 31)] : 0u;
     if (it0 == 0) term = s_terms();  // the float64 softmax terms, while the re-read is in flight
-    uint32_t msk = listed_mask<VEC>(s_ue, ns, a.voff + v * VEC);
+    uint32_t msk = (pmw >> ((vd >> 5) * VEC)) & ((1u << VEC) - 1u);
 #pragma unroll
     for (int t = 0; t < VEC; ++t)
       if (v * VEC + t >= a.vloc) msk |= 1u << t;
-    if (nu > kSelPen)  // very long tables: the tail entries are in global memory only
-      for (int e = kSelPen; e < nu; ++e) {
-        const int k = utab[e].id - a.voff - v * VEC;
-        if (k >= 0 && k < VEC) msk |= 1u << k;
-      }
     if (msk) u4 = Dec<T>::mask(u4, msk);
     uint32_t sel = 0;
 #pragma unroll
@@ -730,7 +732,6 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   // (each placed candidate's weight w = exp((z - M)/tau) in float64 is computed here, in
   // parallel, for the decision)
   const int nc = min(ctl[1], kPool);
-  const double inv_tau = 1.0 / (double)rc.tau;
   for (int i = tid; i < nc; i += kBT) {
     const uint64_t c = ms.pool[i];
     int rank = 0, j = 0;
@@ -774,7 +775,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   // ---- decision (whole block, candidate-parallel)
   STR(20);
   if (tid == 0) ctl[10] = -1;
-  const double u = philox_uniform(seed, prm.request_id, a.step);
+  const double u = *reinterpret_cast<const double*>(ctl + 14);  // (warp kBW - 2, earlier)
   STR(21);
   const int32_t tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
   STR(6);
