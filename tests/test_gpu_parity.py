@@ -117,6 +117,33 @@ def test_determinism_bit_identical():
         assert torch.equal(a[k], b[k]), k
 
 
+def test_cuda_graph_replay_equals_eager_and_oracle():
+    """bench.py replays the step from CUDA graphs: a captured step (programmatic dependent launch
+    inside the graph, in-kernel history append) must give the eager call's bits, and the oracle's
+    tokens on the grown histories."""
+    import torch
+    wl = make_workload("c3", B=64)
+    x = device_logits(wl)
+    se = make_sampler(wl, max_history=1024)
+    sg = make_sampler(wl, max_history=1024)
+    oute = [{k: v.clone() for k, v in se.sample(x, i, append=True).items()} for i in range(3)]
+    outg = sg._outs(wl.B, None)
+    res = []  # (the step id is baked into a graph: one graph per step)
+    for i in range(3):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+            sg.sample(x, i, append=True, out=outg)
+        g.replay()
+        torch.cuda.synchronize()
+        res.append({k: v.clone() for k, v in outg.items()})
+    for i in range(3):
+        for k in ("tokens", "logprobs", "filtered_logprobs", "status"):
+            assert torch.equal(oute[i][k], res[i][k]), (i, k)
+    # histories grew identically
+    for b in (0, 17, 63):
+        assert se.get_history(b) == sg.get_history(b)
+
+
 def test_history_append_matches_sequential_oracle():
     """Decode 6 steps with in-kernel history append; the oracle replays with the grown history."""
     import torch
