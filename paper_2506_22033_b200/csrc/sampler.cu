@@ -495,11 +495,22 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
 static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
   if (h->d_trace)
     CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)h->cfg.max_batch), st));
+  // programmatic dependent launch: the grid may be scheduled while the previous kernel of the
+  // stream finishes (the kernel waits for it before touching memory, stream.cuh)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.dynamicSmemBytes = kStreamSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (h->cfg.logits_dtype == SAMPLER_BF16)
-    stream_kernel<__nv_bfloat16><<<grid, kStreamThreads, kStreamSmem, st>>>(a);
+    CK(h, cudaLaunchKernelEx(&cfg, stream_kernel<__nv_bfloat16>, a));
   else
-    stream_kernel<float><<<grid, kStreamThreads, kStreamSmem, st>>>(a);
-  CK(h, cudaGetLastError());
+    CK(h, cudaLaunchKernelEx(&cfg, stream_kernel<float>, a));
   return SAMPLER_OK;
 }
 

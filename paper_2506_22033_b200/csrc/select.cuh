@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     ctl[5] = 0;
   }
   griddep_wait();  // phase A's hand-off, partial records and keys are visible from here on
+  griddep_launch();  // the next step's phase A may be scheduled as these CTAs retire (it waits)
   // ---- RT1 (one round trip, nothing indexed by slot): the hand-off, the penalised entries, the
   // partial records, the step keys and the group keys of row r
   RowHand* s_hand = reinterpret_cast<RowHand*>(smem + kSOffHand);

@@ -247,7 +247,12 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   float2* segc = reinterpret_cast<float2*>(smem + kSOffSeg);  // per row of the span: (c, 8 / c)
   const uint4 kNegInfVec = make_uint4(Dec<T>::kNegInfWord, Dec<T>::kNegInfWord, Dec<T>::kNegInfWord,
                                       Dec<T>::kNegInfWord);
-  griddep_launch();  // phase B's CTAs may be scheduled as this grid's CTAs retire
+  // programmatic dependent launch on both sides: this grid may have been launched while the
+  // previous kernel of the stream (the last step's phase B) was still running — wait for it before
+  // any memory access (it appends to the histories this pass reads, and reads the scratch this
+  // pass writes); then let phase B's CTAs be scheduled as this grid's CTAs retire
+  griddep_wait();
+  griddep_launch();
   const int64_t s0 = (int64_t)blockIdx.x * a.span;
   const int nspan = (int)min((int64_t)a.span, a.nsteps - s0);  // steps of this CTA
   const int ntiles = (nspan + kTileSteps - 1) / kTileSteps;
