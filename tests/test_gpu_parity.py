@@ -67,6 +67,14 @@ def test_random_params_ragged_shapes(V, ld, dtype):
     assert_parity(wl, out, oracle_run(wl, 11))
 
 
+@pytest.mark.parametrize("cfg", ["c3", "c2", "c1"])
+def test_linear_penalty_mode(cfg):
+    """The paper-literal subtractive penalty (R1 LINEAR)."""
+    wl = make_workload(cfg, B=min(16, make_workload(cfg).B))
+    s, out = _run(wl, step=3, mode=1)
+    assert_parity(wl, out, oracle_run(wl, 3, mode=1))
+
+
 def test_greedy_and_topk1_bit_exact_with_ties():
     rng = np.random.default_rng(5)
     B, V = 64, 20000
