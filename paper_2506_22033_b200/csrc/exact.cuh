@@ -1,7 +1,7 @@
 // exact.cuh — exact multi-pass path for rows whose kept set is not bounded by the one-pass
 // candidates (top-p / min-p-only rows with large nuclei, unfiltered rows, top_k > K_cand).
 //
-// One CTA (512 threads) per pending row; M and S come from the streaming pass.
+// One CTA (1024 threads) per pending row; M and S come from the streaming pass.
 //   pass 0  materialise z' (penalties applied, binary32) into a per-row fp32 scratch row
 //   pass 1  2048-bucket histogram of counts and fixed-point masses, bucket = floor(-x*64) with
 //           x = (z'-M)*log2(e)/tau (1/64-octave buckets of the weight; contiguous in pi order)
@@ -18,7 +18,7 @@
 
 namespace smp {
 
-constexpr int kExThreads = 512;
+constexpr int kExThreads = 1024;
 constexpr int kNB = 2048;
 constexpr int kCapG = 4096;
 constexpr double kFix = 17592186044416.0;  // 2^44 fixed-point scale for masses (w <= 1)
