@@ -120,7 +120,7 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
 // outputs + RowInfo.  Returns the sampled token when the row's status is OK, else -1.
 // Candidates live in registers (candidate i = lane + 32q); the id-order cumulative mass of each
 // kept candidate is accumulated by broadcasting every kept (id, w) once — no sort, no barrier.
-__device__ __noinline__ int warp_decide(const MergeSmem& ms, int n, float M, double S, uint64_t F, bool bad,
+__device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, double S, uint64_t F, bool bad,
                                         const RowCfg& rc, const sampling_params& p, uint64_t seed, uint64_t step,
                                         int row, const RowOut& ro, bool pending_ok, uint64_t* tr,
                                         bool pre = false, double logS_pre = 0.0, double u_pre = 0.0) {

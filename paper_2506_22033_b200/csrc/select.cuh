@@ -778,7 +778,10 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   if (tid == 0) ctl[10] = -1;
   const double u = *reinterpret_cast<const double*>(ctl + 14);  // (warp kBW - 2, earlier)
   STR(21);
-  const int32_t tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
+  int32_t tok;
+  {
+    tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
+  }
   STR(6);
   if (!a.append || tok < 0) return;
   if (nu > kSelPen) {
