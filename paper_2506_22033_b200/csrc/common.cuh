@@ -127,19 +127,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-// wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase completes
-// (or the hint expires) instead of spinning on the issue port
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+// wait with back-off: a warp whose tile is not ready sleeps between polls instead of spinning on
+// the issue port (the consumer warps of a CTA share their sub-partitions with the busy ones)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 128) {
   uint32_t done;
-  do {
+  for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) break;
+    __nanosleep(ns);
+  }
 }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
