@@ -402,7 +402,6 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   }
   cbar_n<kCW * 32>();  // the span's row constants are in smem
 
-  uint64_t wait_ns = 0;  // (trace: time this warp spent waiting for its tiles)
   int cur = -1;  // row being accumulated
   LaneSum ls;
   ls.reset();
@@ -442,9 +441,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       const int vb = k * kStepVec;
       uint4 cur4[kG];
       __syncwarp();  // converged before the spin-wait (a diverged lane must not starve behind it)
-      const uint64_t tw0 = a.trace ? gtimer() : 0;
       mbar_wait_sleep(full + sl, (uint32_t)((t / kNS) & 1));
-      if (a.trace) wait_ns += gtimer() - tw0;
       const uint4* tile = reinterpret_cast<const uint4*>(ring + sl * (kTileSteps * kStepBytes) + w * kStepBytes);
       uint32_t pm = bm[(sl * kTileSteps + w) * 32 + lane];
       if (vb + kStepVec <= nvv) {
@@ -512,7 +509,6 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
     }
   }
   if (cur >= 0) flush();
-  if (a.trace && lane == 0) a.trace[blockIdx.x * 64 + 16 + w] = wait_ns;  // (kCW <= 48)
   if (a.trace && tid == 0) a.trace[blockIdx.x * 64 + 7] = gtimer();
 }
 
