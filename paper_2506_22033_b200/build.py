@@ -38,20 +38,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile sampler.cu into `out` (default: the in-tree library).  `extra` nvcc flags are for
+    tools/variants.sh (A/B builds of the tuning constants), not for the product build."""
+    if not force and out == LIB and not extra and up_to_date():
         return LIB
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC", *extra,
            "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp", os.path.join(CSRC, "sampler.cu")]
+           "-o", out + ".tmp", os.path.join(CSRC, "sampler.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libsampler_b200.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -247,6 +247,15 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     sampler_destroy(h);
     return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
   }
+#ifdef SMP_CARVEOUT
+  // one L1/shared split for every kernel of the step: no reconfiguration at the kernel boundaries
+  cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(select_rows_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(select_rows_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+#endif
   if (getenv("SAMPLER_DBG")) h->dbg = atoi(getenv("SAMPLER_DBG"));
   if (getenv("SAMPLER_TRACE")) {
     if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;

@@ -6,7 +6,7 @@
 //     ring of kNS tiles of 16 steps (32 KB each), full / empty mbarriers;
 //     next to each run of logits, the same steps' words of the slot's penalty presence bitmap
 //     (HistState::pmask — the support of the paper's incremental penalty buffers);
-//   * 24 consumer warps: warp w takes step w of every tile (4 vectors = 32 bf16 / 16 f32 logits per
+//   * 26 consumer warps: warp w takes step w of every tile (4 vectors = 32 bf16 / 16 f32 logits per
 //     lane); penalised ids and the padding tail are masked to -inf in registers (the penalised
 //     elements enter phase B as exact single values); then per lane and step (a "group"):
 //       - the group max by a NaN-propagating packed max tree (bf16x2 HMNMX2), its order-preserving
@@ -29,10 +29,16 @@
 namespace smp {
 
 // ---- geometry of phase A (persistent CTAs, warp-specialised) ----------------------
-constexpr int kCW = 24;                    // consumer warps per CTA (one step of each tile each)
+#ifndef SMP_KCW
+#define SMP_KCW 26
+#endif
+#ifndef SMP_KNS
+#define SMP_KNS 3
+#endif
+constexpr int kCW = SMP_KCW;               // consumer warps per CTA (one step of each tile each)
 constexpr int kStreamCtasPerSm = 1;        // CTAs (independent pipelines) per SM
-constexpr int kTileSteps = kCW;            // steps per ring tile (24 x 2 KB = 48 KB)
-constexpr int kNS = 4;                     // ring tiles (192 KB of bulk copies in flight per SM)
+constexpr int kTileSteps = kCW;            // steps per ring tile (26 x 2 KB = 52 KB)
+constexpr int kNS = SMP_KNS;               // ring tiles (3 x 52 KB; 3 beat 4 and 2 at c3: tools/variants.py)
 constexpr int kMaxSeg = 48;                // rows per CTA span (the host caps the span)
 constexpr int kStreamThreads = (kCW + 2) * 32;  // + producer warp + penalty warp
 constexpr int kStepBytes = kStepVec * 16;
