@@ -727,7 +727,12 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   if (slow) floor = select_collect_slow<T>(a, rowp, utab, s_ue, nu, nus, prm, Tv, lo_k, nvv, gwords, keff, ms, ctl, ql);
   }
   const double S = block_sum_d(term, ms.bs);  // (its barriers also close the collection)
-  const double logS = dlog_call(S);
+  // log S (only the decision's writer needs it): the last warp computes it while the others rank
+  // the pool; read after the rank barrier
+  if (tid >= kBT - 32) {
+    const double l = dlog_call(S);
+    if (tid == kBT - 1) *reinterpret_cast<double*>(ctl + 12) = l;
+  }
   STR(4);
   // ---- exact top-K of the pool by rank counting
   // (each placed candidate's weight w = exp((z - M)/tau) in float64 is computed here, in
@@ -777,6 +782,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   STR(20);
   if (tid == 0) ctl[10] = -1;
   const double u = *reinterpret_cast<const double*>(ctl + 14);  // (warp kBW - 2, earlier)
+  const double logS = *reinterpret_cast<const double*>(ctl + 12);
   STR(21);
   int32_t tok;
   {
