@@ -75,8 +75,8 @@ constexpr int kSelectSmem = kSOffZp + kSelPen * 4;
 
 
 // Append `tok` to the slot's history (P:371 incremental update) from the smem copy of the sorted
-// unique-token table s_ue[0..nu) (nu <= kSelPen): one block-wide count, then every entry above the
-// insertion point is stored one slot up straight from smem.
+// unique-token table s_ue[0..nu) (nu <= kSelPen): the insertion point by binary search, then every
+// entry above it is stored one slot up straight from smem.
 __device__ __forceinline__ void block_append_smem(const HistState& hs, int slot, int32_t tok, const SlotMeta& sm,
                                                   const UniqEntry* s_ue, const BlockScratch& bs) {
   const int tid = threadIdx.x;
@@ -85,11 +85,16 @@ __device__ __forceinline__ void block_append_smem(const HistState& hs, int slot,
     if (tid == 0) hs.meta[slot].flags |= 1;
     return;
   }
-  int cl = 0;
-  for (int i = tid; i < nu; i += kBT) cl += (s_ue[i].id < tok ? 1 : 0) + (s_ue[i].id == tok ? (1 << 20) : 0);
-  const int cs = block_sum_i(cl, bs);
-  const int less = cs & ((1 << 20) - 1);
-  const bool found = (cs >> 20) != 0;
+  // insertion point by binary search of the id-sorted table, in every thread (smem broadcasts,
+  // no block barrier)
+  int lo = 0, hi = nu;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s_ue[mid].id < tok) lo = mid + 1;
+    else hi = mid;
+  }
+  const int less = lo;
+  const bool found = less < nu && s_ue[less].id == tok;
   UniqEntry* u = hs.uniq + (int64_t)slot * hs.L;
   if (found) {
     if (tid == 0) u[less].meta = s_ue[less].meta + 2u;
