@@ -27,7 +27,9 @@
 namespace smp {
 
 constexpr int kSelPen = 2048;          // unique-token entries staged in smem
-constexpr int kSelPR = kSelPen / kBT;  // raw penalised logits per thread (prefetch)
+constexpr int kSelSpec = 1024;         // penalised entries loaded speculatively in RT1 (the rest, if
+                                       // n_uniq is larger, after the hand-off arrives)
+constexpr int kSelPR = kSelSpec / kBT;  // per thread
 constexpr int kSelQ = 2048;            // qualifying-group list capacity
 constexpr int kSelGR = 3;              // group-key words (8 keys) per thread per chunk
 
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   RowHand* s_hand = reinterpret_cast<RowHand*>(smem + kSOffHand);
   if (tid < (int)(sizeof(RowHand) / 16))
     reinterpret_cast<uint4*>(s_hand)[tid] = reinterpret_cast<const uint4*>(a.hand + r)[tid];
-  const int ncap = min(a.hs.L, kSelPen);  // entries loaded speculatively (nu is in the hand-off)
+  const int ncap = min(a.hs.L, kSelSpec);  // entries loaded speculatively (nu is in the hand-off)
   float* s_zp = reinterpret_cast<float*>(smem + kSOffZp);
   {
     uint4 x[kSelPR];  // every load in flight before the first use
@@ -460,6 +462,18 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   const SlotMeta smeta = s_hand->meta;
   const int nu = smeta.n_uniq;
   const int nus = min(nu, kSelPen);
+  if (nus > ncap) {  // (uniform) a long history: the rest of the smem-staged entries
+    const uint4* src = reinterpret_cast<const uint4*>(a.pent + (int64_t)r * a.hs.L);
+    for (int e = ncap + tid; e < nus; e += kBT) {
+      const uint4 x = src[e];
+      UniqEntry ue;
+      ue.id = (int32_t)x.x;
+      ue.meta = x.y;
+      s_ue[e] = ue;
+      s_zp[e] = __uint_as_float(x.z);
+    }
+    cbar();
+  }
   const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
   const uint8_t* rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
   // the penalised entries: smem copy of the table (id order) for masking and the append, and the

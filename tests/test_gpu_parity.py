@@ -307,3 +307,27 @@ def test_adversarial_floods_all_equal_and_increasing():
     assert_parity(wl, out, orc, q=out["q"])
     s, out = _run(wl, step=2)
     assert_parity(wl, out, oracle_run(wl, 2))
+
+
+@pytest.mark.parametrize("n_hist", [700, 1800, 5000])
+def test_long_histories_penalties(n_hist):
+    """Unique-token tables beyond the speculative RT1 load (1024 entries), beyond the smem staging
+    (2048: the selection reads the table from global), with all three penalties and top-k / top-p /
+    min-p rows."""
+    rng = np.random.default_rng(11 + n_hist)
+    B, V = 8, 20000
+    z = gen_logits(rng, B, V, "bf16")
+    prompts, outputs = [], []
+    for b in range(B):
+        h = rng.choice(V, size=n_hist, replace=b % 2 == 0).tolist()
+        prompts.append(h[: n_hist // 2])
+        outputs.append(h[n_hist // 2:])
+    params = []
+    for b in range(B):
+        params.append(RowParams(temperature=0.8, top_k=[0, 40, 128, 5][b % 4], top_p=[0.9, 1.0, 0.95, 1.0][b % 4],
+                                min_p=[0.0, 0.0, 0.02, 0.1][b % 4], repetition_penalty=1.3, presence_penalty=0.4,
+                                frequency_penalty=0.2, seed=100 + b, request_id=b))
+    wl = Workload("longhist", B, V, "bf16", z, prompts, outputs, params)
+    orc = oracle_run(wl, step=3)
+    s, out = _run(wl, step=3)
+    assert_parity(wl, out, orc)
