@@ -34,7 +34,7 @@ def main():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     vec = 8 if wl.dtype == "bf16" else 4
     spr = -(-(-(-wl.V // vec)) // 128)
-    nA = 64 * (wl.B * spr // int(os.environ.get("TILE_STEPS", "24")) + 1)
+    nA = 64 * (wl.B * spr // int(os.environ.get("TILE_STEPS", "26")) + 1)
     n = nA + 32 * wl.B
     buf = (ctypes.c_uint64 * n)()
     rc = smod._lib.sampler_debug_trace(s.h, buf, n)
