@@ -129,7 +129,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // wait with back-off: a warp whose tile is not ready sleeps between polls instead of spinning on
 // the issue port (the consumer warps of a CTA share their sub-partitions with the busy ones)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 128) {
+#ifndef SMP_SLEEP_NS
+#define SMP_SLEEP_NS 128  // back-off of the ring waits (tools/variants.py: 32-512 tried)
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = SMP_SLEEP_NS) {
   uint32_t done;
   for (;;) {
     asm volatile(
