@@ -226,7 +226,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2506_22033_b200 import Sampler
-    from tests._helpers import device_logits
+    from workloads.synth import device_logits
     from workloads.synth import make_workload
 
     rank, world, local = dist_env()

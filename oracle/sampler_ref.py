@@ -42,7 +42,12 @@ ROW_NONFINITE = 1   # a NaN or +inf logit in the row
 ROW_ALL_NEG_INF = 2  # no token has positive weight
 
 GREEDY_EPS = 1e-5    # DESIGN.md R5: tau < 1e-5 (incl. 0) => greedy
-FLAG_EPS = 1e-6      # north star: boundary margin that excuses a row
+FLAG_EPS = 1e-6      # north star: "within 1e-6 of a CDF or tie boundary" (reported: RowResult.flagged6)
+FLAG_EPS_GPU = 1e-9  # DESIGN.md R16: the excuse band actually applied (RowResult.flagged).  Both sides
+                     # compute kept-set weights and prefix sums in float64 (error <= V * 2^-53 * W,
+                     # < 2e-11 * W for V <= 2e5), so a token may differ only when a boundary lies within
+                     # this band; the north star's 1e-6 is its upper limit, not its value (at 1e-6 a
+                     # 1e5-token nucleus is flagged in ~20% of draws, against the < 1e-4 bar)
 
 
 @dataclass
@@ -72,7 +77,9 @@ class RowResult:
     u: float = float("nan")
     kept: np.ndarray | None = None        # K3, ascending ids
     q: np.ndarray | None = None           # final filtered distribution over V
-    flags: dict = field(default_factory=dict)
+    flags: dict = field(default_factory=dict)       # band FLAG_EPS_GPU (the excuse; R16)
+    flagged6: bool = False                          # any boundary within FLAG_EPS (north star literal)
+    flags6: dict = field(default_factory=dict)
 
 
 def f32(x):
@@ -249,17 +256,24 @@ def sample_row(raw_row, dtype: str, prompt, output, p: Params, step: int,
     tok, W, Ct, Cp = draw_from(K3, w, u)
     lp = (zp[tok] - M) / tau - math.log(S)                   # step 8 / R12
     flp = math.log(w[tok] / W)
-    # step 10: boundary flags that excuse a token mismatch
+    # step 10: boundary flags that excuse a token mismatch, at two bands
     pf = float(np.float32(p.top_p))
-    if pf < 1.0 and c is not None:
-        tgt = pf * W1
-        fl = abs(c[j] - tgt) <= FLAG_EPS * W1 or (j > 0 and abs(c[j - 1] - tgt) <= FLAG_EPS * W1)
-        flags["top_p"] = bool(fl)
-    if mp > 0.0:
-        flags["min_p"] = bool(np.any(np.abs(w[K2] - mp) <= FLAG_EPS))
-    tgt = u * W
-    flags["draw"] = bool(abs(Ct - tgt) <= FLAG_EPS * W or abs(Cp - tgt) <= FLAG_EPS * W)
-    res = RowResult(tok, lp, flp, ROW_OK, any(flags.values()), False, M, S, u, np.sort(K3), flags=flags)
+
+    def boundary_flags(eps):
+        fl = {}
+        if pf < 1.0 and c is not None:
+            tgt = pf * W1
+            fl["top_p"] = bool(abs(c[j] - tgt) <= eps * W1 or (j > 0 and abs(c[j - 1] - tgt) <= eps * W1))
+        if mp > 0.0:
+            fl["min_p"] = bool(np.any(np.abs(w[K2] - mp) <= eps))
+        tgt = u * W
+        fl["draw"] = bool(abs(Ct - tgt) <= eps * W or abs(Cp - tgt) <= eps * W)
+        return fl
+
+    flags = boundary_flags(FLAG_EPS_GPU)
+    flags6 = boundary_flags(FLAG_EPS)
+    res = RowResult(tok, lp, flp, ROW_OK, any(flags.values()), False, M, S, u, np.sort(K3), flags=flags,
+                    flagged6=any(flags6.values()), flags6=flags6)
     if want_q:
         q = np.zeros(V)
         q[K3] = w[K3] / W

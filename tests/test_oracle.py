@@ -301,3 +301,93 @@ def test_exact_boundaries_ge_semantics():
     w = np.ones(4)
     assert draw_from(np.arange(4), w, 0.25)[0] == 1   # C = 1,2,.. ; u*W = 1.0; first C > 1 -> id 1
     assert draw_from(np.arange(4), w, 0.0)[0] == 0
+
+
+# ----------------------------------------------------------------------------- pins added in round 2
+def _kat_rows():
+    rows = []
+    for line in open(os.path.join(GOLD, "philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        rows.append([int(x, 16) for x in line.split()])
+    return rows
+
+
+def test_uniform_word_and_counter_mapping_from_kat():
+    """DESIGN.md R11 / SURVEY §8c-9: key = (seed_lo, seed_hi), counter = (step_lo, step_hi,
+    request_lo, request_hi), u = ((x1 << 32 | x0) >> 11) * 2^-53.  Each published Random123 vector
+    is re-read as a (seed, request, step) triple, so a swapped word, counter slot or shift in
+    uniform() fails here (the KAT test above only pins philox4x32_10 itself)."""
+    for w in _kat_rows():
+        c0, c1, c2, c3, k0, k1, x0, x1 = w[:8]
+        seed = (k1 << 32) | k0
+        step = (c1 << 32) | c0
+        req = (c3 << 32) | c2
+        expect = (((x1 << 32) | x0) >> 11) * 2.0 ** -53
+        assert uniform(seed, req, step) == expect
+    # the first vector written out: all-zero key and counter -> x0 = 0x6627e8d5, x1 = 0xe169c58d
+    assert uniform(0, 0, 0) == ((0xE169C58D << 32 | 0x6627E8D5) >> 11) * 2.0 ** -53
+
+
+def test_decode_bf16_all_bit_patterns_match_torch():
+    """Step 1 for dtype 'bf16' against torch's bfloat16 -> float64 conversion on
+    every one of the 65536 bit patterns (NaN patterns compared as NaN)."""
+    import torch
+    from oracle import decode_logits
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    ours = decode_logits(bits, "bf16")
+    ref = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).to(torch.float64).numpy()
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(ours), nan)
+    assert np.array_equal(ours[~nan], ref[~nan])
+    # signed zeros and infinities keep their sign
+    assert np.array_equal(np.signbit(ours[~nan]), np.signbit(ref[~nan]))
+
+
+def _p(**kw):
+    return Params(**kw)
+
+
+def test_flags_top_p_boundary_both_bands():
+    """SURVEY §8c-10 top-p flag: |c_j - p*W1| <= eps*W1 (or the same for c_{j-1}).  1024 equal
+    logits give w = 1 exactly, so W1 = 1024 and c_j = j + 1 exactly; p = 2^-10 + m*2^-33 is exact in
+    binary32 and puts p*W1 exactly m*2^-23 above c_0 = 1: the gap is known to the last bit."""
+    from oracle.sampler_ref import FLAG_EPS, FLAG_EPS_GPU
+    z = np.zeros(1024, np.float32)
+    for m, f6, fg in ((4, True, True), (4000, True, False), (20000, False, False)):
+        p = 2.0 ** -10 + m * 2.0 ** -33
+        assert float(np.float32(p)) == p
+        gap = m * 2.0 ** -23 / 1024.0                   # |c_0 - p*W1| / W1
+        assert (gap <= FLAG_EPS) == f6 and (gap <= FLAG_EPS_GPU) == fg
+        r = run(z, _p(temperature=1.0, top_p=p, seed=3), u=0.7)
+        assert list(r.kept) == [0, 1]                    # c_0 = 1 < p*W1 <= c_1 = 2
+        assert r.flags6["top_p"] == f6 and r.flags["top_p"] == fg, (m, r.flags6, r.flags)
+        assert r.flagged6 == f6 and r.flagged == fg      # u = 0.7 is far from the draw boundary
+
+
+def test_flags_min_p_boundary_both_bands():
+    """min-p flag: some kept w_v within eps of min_p (absolute: w_max = 1).  The element's weight is
+    w = e^-14 (logit -14 exact in binary32, max 0); min_p is a binary32 a known distance from it
+    (near 2^-20 the binary32 spacing is 2^-44, far below both bands)."""
+    from oracle.sampler_ref import FLAG_EPS, FLAG_EPS_GPU
+    w1 = math.exp(-14.0)
+    z = np.array([0.0, -14.0, -30.0], np.float32)
+    for dist, f6, fg in ((4e-10, True, True), (-4e-10, True, True), (5e-7, True, False), (2e-6, False, False)):
+        mp = float(np.float32(w1 + dist))
+        d = abs(w1 - mp)
+        assert abs(d - abs(dist)) < 1e-12
+        r = run(z, _p(temperature=1.0, min_p=mp, seed=1), u=0.3)
+        assert r.flags6["min_p"] == f6 and r.flags["min_p"] == fg, (dist, r.flags6, r.flags)
+        assert (1 in r.kept.tolist()) == (w1 >= mp)
+        assert 2 not in r.kept.tolist()                  # w = e^-30 < min_p
+
+
+def test_flags_draw_boundary_both_bands():
+    """draw flag: |C_tok - u*W| or |C_prev - u*W| <= eps*W, with u passed in explicitly."""
+    z = np.array([0.0, 0.0, 0.0, 0.0], np.float32)     # w = 1 each, W = 4, C = 1, 2, 3, 4
+    for du, f6, fg in ((2e-7, True, False), (2e-10, True, True), (-2e-10, True, True), (1e-3, False, False)):
+        u = 0.5 + du                                   # u*W = 2 + 4*du: next to C = 2
+        r = run(z, _p(temperature=1.0, seed=1), u=u)
+        assert r.flags6["draw"] == f6 and r.flags["draw"] == fg, (du, r.flags6, r.flags)
+        assert r.token == (2 if du > 0 else 1)
+        assert r.flagged == fg and r.flagged6 == f6

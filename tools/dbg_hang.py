@@ -2,7 +2,7 @@ import sys, time, os
 sys.path.insert(0, os.getcwd())
 import torch
 from paper_2506_22033_b200 import Sampler
-from tests._helpers import device_logits
+from workloads.synth import device_logits
 from workloads.synth import make_workload
 for B in [int(x) for x in os.environ.get("BS", "8,64,256").split(",")]:
     wl = make_workload("c3", B=B)

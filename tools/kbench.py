@@ -46,7 +46,7 @@ def ktimes(s, fn, xs, iters=30, warm=3):
 def c3_bench(nbuf=5, append=True):
     """The bench.py c3 workload (synthetic logits + histories + params), per-kernel times."""
     from workloads.synth import make_workload
-    from tests._helpers import device_logits
+    from workloads.synth import device_logits
     wls = [make_workload("c3", seed_offset=i) for i in range(nbuf)]
     wl = wls[0]
     s = Sampler(wl.V, wl.B, max_history=2048, max_top_k=128, dtype=wl.dtype)

@@ -14,7 +14,7 @@ import torch
 
 from paper_2506_22033_b200 import Sampler
 from paper_2506_22033_b200 import sampler as smod
-from tests._helpers import device_logits
+from workloads.synth import device_logits
 from workloads.synth import make_workload
 
 

@@ -200,3 +200,20 @@ def random_params(rng: np.random.Generator, b: int, V: int) -> RowParams:
         p.presence_penalty = float(rng.choice([0.0, 0.4, -0.2]))
         p.frequency_penalty = float(rng.choice([0.0, 0.3, 0.05]))
     return p
+
+
+def device_logits(wl: Workload, ld=None, device="cuda"):
+    """The workload's logits as a torch CUDA tensor [B, V] (row stride ld >= V when given).
+    Placement only (no arithmetic of the method); used by tests, smoke() and bench.py."""
+    import torch
+    ld = wl.V if ld is None else ld
+    if wl.dtype == "bf16":
+        buf = np.zeros((wl.B, ld), dtype=np.uint16)
+        buf[:, :wl.V] = wl.raw
+        t = torch.from_numpy(buf.view(np.int16)).view(torch.bfloat16)
+    else:
+        buf = np.zeros((wl.B, ld), dtype=np.float32)
+        buf[:, :wl.V] = wl.raw
+        t = torch.from_numpy(buf)
+    t = t.to(device)
+    return t[:, :wl.V] if ld != wl.V else t
