@@ -1,0 +1,870 @@
+// rowres.cuh — the sampling step as one persistent cluster kernel with the rows resident in
+// distributed shared memory (DSMEM).
+//
+// The batch [B x V] is cut by rows: a thread-block cluster of C CTAs takes one row at a time, CTA c
+// holding the row's vocabulary chunk [c*Lc, (c+1)*Lc) in its shared memory (1-D bulk copies, TMA
+// engine).  Every pass of the row then runs from shared memory, and the row crosses HBM exactly
+// once (the logits z_s of the last stage).  Per CTA and row (one "row group" of 4 warps):
+//   pen     the penalised ids of the chunk (presence bitmap + the slot's unique-token entries of
+//           the chunk, located by the per-slot prefix table) get their exact penalised value
+//           z' = ApplyPenalty(z, y_<s) (R1-R3); in the chunk they
+//           are masked to -inf, so the bulk passes below see only unpenalised logits;
+//   A1      max over the chunk (NaN-propagating: NaN / +inf rows are detected for free) and one
+//           max per thread;  T_c = the keff-th largest thread max (keff = top-k, or 1 for greedy):
+//           keff distinct elements are >= T_c, so every element of the row's top-k in this chunk
+//           is >= T_c;
+//   A2      S_c = sum 2^((z' - m_c) log2(e)/tau) (P:149's softmax denominator, relative to the
+//           chunk max m_c: every term <= 1, no rebasing), and every element >= T_c pushed
+//           straight into the leader CTA's candidate list (DSMEM stores);
+//   send    the chunk record {m_c, S_c, frontier, count} to the row's leader, CTA (row index mod C),
+//           one remote mbarrier arrive.
+// The leader's decider warp merges the C records (M = max m_c, S = sum S_c 2^((m_c - M) c),
+// frontier = max, candidates >= frontier), takes the exact top-k by (z' desc, id asc), and runs the
+// decision of merge.cuh (top-k -> top-p -> min-p in float64, Philox draw in id order, logprobs,
+// history append) while the row groups already stream the next rows: a row's decision overlaps
+// the streaming of the C-1 rows after it.  Two row groups per CTA, each with its own buffer, keep
+// two rows in flight per SM (one group's latency-bound steps overlap the other's passes).
+// Rows whose kept set is not bounded by the candidates (top-p / min-p-only, unfiltered, top_k >
+// K_cand) leave a pending RowInfo {M, S} for exact.cuh.  Mode 1 (vocab-sharded phase 1) writes the
+// row's candidate record instead of deciding.
+#pragma once
+#include "common.cuh"
+#include "elem.cuh"
+#include "merge.cuh"
+#include "philox.cuh"
+
+namespace smp {
+
+constexpr int kRNG = 2;                     // row groups (= chunk buffers) per CTA
+constexpr int kRWG = 4;                     // warps per row group
+constexpr int kRGT = kRWG * 32;             // threads per row group
+constexpr int kRThreads = kRNG * kRGT + 64; // + producer warp + decider warp
+constexpr int kRProdW = kRNG * kRWG;        // producer warp index
+constexpr int kRDecW = kRProdW + 1;         // decider warp index
+constexpr int kRPen = 512;                  // penalised entries staged per chunk (more: handled in-loop)
+constexpr int kRCMax = 16;                  // max cluster size
+constexpr int kRPool = 1024;                // decider candidate pool
+constexpr int kLcAlign = 128;               // chunk length granularity (16-byte bitmap rows, 16-byte copies)
+
+// per-row staging, written by the producer next to the bulk copies of the chunk
+struct __align__(16) RowStage {
+  sampling_params prm;
+  int32_t slot, pad[3];
+};
+
+// chunk record sent to the row's leader
+struct __align__(16) RecC {
+  float m;          // max z' over the chunk
+  uint32_t flags;   // bit0 NaN / +inf seen
+  double s;         // sum 2^((z' - m) * c)
+  uint64_t front;   // every element of the chunk with composite >= front is in the list (0: all)
+  uint64_t best;    // greedy rows: the chunk's best composite
+  int32_t n;        // list entries
+  int32_t pad[3];
+};
+
+struct RArgs {
+  const void* logits;
+  int64_t ld;
+  int B, V, voff, vloc;
+  int C;        // cluster size
+  int Lc;       // chunk length (elements, multiple of kLcAlign)
+  int cap;      // candidate list capacity per chunk
+  const int32_t* slots;
+  const sampling_params* params_dev;
+  const sampling_params* params_tab;
+  const uint64_t* seeds;
+  uint64_t step;
+  int kcand, pen_mode, mode, append;
+  HistState hs;
+  RowOut ro;
+  uint8_t* out_records;
+  int64_t out_stride;
+};
+
+// ---- shared-memory layout (host and device) ----------------------------------------
+struct RLay {
+  int buf, bm, stg, wpre, pli, pme, pz, rinfo, hdr, rec, pool, top, wv, byid, dscr, gscr, bar, total;
+};
+constexpr int kGScrBytes = 1024 + 256;
+__host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
+  RLay l;
+  int o = 0;
+  auto A = [&o](int bytes) {
+    const int r = o;
+    o += (bytes + 127) / 128 * 128;
+    return r;
+  };
+  l.buf = A(kRNG * Lc * esz);
+  l.bm = A(kRNG * (Lc / 8));
+  l.stg = A(kRNG * (int)sizeof(RowStage));
+  l.wpre = A(kRNG * (Lc / 32) * 4);
+  l.pli = A(kRNG * kRPen * 4);
+  l.pme = A(kRNG * kRPen * 4);
+  l.pz = A(kRNG * kRPen * 4);
+  l.rinfo = A((int)sizeof(RowStage));
+  l.hdr = A(C * (int)sizeof(RecC));
+  l.rec = A(C * cap * 8);
+  l.pool = A(kRPool * 8);
+  l.top = A(SAMPLER_KCAND_MAX * 8);
+  l.wv = A(SAMPLER_KCAND_MAX * 8);
+  l.byid = A(SAMPLER_KCAND_MAX * 8);
+  l.dscr = A(512);
+  l.gscr = A(kRNG * kGScrBytes);
+  l.bar = A((2 * kRNG + 1 + kRCMax) * 8);
+  l.total = o;
+  return l;
+}
+
+// ---- cluster / DSMEM PTX ------------------------------------------------------------
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_num() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void cl_fence() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+// arrive (count 1) on an mbarrier of another CTA of the cluster; releases this thread's prior writes
+__device__ __forceinline__ void cl_arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+// wait on a local mbarrier whose arrivals may come from other CTAs (cluster-scope acquire)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 4-byte asynchronous global -> shared copy (LDGSTS): gathers that complete behind other work
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// named barrier of one row group (ids 1..kRNG)
+__device__ __forceinline__ void gbar(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kRGT) : "memory"); }
+
+// ---- element formats ----------------------------------------------------------------
+template <typename T>
+struct RV;
+template <>
+struct RV<__nv_bfloat16> {
+  static constexpr int N = 8;
+  // bit t of b set => element t becomes -inf
+  static __device__ __forceinline__ uint4 mask(uint4 u, uint32_t b) {
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if ((b >> (2 * i)) & 1u) w[i] = (w[i] & 0xFFFF0000u) | 0xFF80u;
+      if ((b >> (2 * i + 1)) & 1u) w[i] = (w[i] & 0x0000FFFFu) | 0xFF800000u;
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  static __device__ __forceinline__ __nv_bfloat162 h2(uint32_t w) { return *reinterpret_cast<__nv_bfloat162*>(&w); }
+  // NaN-propagating max of the 8 elements, as a bf16x2 pair
+  static __device__ __forceinline__ __nv_bfloat162 vmax2_nan(uint4 u) {
+    return __hmax2_nan(__hmax2_nan(h2(u.x), h2(u.y)), __hmax2_nan(h2(u.z), h2(u.w)));
+  }
+  static __device__ __forceinline__ float vmax(uint4 u) {
+    const __nv_bfloat162 m = __hmax2(__hmax2(h2(u.x), h2(u.y)), __hmax2(h2(u.z), h2(u.w)));
+    return fmaxf(__low2float(m), __high2float(m));
+  }
+  static __device__ __forceinline__ float elem(uint4 u, int t) {
+    const uint32_t w = (t < 2) ? u.x : (t < 4) ? u.y : (t < 6) ? u.z : u.w;
+    return __uint_as_float((t & 1) ? (w & 0xFFFF0000u) : (w << 16));
+  }
+  static __device__ __forceinline__ float at(const uint8_t* buf, int i) {
+    return __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(buf)[i] << 16);
+  }
+  // sum over the 8 elements of 2^((z - m) * c): exact bf16 -> f32 differences (FFMA with a bf16
+  // operand), packed multiply, MUFU ex2, packed adds; masked (-inf) elements give 0
+  static __device__ __forceinline__ float esum(uint4 u, float nm, float, uint64_t c2) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint64_t p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float a, b;
+      asm("{.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+          "fma.rn.f32.bf16 %0, l, %3, %4;\n\tfma.rn.f32.bf16 %1, h, %3, %4;}"
+          : "=f"(a), "=f"(b)
+          : "r"(w[i]), "h"((unsigned short)0x3F80), "f"(nm));
+      uint64_t t2, x2;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(t2) : "f"(a), "f"(b));
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(x2) : "l"(t2), "l"(c2));
+      float xa, xb;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(xa), "=f"(xb) : "l"(x2));
+      const float ea = ex2f(xa), eb = ex2f(xb);
+      asm("mov.b64 %0, {%1, %2};" : "=l"(p[i]) : "f"(ea), "f"(eb));
+    }
+    uint64_t s01, s23, s;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s01) : "l"(p[0]), "l"(p[1]));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s23) : "l"(p[2]), "l"(p[3]));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(s01), "l"(s23));
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(s));
+    return a + b;
+  }
+};
+template <>
+struct RV<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ uint4 mask(uint4 u, uint32_t b) {
+    if (b & 1u) u.x = 0xFF800000u;
+    if (b & 2u) u.y = 0xFF800000u;
+    if (b & 4u) u.z = 0xFF800000u;
+    if (b & 8u) u.w = 0xFF800000u;
+    return u;
+  }
+  static __device__ __forceinline__ float vmax_nan(uint4 u) {
+    return fmax_nan(fmax_nan(__uint_as_float(u.x), __uint_as_float(u.y)),
+                    fmax_nan(__uint_as_float(u.z), __uint_as_float(u.w)));
+  }
+  static __device__ __forceinline__ float vmax(uint4 u) {
+    return fmaxf(fmaxf(__uint_as_float(u.x), __uint_as_float(u.y)), fmaxf(__uint_as_float(u.z), __uint_as_float(u.w)));
+  }
+  static __device__ __forceinline__ float elem(uint4 u, int t) {
+    return __uint_as_float(t == 0 ? u.x : t == 1 ? u.y : t == 2 ? u.z : u.w);
+  }
+  static __device__ __forceinline__ float at(const uint8_t* buf, int i) {
+    return reinterpret_cast<const float*>(buf)[i];
+  }
+  static __device__ __forceinline__ float esum(uint4 u, float nm, float cf, uint64_t) {
+    const float z[4] = {__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w)};
+    float e[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e[i] = ex2f(__fmul_rn(__fadd_rn(z[i], nm), cf));
+    return (e[0] + e[1]) + (e[2] + e[3]);
+  }
+};
+
+// bitmap bits of vector v (VEC elements) from the chunk bitmap (bit i = element i)
+template <int VEC>
+__device__ __forceinline__ uint32_t vec_bits(const uint8_t* bm, int v) {
+  if (VEC == 8) return bm[v];
+  return (bm[v >> 1] >> ((v & 1) * 4)) & 0xFu;
+}
+
+// keff-th largest of the kRGT keys s_key[] (one warp, every warp of the group redundantly): MSB
+// first, the largest x with |{keys >= x}| >= keff.  Keys of bf16 values are exact in their top 16
+// bits (NB = 16); fp32 keys use all 32.  Returns 0 when fewer than keff keys are non-zero.
+template <int NB>
+__device__ __forceinline__ uint32_t kth_key(const uint32_t* s_key, int keff, int lane) {
+  uint32_t k[kRGT / 32];
+#pragma unroll
+  for (int i = 0; i < kRGT / 32; ++i) k[i] = s_key[lane + 32 * i];
+  uint32_t pre = 0;
+#pragma unroll 1
+  for (int b = 31; b >= 32 - NB; --b) {
+    const uint32_t cand = pre | (1u << b);
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kRGT / 32; ++i) c += (k[i] >= cand) ? 1u : 0u;
+    if ((int)__reduce_add_sync(kFull, c) >= keff) pre = cand;
+  }
+  return pre;
+}
+
+// Exact top-keff of a chunk whose candidates overflow the list (massive ties): radix select of
+// the keff-th largest composite among the elements >= Tf (8-bit digits, MSB first), over the
+// chunk in shared memory and its penalised values.  Returns that composite.  One row group.
+struct PenCtx {
+  const uint32_t* bmw;   // chunk bitmap words
+  const uint32_t* wpre;  // per word: index of its first set bit among the chunk's set bits
+  const int32_t* li;     // staged: local index of set bit e (e < kRPen)
+  const float* pz;       // staged: penalised value of set bit e
+  const uint32_t* gme;   // global per-id meta of the chunk (unstaged bits)
+  int npen;
+  // penalised value of the set bit at local index l (any e)
+  template <typename T>
+  __device__ __forceinline__ float value(int l, const uint8_t* buf, const sampling_params& prm, int mode) const {
+    const int w = l >> 5;
+    const int e = (int)wpre[w] + __popc(bmw[w] & ((1u << (l & 31)) - 1u));
+    if (e < kRPen) return pz[e];
+    return apply_penalty(RV<T>::at(buf, l), gme[l], prm, mode);
+  }
+};
+
+template <typename T>
+__device__ __noinline__ uint64_t group_kth_comp(const uint8_t* buf, const uint8_t* bm, int nvec, int nval,
+                                                const PenCtx& pc, const sampling_params& prm, int pen_mode,
+                                                int gid0, float Tf, int keff, uint32_t* hist, int* ctl, int g) {
+  constexpr int VEC = RV<T>::N;
+  const int tid = threadIdx.x - g * kRGT;
+  uint64_t pre = 0;
+  int need = keff;
+  for (int d = 56; d >= 0; d -= 8) {
+    for (int i = tid; i < 256; i += kRGT) hist[i] = 0;
+    gbar(g);
+    auto add = [&](uint64_t c) {
+      if (d == 56 || (c >> (d + 8)) == pre) atomicAdd(&hist[(c >> d) & 255], 1u);
+    };
+    for (int v = tid; v < nvec; v += kRGT) {
+      uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+      uint32_t b = vec_bits<VEC>(bm, v);
+      if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
+      const uint32_t pb = vec_bits<VEC>(bm, v);
+      if (b) u = RV<T>::mask(u, b);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) {
+        float z = RV<T>::elem(u, t);
+        if ((pb >> t) & 1u) z = pc.value<T>(v * VEC + t, buf, prm, pen_mode);
+        if (z >= Tf && z > -INFINITY && z < INFINITY) add(make_comp(z, gid0 + v * VEC + t));
+      }
+    }
+    gbar(g);
+    if (tid == 0) {  // the digit: running count from the top
+      int run = 0, dg = 255;
+      for (; dg > 0; --dg) {
+        if (run + (int)hist[dg] >= need) break;
+        run += (int)hist[dg];
+      }
+      ctl[0] = dg;
+      ctl[1] = run;
+    }
+    gbar(g);
+    need -= ctl[1];
+    pre = (pre << 8) | (uint64_t)ctl[0];
+    gbar(g);
+  }
+  return pre;
+}
+
+// The keff largest of pool[0..n) (unique composites) into top[0..min(n, keff)), sorted descending.
+// One warp: the keff-th largest composite by bitwise radix select (value key first, then the id
+// part among ties), then a rank sort of the survivors.  scr: >= SAMPLER_KCAND_MAX entries.
+__device__ __forceinline__ int warp_topk(const uint64_t* pool, int n, int keff, uint64_t* scr, uint64_t* top,
+                                         int lane) {
+  uint64_t kc = 0;
+  if (n > keff) {
+    uint32_t hk = 0;
+#pragma unroll 1
+    for (int b = 31; b >= 0; --b) {
+      const uint32_t cand = hk | (1u << b);
+      uint32_t c = 0;
+      for (int i = lane; i < n; i += 32) c += ((uint32_t)(pool[i] >> 32) >= cand) ? 1u : 0u;
+      if ((int)__reduce_add_sync(kFull, c) >= keff) hk = cand;
+    }
+    uint32_t gt = 0, eq = 0;
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t h = (uint32_t)(pool[i] >> 32);
+      gt += h > hk ? 1u : 0u;
+      eq += h == hk ? 1u : 0u;
+    }
+    const int ngt = (int)__reduce_add_sync(kFull, gt), neq = (int)__reduce_add_sync(kFull, eq);
+    const int need = keff - ngt;
+    uint32_t lk = 0;
+    if (neq > need) {
+#pragma unroll 1
+      for (int b = 31; b >= 0; --b) {
+        const uint32_t cand = lk | (1u << b);
+        uint32_t c = 0;
+        for (int i = lane; i < n; i += 32)
+          c += ((uint32_t)(pool[i] >> 32) == hk && (uint32_t)pool[i] >= cand) ? 1u : 0u;
+        if ((int)__reduce_add_sync(kFull, c) >= need) lk = cand;
+      }
+    }
+    kc = ((uint64_t)hk << 32) | lk;
+  }
+  int m = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = (i < n) ? pool[i] : 0ull;
+    const bool keep = i < n && v >= kc;
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (keep) scr[m + __popc(bal & ((1u << lane) - 1u))] = v;
+    m += __popc(bal);
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {
+    const uint64_t c = scr[i];
+    int rk = 0;
+    for (int j = 0; j < m; ++j) rk += (scr[j] > c) ? 1 : 0;
+    top[rk] = c;
+  }
+  __syncwarp();
+  return m;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant__ RArgs a) {
+  constexpr int VEC = RV<T>::N;
+  constexpr int ESZ = (int)sizeof(T);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const RLay L = rlayout(a.C, a.Lc, ESZ, a.cap);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cl_rank(), q = cl_id(), nclus = cl_num();
+  const int C = a.C;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* full = bar;                 // [kRNG]
+  uint64_t* empty = bar + kRNG;         // [kRNG]
+  uint64_t* recfull = bar + 2 * kRNG;   // [1]
+  uint64_t* slotfree = recfull + 1;     // [kRCMax]: leader l has consumed our last list
+  const int nrows = (a.B > (int)q) ? (a.B - (int)q + (int)nclus - 1) / (int)nclus : 0;  // rows of this cluster
+  const int c0 = (int)rank * a.Lc;                                // first local id of this CTA's chunk
+  const int nval = max(0, min(a.Lc, a.vloc - c0));                // valid elements of the chunk
+  const int nvec = (nval + VEC - 1) / VEC;
+
+  if (tid == 0) {
+    for (int g = 0; g < kRNG; ++g) {
+      mbar_init(full + g, 1);
+      mbar_init(empty + g, kRWG);
+    }
+    mbar_init(recfull, C);
+    for (int l = 0; l < kRCMax; ++l) mbar_init(slotfree + l, 1);
+    fence_mbar_init();
+  }
+  // the previous kernel of the stream (the last step, which appended to the histories) is complete
+  // before any memory access; the next step may be scheduled as this grid retires
+  griddep_wait();
+  griddep_launch();
+  cl_sync();  // every CTA's barriers are initialised before any remote arrive
+
+  if (warp == kRProdW) {
+    // ================= producer: bulk copies of this CTA's chunk of each row =================
+    if (lane == 0 && nrows > 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      const uint8_t* lg = reinterpret_cast<const uint8_t*>(a.logits);
+      const uint32_t dbytes = (uint32_t)((nval * ESZ + 15) / 16 * 16);
+      const uint32_t bmb = (uint32_t)((nval + 127) / 128 * 16);
+      for (int it = 0; it < nrows; ++it) {
+        const int g = it % kRNG;
+        if (it >= kRNG) mbar_wait(empty + g, (uint32_t)((it / kRNG - 1) & 1));
+        const int64_t r = (int64_t)q + (int64_t)it * nclus;
+        RowStage* st = reinterpret_cast<RowStage*>(smem + L.stg) + g;
+        if (nval > 0) {  // the logits first: they do not depend on the slot
+          mbar_expect_tx(full + g, dbytes + bmb);
+          bulk_g2s(smem + L.buf + g * a.Lc * ESZ, lg + (r * a.ld + c0) * ESZ, dbytes, full + g, pol);
+        }
+        const int slot = a.slots ? a.slots[r] : (int)r;
+        if (nval > 0)
+          bulk_g2s(smem + L.bm + g * (a.Lc / 8), a.hs.pmask + (int64_t)slot * a.hs.pmw + c0 / 32, bmb, full + g, pol);
+        st->prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
+        st->slot = slot;
+        mbar_arrive(full + g);  // (release: the staged row info above)
+      }
+    }
+  } else if (warp == kRDecW) {
+    // ================= decider: the rows this CTA leads (row index it with it % C == rank) =========
+    MergeSmem ms;
+    ms.pool = reinterpret_cast<uint64_t*>(smem + L.pool);
+    ms.top = reinterpret_cast<uint64_t*>(smem + L.top);
+    ms.wv = reinterpret_cast<double*>(smem + L.wv);
+    ms.byid = reinterpret_cast<uint64_t*>(smem + L.byid);
+    ms.hdr = nullptr;
+    ms.off = nullptr;
+    uint8_t* dsc = smem + L.dscr;
+    ms.bs.f = reinterpret_cast<float*>(dsc);
+    ms.bs.d = reinterpret_cast<double*>(dsc + 32);
+    ms.bs.u = reinterpret_cast<uint64_t*>(dsc + 96);
+    ms.bs.i = reinterpret_cast<int*>(dsc + 224);
+    const RecC* hdr = reinterpret_cast<const RecC*>(smem + L.hdr);
+    const uint64_t* rec = reinterpret_cast<const uint64_t*>(smem + L.rec);
+    const RowStage* ri = reinterpret_cast<const RowStage*>(smem + L.rinfo);
+    for (int it = (int)rank; it < nrows; it += C) {
+      const int r = (int)q + it * (int)nclus;
+      mbar_wait_cl(recfull, (uint32_t)((it / C) & 1));
+      const sampling_params prm = ri->prm;
+      const int slot = ri->slot;
+      const RowCfg rc = decode_row(prm, a.V, a.kcand);
+      const bool bounded = rc.greedy || (rc.topk_on && rc.k <= a.kcand);
+      const int keff = rc.keff;
+      // M, S, frontier, flags: lane c holds chunk c (fixed order: deterministic)
+      const bool has = lane < C;
+      RecC h;
+      if (has) h = hdr[lane];
+      const float M = warp_max(has ? h.m : -INFINITY);
+      const double term = (has && h.s != 0.0) ? h.s * exp2(((double)h.m - (double)M) * rc.c_d) : 0.0;
+      const double S = warp_sum_d(term);
+      uint64_t F = warp_max_u64(has ? h.front : 0ull);
+      const bool bad = __any_sync(kFull, has && (h.flags & 1u));
+      const uint64_t best = warp_max_u64(has ? h.best : 0ull);
+      // candidates >= F into the pool (warp compaction, chunk order)
+      int n = 0;
+      if (!rc.greedy) {
+        for (int c = 0; c < C; ++c) {
+          const int nc = min(hdr[c].n, a.cap);
+          for (int i0 = 0; i0 < nc; i0 += 32) {
+            const int i = i0 + lane;
+            const uint64_t v = (i < nc) ? rec[c * a.cap + i] : 0ull;
+            const bool keep = i < nc && v >= F;
+            const unsigned bal = __ballot_sync(kFull, keep);
+            const int at = n + __popc(bal & ((1u << lane) - 1u));
+            if (keep && at < kRPool) ms.pool[at] = v;
+            n += __popc(bal);
+          }
+        }
+      }
+      __syncwarp();
+      // the chunk lists are consumed: release every sender's slot for this leader
+      if (lane < C) cl_arrive_remote(cl_map(smem_u32(slotfree + rank), (uint32_t)lane));
+      const bool over = n > kRPool;
+      n = min(n, kRPool);
+      if (rc.greedy) {
+        if (lane == 0) ms.top[0] = best;
+        __syncwarp();
+        n = (best != 0ull) ? 1 : 0;
+        F = best;
+      } else {
+        n = warp_topk(ms.pool, n, keff, reinterpret_cast<uint64_t*>(ms.wv), ms.top, lane);
+      }
+      const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
+      if (a.mode == 1) {  // vocab-sharded phase 1: the row's candidate record (merge.cuh)
+        uint8_t* out = a.out_records + (int64_t)r * a.out_stride;
+        uint64_t* oe = reinterpret_cast<uint64_t*>(out + kRecHdrBytes);
+        for (int i = lane; i < n; i += 32) oe[i] = ms.top[i];
+        if (lane == 0) {
+          RecHdr o;
+          o.m = M;
+          o.flags = bad ? kRecBad : 0u;
+          o.s = S;
+          o.R = (double)M * rc.c_d;
+          o.n = (uint32_t)n;
+          o.rsv = 0;
+          o.frontier = over ? ~0ull : F;
+          *reinterpret_cast<RecHdr*>(out) = o;
+        }
+        __syncwarp();
+        continue;
+      }
+      if (!bounded || over) {  // exact.cuh finishes the row from {M, S}
+        if (lane == 0) {
+          RowInfo o;
+          o.M = M;
+          o.status = bad ? SAMPLER_ROW_NONFINITE : (M > -INFINITY ? kRowPending : SAMPLER_ROW_ALL_NEG_INF);
+          o.S = S;
+          o.W = 0.0;
+          o.cutoff = 0;
+          o.token = -1;
+          o.greedy = rc.greedy;
+          a.ro.info[r] = o;
+          if (o.status != kRowPending) {
+            a.ro.tokens[r] = -1;
+            a.ro.logprobs[r] = NAN;
+            if (a.ro.flogprobs) a.ro.flogprobs[r] = NAN;
+            if (a.ro.status) a.ro.status[r] = o.status;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      const int tok = warp_decide(ms, n, M, S, F, bad, rc, prm, seed, a.step, r, a.ro, false, nullptr);
+      if (a.append && tok >= 0 && lane == 0) hist_append(a.hs, slot, tok);
+      __syncwarp();
+    }
+  } else {
+    // ================= row groups: rows it = g, g + kRNG, ... =================
+    const int g = warp / kRWG;
+    const int gt = tid - g * kRGT, gw = gt >> 5;
+    const uint8_t* buf = smem + L.buf + g * a.Lc * ESZ;
+    const uint8_t* bm = smem + L.bm + g * (a.Lc / 8);
+    const uint32_t* bmw = reinterpret_cast<const uint32_t*>(bm);
+    const RowStage* st = reinterpret_cast<const RowStage*>(smem + L.stg) + g;
+    uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + L.wpre + g * (a.Lc / 32) * 4);
+    int32_t* pli = reinterpret_cast<int32_t*>(smem + L.pli + g * kRPen * 4);
+    uint32_t* pme = reinterpret_cast<uint32_t*>(smem + L.pme + g * kRPen * 4);
+    float* pz = reinterpret_cast<float*>(smem + L.pz + g * kRPen * 4);
+    uint8_t* gsc = smem + L.gscr + g * kGScrBytes;
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(gsc);             // [kRGT] thread-max keys | slow-path hist
+    uint8_t* gs = gsc + 1024;
+    uint32_t* s_wm = reinterpret_cast<uint32_t*>(gs);               // [4] max keys (incl. penalised)
+    uint32_t* s_wb = reinterpret_cast<uint32_t*>(gs + 16);          // [4] bad flags
+    double* s_ws = reinterpret_cast<double*>(gs + 32);              // [4] sums
+    uint64_t* s_wbest = reinterpret_cast<uint64_t*>(gs + 64);       // [4] greedy best
+    int* s_cnt = reinterpret_cast<int*>(gs + 96);                   // [2] candidate counters (row parity)
+    int* s_ctl = reinterpret_cast<int*>(gs + 112);                  // [4] slow-path control
+    int* s_ps = reinterpret_cast<int*>(gs + 128);                   // [4] penalised-bit counts per warp
+    const int gid0 = a.voff + c0;
+    const int nw = (nval + 31) >> 5;                 // bitmap words of the chunk
+    const int wpt = (nw + kRGT - 1) / kRGT;          // words per thread (contiguous)
+    const int w0 = min(nw, gt * wpt), w1 = min(nw, w0 + wpt);
+    for (int it = g; it < nrows; it += kRNG) {
+      const int par = (it / kRNG) & 1;
+      mbar_wait(full + g, (uint32_t)par);
+      const RowStage stc = *st;  // (the producer rewrites the stage once the buffer is released)
+      const sampling_params& prm = stc.prm;
+      const RowCfg rc = decode_row(prm, a.V, a.kcand);
+      const int keff = rc.keff;
+      const float cf = __fdiv_rn((float)kLog2e, rc.tau);
+      const int leader = it % C;
+      const uint32_t* gme = a.hs.pmeta + (int64_t)stc.slot * a.hs.vls + c0;
+      // ---- penalised ids of the chunk: the set bits of the presence bitmap.  Index them (group
+      //      scan over contiguous word ranges) and gather their counts asynchronously (LDGSTS),
+      //      behind A1.
+      int mycnt = 0;
+      for (int w = w0; w < w1; ++w) mycnt += __popc(bmw[w]);
+      const int incl = warp_incl_scan_i(mycnt, lane);
+      if (lane == 31) s_ps[gw] = incl;
+      if (gt == 0) {
+        s_cnt[par] = 0;
+        // the leader's list for this row must be free before any candidate is pushed into it
+        if (it >= C) mbar_wait_cl(slotfree + leader, (uint32_t)((it / C - 1) & 1));
+      }
+      gbar(g);
+      int base = incl - mycnt, npen = 0;
+#pragma unroll
+      for (int j = 0; j < kRWG; ++j) {
+        base += (j < gw) ? s_ps[j] : 0;
+        npen += s_ps[j];
+      }
+      for (int w = w0, e = base; w < w1; ++w) {
+        wpre[w] = (uint32_t)e;
+        uint32_t bits = bmw[w];
+        while (bits) {
+          const int l = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (e < kRPen) {
+            pli[e] = l;
+            cp_async4(pme + e, gme + l);
+          }
+          ++e;
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      PenCtx pc;
+      pc.bmw = bmw;
+      pc.wpre = wpre;
+      pc.li = pli;
+      pc.pz = pz;
+      pc.gme = gme;
+      pc.npen = npen;
+      const bool ovf = npen > kRPen;  // (group-uniform) more penalised ids than staged: in-loop
+      if (ovf) gbar(g);               // wpre complete before any lookup
+      // ---- A1: max over the chunk (penalised ids and the tail masked; NaN-propagating)
+      float tmax = -INFINITY, pmax = -INFINITY;
+      uint32_t pbad = 0;
+      auto ovf_pen = [&](int v, uint32_t pb, auto&& use) {
+        while (pb) {
+          const int l = v * VEC + __ffs(pb) - 1;
+          pb &= pb - 1;
+          const int w = l >> 5;
+          const int e = (int)wpre[w] + __popc(bmw[w] & ((1u << (l & 31)) - 1u));
+          if (e >= kRPen) use(l, apply_penalty(RV<T>::at(buf, l), gme[l], prm, a.pen_mode));
+        }
+      };
+      if (VEC == 8) {
+        __nv_bfloat162 acc = __float2bfloat162_rn(-INFINITY);
+        for (int v = gt; v < nvec; v += kRGT) {
+          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+          const uint32_t pb = vec_bits<VEC>(bm, v);
+          uint32_t b = pb;
+          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & 0xFFu;
+          if (b) {
+            u = RV<T>::mask(u, b);
+            if (ovf && pb)
+              ovf_pen(v, pb, [&](int, float zp) {
+                if (!(zp < INFINITY)) pbad = 1;
+                else pmax = fmaxf(pmax, zp);
+              });
+          }
+          acc = __hmax2_nan(acc, RV<__nv_bfloat16>::vmax2_nan(u));
+        }
+        tmax = fmax_nan(__low2float(acc), __high2float(acc));
+      } else {
+        for (int v = gt; v < nvec; v += kRGT) {
+          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+          const uint32_t pb = vec_bits<VEC>(bm, v);
+          uint32_t b = pb;
+          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & 0xFu;
+          if (b) {
+            u = RV<T>::mask(u, b);
+            if (ovf && pb)
+              ovf_pen(v, pb, [&](int, float zp) {
+                if (!(zp < INFINITY)) pbad = 1;
+                else pmax = fmaxf(pmax, zp);
+              });
+          }
+          tmax = fmax_nan(tmax, RV<float>::vmax_nan(u));
+        }
+      }
+      // ---- the staged penalised values (exact binary32 penalty, P:146 / P:371)
+      cp_async_wait_all();
+      gbar(g);
+      const int nst = min(npen, kRPen);
+      for (int e = gt; e < nst; e += kRGT) {
+        const float zp = apply_penalty(RV<T>::at(buf, pli[e]), pme[e], prm, a.pen_mode);
+        pz[e] = zp;
+        if (!(zp < INFINITY)) pbad = 1;  // NaN / +inf
+        else pmax = fmaxf(pmax, zp);
+      }
+      const uint32_t bad_t = (tmax != tmax || tmax == INFINITY) ? 1u : pbad;
+      // thread-max key for the bound (unpenalised elements; 0 = none); chunk max incl. penalised
+      s_key[gt] = (bad_t || !(tmax > -INFINITY)) ? 0u : f2key(tmax);
+      const float mloc = fmaxf(bad_t ? -INFINITY : tmax, pmax);
+      const uint32_t mk = __reduce_max_sync(kFull, f2key(mloc));
+      const uint32_t bw = __reduce_or_sync(kFull, bad_t);
+      if (lane == 0) {
+        s_wm[gw] = mk;
+        s_wb[gw] = bw;
+      }
+      gbar(g);
+      uint32_t mkey = s_wm[0], badc = s_wb[0];
+#pragma unroll
+      for (int j = 1; j < kRWG; ++j) {
+        mkey = max(mkey, s_wm[j]);
+        badc |= s_wb[j];
+      }
+      const float mc = key2f(mkey);  // chunk max (-inf if empty)
+      // bound T_c: the keff-th largest thread max (0: fewer than keff non-empty threads -> all)
+      const uint32_t tkey = (VEC == 8) ? kth_key<16>(s_key, keff, lane) : kth_key<32>(s_key, keff, lane);
+      const float Tf = tkey ? key2f(tkey) : -INFINITY;
+      // ---- A2: exp-sum relative to the chunk max; candidates >= T pushed into the leader's list
+      const uint32_t rec_remote = cl_map(smem_u32(smem + L.rec), (uint32_t)leader) + rank * (uint32_t)(a.cap * 8);
+      double ssum = 0.0;
+      uint64_t tbest = 0ull;
+      const bool live = !badc && mc > -INFINITY;
+      auto push = [&](float z, int gid) {
+        const uint64_t cmp = make_comp(z, gid);
+        if (rc.greedy) {
+          tbest = cmp > tbest ? cmp : tbest;
+        } else {
+          const int at = atomicAdd(&s_cnt[par], 1);
+          if (at < a.cap) cl_st64(rec_remote + (uint32_t)at * 8u, cmp);
+        }
+      };
+      if (live) {
+        const float nm = -mc;
+        uint64_t c2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cf), "f"(cf));
+        float acc = 0.f;
+        int nacc = 0;
+        for (int v = gt; v < nvec; v += kRGT) {
+          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+          const uint32_t pb = vec_bits<VEC>(bm, v);
+          uint32_t b = pb;
+          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
+          if (b) {
+            u = RV<T>::mask(u, b);
+            if (ovf && pb)
+              ovf_pen(v, pb, [&](int l, float zp) {
+                if (zp > -INFINITY) {
+                  ssum += (double)ex2f(__fmul_rn(__fsub_rn(zp, mc), cf));
+                  if (zp >= Tf) push(zp, gid0 + l);
+                }
+              });
+          }
+          acc += RV<T>::esum(u, nm, cf, c2);
+          if (++nacc == 8) {
+            ssum += (double)acc;
+            acc = 0.f;
+            nacc = 0;
+          }
+          if (RV<T>::vmax(u) >= Tf) {
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) {
+              const float z = RV<T>::elem(u, t);
+              if (z >= Tf && z > -INFINITY) push(z, gid0 + v * VEC + t);
+            }
+          }
+        }
+        ssum += (double)acc;
+        for (int e = gt; e < nst; e += kRGT) {
+          const float zp = pz[e];
+          if (zp > -INFINITY) {
+            ssum += (double)ex2f(__fmul_rn(__fsub_rn(zp, mc), cf));
+            if (zp >= Tf) push(zp, gid0 + pli[e]);
+          }
+        }
+      }
+      // ---- reductions (fixed order)
+      ssum = warp_sum_d(ssum);
+      tbest = warp_max_u64(tbest);
+      if (lane == 0) {
+        s_ws[gw] = ssum;
+        s_wbest[gw] = tbest;
+      }
+      gbar(g);
+      int cnt = s_cnt[par];
+      uint64_t front = tkey ? make_comp(Tf, 0x7FFFFFFF) : 0ull;
+      if (live && !rc.greedy && cnt > a.cap) {
+        // massive ties: the chunk's exact top-keff by composite, then the list again (rare)
+        const uint64_t kc = group_kth_comp<T>(buf, bm, nvec, nval, pc, prm, a.pen_mode, gid0, Tf, keff, s_key,
+                                              s_ctl, g);
+        if (gt == 0) s_cnt[par] = 0;
+        gbar(g);
+        for (int v = gt; v < nvec; v += kRGT) {
+          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+          const uint32_t pb = vec_bits<VEC>(bm, v);
+          uint32_t b = pb;
+          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
+          if (b) u = RV<T>::mask(u, b);
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) {
+            float z = RV<T>::elem(u, t);
+            if ((pb >> t) & 1u) z = pc.value<T>(v * VEC + t, buf, prm, a.pen_mode);
+            if (z >= Tf && z > -INFINITY && z < INFINITY && make_comp(z, gid0 + v * VEC + t) >= kc)
+              push(z, gid0 + v * VEC + t);
+          }
+        }
+        gbar(g);
+        cnt = s_cnt[par];
+        front = kc;
+      }
+      // the buffer is consumed
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + g);
+      cl_fence();  // this thread's list entries, before the leader is signalled
+      gbar(g);
+      if (gt == 0) {
+        RecC h;
+        h.m = mc;
+        h.flags = badc ? 1u : 0u;
+        double s = 0.0;
+        uint64_t bb = 0ull;
+#pragma unroll
+        for (int j = 0; j < kRWG; ++j) {
+          s += s_ws[j];
+          bb = s_wbest[j] > bb ? s_wbest[j] : bb;
+        }
+        h.s = s;
+        h.front = front;
+        h.best = bb;
+        h.n = min(cnt, a.cap);
+        h.pad[0] = h.pad[1] = h.pad[2] = 0;
+        const uint32_t hr = cl_map(smem_u32(smem + L.hdr), (uint32_t)leader) + rank * (uint32_t)sizeof(RecC);
+        const uint4* hv = reinterpret_cast<const uint4*>(&h);
+#pragma unroll
+        for (int j = 0; j < (int)(sizeof(RecC) / 16); ++j) cl_st128(hr + 16 * j, hv[j]);
+        if (rank == (uint32_t)leader) *reinterpret_cast<RowStage*>(smem + L.rinfo) = stc;  // for the decider
+        cl_arrive_remote(cl_map(smem_u32(recfull), (uint32_t)leader));
+      }
+    }
+  }
+  __syncwarp();
+  cl_sync();  // no CTA leaves while another may still address its shared memory
+}
+
+}  // namespace smp
