@@ -36,14 +36,14 @@
 namespace smp {
 
 constexpr int kRNG = 2;                     // row groups (= chunk buffers) per CTA
-constexpr int kRWG = 4;                     // warps per row group
+constexpr int kRWG = 8;                     // warps per row group
 constexpr int kRGT = kRWG * 32;             // threads per row group
 constexpr int kRThreads = kRNG * kRGT + 64; // + producer warp + decider warp
 constexpr int kRProdW = kRNG * kRWG;        // producer warp index
 constexpr int kRDecW = kRProdW + 1;         // decider warp index
-constexpr int kRPen = 512;                  // penalised entries staged per chunk (more: handled in-loop)
+constexpr int kPT = 4;                      // penalised ids staged per thread and row (more: read synchronously)
 constexpr int kRCMax = 16;                  // max cluster size
-constexpr int kRPool = 1024;                // decider candidate pool
+constexpr int kRCapL = 256;                 // local candidate list per row group
 constexpr int kLcAlign = 128;               // chunk length granularity (16-byte bitmap rows, 16-byte copies)
 
 // per-row staging, written by the producer next to the bulk copies of the chunk
@@ -69,7 +69,7 @@ struct RArgs {
   int B, V, voff, vloc;
   int C;        // cluster size
   int Lc;       // chunk length (elements, multiple of kLcAlign)
-  int cap;      // candidate list capacity per chunk
+  int cap;      // sorted candidate list capacity per chunk in the leader (>= max_top_k)
   const int32_t* slots;
   const sampling_params* params_dev;
   const sampling_params* params_tab;
@@ -80,13 +80,35 @@ struct RArgs {
   RowOut ro;
   uint8_t* out_records;
   int64_t out_stride;
+  uint64_t* trace;  // SMP_TRACE builds only (development): [CTA][kTrRows][16] globaltimer stamps
 };
+
+// Development timeline (tools/trace_row.py): compiled in only with -DSMP_TRACE, never in the
+// product library.  Slot = (CTA, row of the cluster < kTrRows, event < 16).
+constexpr int kTrRows = 64;
+#ifdef SMP_TRACE
+#define RTR(it, ev)                                                                                   \
+  do {                                                                                                \
+    if (a.trace && (it) < kTrRows) a.trace[((int64_t)blockIdx.x * kTrRows + (it)) * 16 + (ev)] = gtimer(); \
+  } while (0)
+#define RTV(it, ev, val)                                                                               \
+  do {                                                                                                  \
+    if (a.trace && (it) < kTrRows) a.trace[((int64_t)blockIdx.x * kTrRows + (it)) * 16 + (ev)] = (uint64_t)(val); \
+  } while (0)
+#else
+#define RTV(it, ev, val) \
+  do {                   \
+  } while (0)
+#define RTR(it, ev) \
+  do {              \
+  } while (0)
+#endif
 
 // ---- shared-memory layout (host and device) ----------------------------------------
 struct RLay {
-  int buf, bm, stg, wpre, pli, pme, pz, rinfo, hdr, rec, pool, top, wv, byid, dscr, gscr, bar, total;
+  int buf, bm, stg, pme, gk, rinfo, hdr, rec, pool, top, wv, byid, dscr, gscr, bslot, bar, total;
 };
-constexpr int kGScrBytes = 1024 + 256;
+constexpr int kGScrBytes = 1024 + kRCapL * 8 + 256;
 __host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
   RLay l;
   int o = 0;
@@ -98,20 +120,19 @@ __host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
   l.buf = A(kRNG * Lc * esz);
   l.bm = A(kRNG * (Lc / 8));
   l.stg = A(kRNG * (int)sizeof(RowStage));
-  l.wpre = A(kRNG * (Lc / 32) * 4);
-  l.pli = A(kRNG * kRPen * 4);
-  l.pme = A(kRNG * kRPen * 4);
-  l.pz = A(kRNG * kRPen * 4);
+  l.pme = A(kRNG * kRGT * kPT * 4);
+  l.gk = A(kRNG * (Lc / 16) * 4);  // group keys: one per 2 vectors (<= 16 elements)
   l.rinfo = A((int)sizeof(RowStage));
   l.hdr = A(C * (int)sizeof(RecC));
   l.rec = A(C * cap * 8);
-  l.pool = A(kRPool * 8);
+  l.pool = A(C * cap * 8);
   l.top = A(SAMPLER_KCAND_MAX * 8);
-  l.wv = A(SAMPLER_KCAND_MAX * 8);
+  l.wv = A((SAMPLER_KCAND_MAX + 64) * 8);  // (also warp_topk's survivor scratch)
   l.byid = A(SAMPLER_KCAND_MAX * 8);
   l.dscr = A(512);
   l.gscr = A(kRNG * kGScrBytes);
-  l.bar = A((2 * kRNG + 1 + kRCMax) * 8);
+  l.bslot = A(kRNG * 2 * kRCMax * 4);  // row bounds exchanged between the cluster's CTAs
+  l.bar = A((3 * kRNG + 1 + kRCMax) * 8);
   l.total = o;
   return l;
 }
@@ -154,9 +175,10 @@ __device__ __forceinline__ void cl_arrive_remote(uint32_t addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 // wait on a local mbarrier whose arrivals may come from other CTAs (cluster-scope acquire)
+// (back-off between polls: a waiting warp must not take issue slots from the row groups)
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
   uint32_t done;
-  do {
+  for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
@@ -164,7 +186,9 @@ __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) break;
+    __nanosleep(SMP_SLEEP_NS);
+  }
 }
 // 4-byte asynchronous global -> shared copy (LDGSTS): gathers that complete behind other work
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -300,49 +324,34 @@ __device__ __forceinline__ uint32_t kth_key(const uint32_t* s_key, int keff, int
 
 // Exact top-keff of a chunk whose candidates overflow the list (massive ties): radix select of
 // the keff-th largest composite among the elements >= Tf (8-bit digits, MSB first), over the
-// chunk in shared memory and its penalised values.  Returns that composite.  One row group.
-struct PenCtx {
-  const uint32_t* bmw;   // chunk bitmap words
-  const uint32_t* wpre;  // per word: index of its first set bit among the chunk's set bits
-  const int32_t* li;     // staged: local index of set bit e (e < kRPen)
-  const float* pz;       // staged: penalised value of set bit e
-  const uint32_t* gme;   // global per-id meta of the chunk (unstaged bits)
-  int npen;
-  // penalised value of the set bit at local index l (any e)
-  template <typename T>
-  __device__ __forceinline__ float value(int l, const uint8_t* buf, const sampling_params& prm, int mode) const {
-    const int w = l >> 5;
-    const int e = (int)wpre[w] + __popc(bmw[w] & ((1u << (l & 31)) - 1u));
-    if (e < kRPen) return pz[e];
-    return apply_penalty(RV<T>::at(buf, l), gme[l], prm, mode);
-  }
-};
-
+// chunk in shared memory (penalised ids re-evaluated from their counts).  One row group.
 template <typename T>
 __device__ __noinline__ uint64_t group_kth_comp(const uint8_t* buf, const uint8_t* bm, int nvec, int nval,
-                                                const PenCtx& pc, const sampling_params& prm, int pen_mode,
+                                                const uint32_t* gme, const sampling_params& prm, int pen_mode,
                                                 int gid0, float Tf, int keff, uint32_t* hist, int* ctl, int g) {
   constexpr int VEC = RV<T>::N;
   const int tid = threadIdx.x - g * kRGT;
+  const int nfull = nval / VEC;
+  const uint32_t tailmask = (nvec > nfull) ? (~((1u << (nval - nfull * VEC)) - 1u) & ((1u << VEC) - 1u)) : 0u;
   uint64_t pre = 0;
   int need = keff;
   for (int d = 56; d >= 0; d -= 8) {
     for (int i = tid; i < 256; i += kRGT) hist[i] = 0;
     gbar(g);
-    auto add = [&](uint64_t c) {
-      if (d == 56 || (c >> (d + 8)) == pre) atomicAdd(&hist[(c >> d) & 255], 1u);
-    };
     for (int v = tid; v < nvec; v += kRGT) {
       uint4 u = reinterpret_cast<const uint4*>(buf)[v];
-      uint32_t b = vec_bits<VEC>(bm, v);
-      if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
       const uint32_t pb = vec_bits<VEC>(bm, v);
+      const uint32_t b = pb | (v == nfull ? tailmask : 0u);
       if (b) u = RV<T>::mask(u, b);
 #pragma unroll
       for (int t = 0; t < VEC; ++t) {
         float z = RV<T>::elem(u, t);
-        if ((pb >> t) & 1u) z = pc.value<T>(v * VEC + t, buf, prm, pen_mode);
-        if (z >= Tf && z > -INFINITY && z < INFINITY) add(make_comp(z, gid0 + v * VEC + t));
+        const int l = v * VEC + t;
+        if ((pb >> t) & 1u) z = apply_penalty(RV<T>::at(buf, l), gme[l], prm, pen_mode);
+        if (z >= Tf && z > -INFINITY && z < INFINITY) {
+          const uint64_t c = make_comp(z, gid0 + l);
+          if (d == 56 || (c >> (d + 8)) == pre) atomicAdd(&hist[(c >> d) & 255], 1u);
+        }
       }
     }
     gbar(g);
@@ -363,31 +372,40 @@ __device__ __noinline__ uint64_t group_kth_comp(const uint8_t* buf, const uint8_
   return pre;
 }
 
-// The keff largest of pool[0..n) (unique composites) into top[0..min(n, keff)), sorted descending.
-// One warp: the keff-th largest composite by bitwise radix select (value key first, then the id
-// part among ties), then a rank sort of the survivors.  scr: >= SAMPLER_KCAND_MAX entries.
+// The keff largest of pool[0..n) (unique composites) into top[0..min(n, keff)), sorted descending;
+// one warp.  The keff-th largest value key by bitwise radix select (ballot counts; the bits above
+// the first one where the largest and smallest key differ are common to all), the survivors (key
+// above it, and the ties at it) compacted into scr (>= SAMPLER_KCAND_MAX + 64 entries, else the
+// id part is selected too), then a rank sort of the survivors.
 __device__ __forceinline__ int warp_topk(const uint64_t* pool, int n, int keff, uint64_t* scr, uint64_t* top,
                                          int lane) {
-  uint64_t kc = 0;
+  uint64_t kc = 0;  // survivors: composites >= kc
   if (n > keff) {
-    uint32_t hk = 0;
+    uint32_t kmax = 0, kmin = 0xFFFFFFFFu;
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t h = (uint32_t)(pool[i] >> 32);
+      kmax = max(kmax, h);
+      kmin = min(kmin, h);
+    }
+    kmax = __reduce_max_sync(kFull, kmax);
+    kmin = __reduce_min_sync(kFull, kmin);
+    const int top_bit = 31 - __clz(kmax ^ kmin);  // (-1: all keys equal)
+    uint32_t hk = top_bit >= 0 ? (kmax & ~((2u << top_bit) - 1u)) : kmax;
 #pragma unroll 1
-    for (int b = 31; b >= 0; --b) {
+    for (int b = top_bit; b >= 0; --b) {
       const uint32_t cand = hk | (1u << b);
       uint32_t c = 0;
       for (int i = lane; i < n; i += 32) c += ((uint32_t)(pool[i] >> 32) >= cand) ? 1u : 0u;
       if ((int)__reduce_add_sync(kFull, c) >= keff) hk = cand;
     }
-    uint32_t gt = 0, eq = 0;
-    for (int i = lane; i < n; i += 32) {
-      const uint32_t h = (uint32_t)(pool[i] >> 32);
-      gt += h > hk ? 1u : 0u;
-      eq += h == hk ? 1u : 0u;
-    }
-    const int ngt = (int)__reduce_add_sync(kFull, gt), neq = (int)__reduce_add_sync(kFull, eq);
-    const int need = keff - ngt;
-    uint32_t lk = 0;
-    if (neq > need) {
+    kc = (uint64_t)hk << 32;
+    uint32_t ge = 0;
+    for (int i = lane; i < n; i += 32) ge += ((uint32_t)(pool[i] >> 32) >= hk) ? 1u : 0u;
+    if ((int)__reduce_add_sync(kFull, ge) > SAMPLER_KCAND_MAX + 64) {  // massive ties at hk: the id part too
+      uint32_t gt = 0;
+      for (int i = lane; i < n; i += 32) gt += ((uint32_t)(pool[i] >> 32) > hk) ? 1u : 0u;
+      const int need = keff - (int)__reduce_add_sync(kFull, gt);
+      uint32_t lk = 0;
 #pragma unroll 1
       for (int b = 31; b >= 0; --b) {
         const uint32_t cand = lk | (1u << b);
@@ -396,8 +414,8 @@ __device__ __forceinline__ int warp_topk(const uint64_t* pool, int n, int keff, 
           c += ((uint32_t)(pool[i] >> 32) == hk && (uint32_t)pool[i] >= cand) ? 1u : 0u;
         if ((int)__reduce_add_sync(kFull, c) >= need) lk = cand;
       }
+      kc |= lk;
     }
-    kc = ((uint64_t)hk << 32) | lk;
   }
   int m = 0;
   for (int i0 = 0; i0 < n; i0 += 32) {
@@ -413,10 +431,10 @@ __device__ __forceinline__ int warp_topk(const uint64_t* pool, int n, int keff, 
     const uint64_t c = scr[i];
     int rk = 0;
     for (int j = 0; j < m; ++j) rk += (scr[j] > c) ? 1 : 0;
-    top[rk] = c;
+    if (rk < keff) top[rk] = c;
   }
   __syncwarp();
-  return m;
+  return min(m, keff);
 }
 
 template <typename T>
@@ -433,6 +451,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
   uint64_t* empty = bar + kRNG;         // [kRNG]
   uint64_t* recfull = bar + 2 * kRNG;   // [1]
   uint64_t* slotfree = recfull + 1;     // [kRCMax]: leader l has consumed our last list
+  uint64_t* bound = slotfree + kRCMax;  // [kRNG]: the C chunk bounds of the group's current row
   const int nrows = (a.B > (int)q) ? (a.B - (int)q + (int)nclus - 1) / (int)nclus : 0;  // rows of this cluster
   const int c0 = (int)rank * a.Lc;                                // first local id of this CTA's chunk
   const int nval = max(0, min(a.Lc, a.vloc - c0));                // valid elements of the chunk
@@ -445,6 +464,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
     }
     mbar_init(recfull, C);
     for (int l = 0; l < kRCMax; ++l) mbar_init(slotfree + l, 1);
+    for (int g = 0; g < kRNG; ++g) mbar_init(bound + g, C);
     fence_mbar_init();
   }
   // the previous kernel of the stream (the last step, which appended to the histories) is complete
@@ -462,7 +482,8 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
       const uint32_t bmb = (uint32_t)((nval + 127) / 128 * 16);
       for (int it = 0; it < nrows; ++it) {
         const int g = it % kRNG;
-        if (it >= kRNG) mbar_wait(empty + g, (uint32_t)((it / kRNG - 1) & 1));
+        if (it >= kRNG) mbar_wait_sleep(empty + g, (uint32_t)((it / kRNG - 1) & 1));
+        RTR(it, 0);
         const int64_t r = (int64_t)q + (int64_t)it * nclus;
         RowStage* st = reinterpret_cast<RowStage*>(smem + L.stg) + g;
         if (nval > 0) {  // the logits first: they do not depend on the slot
@@ -475,6 +496,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
         st->prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
         st->slot = slot;
         mbar_arrive(full + g);  // (release: the staged row info above)
+        RTR(it, 1);
       }
     }
   } else if (warp == kRDecW) {
@@ -497,6 +519,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
     for (int it = (int)rank; it < nrows; it += C) {
       const int r = (int)q + it * (int)nclus;
       mbar_wait_cl(recfull, (uint32_t)((it / C) & 1));
+      if (lane == 0) RTR(it, 12);
       const sampling_params prm = ri->prm;
       const int slot = ri->slot;
       const RowCfg rc = decode_row(prm, a.V, a.kcand);
@@ -512,35 +535,34 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
       uint64_t F = warp_max_u64(has ? h.front : 0ull);
       const bool bad = __any_sync(kFull, has && (h.flags & 1u));
       const uint64_t best = warp_max_u64(has ? h.best : 0ull);
-      // candidates >= F into the pool (warp compaction, chunk order)
+      // the candidates of the C chunks (every element of the row >= the row bound, unsorted) into the
+      // pool, then the exact top-keff by rank counting (composites are unique)
+      const int nc = has ? h.n : 0;
+      const int ninc = warp_incl_scan_i(nc, lane);
+      const int tot = __shfl_sync(kFull, ninc, 31);  // (<= C * cap)
       int n = 0;
       if (!rc.greedy) {
-        for (int c = 0; c < C; ++c) {
-          const int nc = min(hdr[c].n, a.cap);
-          for (int i0 = 0; i0 < nc; i0 += 32) {
-            const int i = i0 + lane;
-            const uint64_t v = (i < nc) ? rec[c * a.cap + i] : 0ull;
-            const bool keep = i < nc && v >= F;
-            const unsigned bal = __ballot_sync(kFull, keep);
-            const int at = n + __popc(bal & ((1u << lane) - 1u));
-            if (keep && at < kRPool) ms.pool[at] = v;
-            n += __popc(bal);
-          }
+        for (int c = 0, base = 0; c < C; ++c) {
+          const int ncc = hdr[c].n;
+          for (int i = lane; i < ncc && base + i < tot; i += 32) ms.pool[base + i] = rec[c * a.cap + i];
+          base += ncc;
         }
+        __syncwarp();
+        n = warp_topk(ms.pool, tot, keff, reinterpret_cast<uint64_t*>(ms.wv), ms.top, lane);
       }
       __syncwarp();
       // the chunk lists are consumed: release every sender's slot for this leader
       if (lane < C) cl_arrive_remote(cl_map(smem_u32(slotfree + rank), (uint32_t)lane));
-      const bool over = n > kRPool;
-      n = min(n, kRPool);
       if (rc.greedy) {
         if (lane == 0) ms.top[0] = best;
         __syncwarp();
         n = (best != 0ull) ? 1 : 0;
         F = best;
-      } else {
-        n = warp_topk(ms.pool, n, keff, reinterpret_cast<uint64_t*>(ms.wv), ms.top, lane);
+      } else if (tot > keff && n > 0) {
+        const uint64_t last = ms.top[n - 1];
+        F = last > F ? last : F;
       }
+      if (lane == 0) RTR(it, 13);
       const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
       if (a.mode == 1) {  // vocab-sharded phase 1: the row's candidate record (merge.cuh)
         uint8_t* out = a.out_records + (int64_t)r * a.out_stride;
@@ -554,13 +576,13 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
           o.R = (double)M * rc.c_d;
           o.n = (uint32_t)n;
           o.rsv = 0;
-          o.frontier = over ? ~0ull : F;
+          o.frontier = F;
           *reinterpret_cast<RecHdr*>(out) = o;
         }
         __syncwarp();
         continue;
       }
-      if (!bounded || over) {  // exact.cuh finishes the row from {M, S}
+      if (!bounded) {  // exact.cuh finishes the row from {M, S}
         if (lane == 0) {
           RowInfo o;
           o.M = M;
@@ -583,6 +605,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
       }
       const int tok = warp_decide(ms, n, M, S, F, bad, rc, prm, seed, a.step, r, a.ro, false, nullptr);
       if (a.append && tok >= 0 && lane == 0) hist_append(a.hs, slot, tok);
+      if (lane == 0) RTR(it, 14);
       __syncwarp();
     }
   } else {
@@ -590,160 +613,212 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
     const int g = warp / kRWG;
     const int gt = tid - g * kRGT, gw = gt >> 5;
     const uint8_t* buf = smem + L.buf + g * a.Lc * ESZ;
+    const uint4* buf4 = reinterpret_cast<const uint4*>(buf);
     const uint8_t* bm = smem + L.bm + g * (a.Lc / 8);
     const uint32_t* bmw = reinterpret_cast<const uint32_t*>(bm);
     const RowStage* st = reinterpret_cast<const RowStage*>(smem + L.stg) + g;
-    uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + L.wpre + g * (a.Lc / 32) * 4);
-    int32_t* pli = reinterpret_cast<int32_t*>(smem + L.pli + g * kRPen * 4);
-    uint32_t* pme = reinterpret_cast<uint32_t*>(smem + L.pme + g * kRPen * 4);
-    float* pz = reinterpret_cast<float*>(smem + L.pz + g * kRPen * 4);
+    uint32_t* pme = reinterpret_cast<uint32_t*>(smem + L.pme) + g * kRGT * kPT + gt * kPT;  // this thread's
+    uint32_t* gk = reinterpret_cast<uint32_t*>(smem + L.gk + g * (a.Lc / 16) * 4);        // group keys
     uint8_t* gsc = smem + L.gscr + g * kGScrBytes;
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(gsc);             // [kRGT] thread-max keys | slow-path hist
-    uint8_t* gs = gsc + 1024;
-    uint32_t* s_wm = reinterpret_cast<uint32_t*>(gs);               // [4] max keys (incl. penalised)
-    uint32_t* s_wb = reinterpret_cast<uint32_t*>(gs + 16);          // [4] bad flags
-    double* s_ws = reinterpret_cast<double*>(gs + 32);              // [4] sums
-    uint64_t* s_wbest = reinterpret_cast<uint64_t*>(gs + 64);       // [4] greedy best
-    int* s_cnt = reinterpret_cast<int*>(gs + 96);                   // [2] candidate counters (row parity)
-    int* s_ctl = reinterpret_cast<int*>(gs + 112);                  // [4] slow-path control
-    int* s_ps = reinterpret_cast<int*>(gs + 128);                   // [4] penalised-bit counts per warp
+    uint32_t* s_hist = reinterpret_cast<uint32_t*>(gsc);                     // [256] slow-path histogram
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(gsc);                      // [kRGT] thread-max keys (aliases)
+    uint64_t* lc = reinterpret_cast<uint64_t*>(gsc + 1024);                  // [kRCapL] local candidates
+    uint8_t* gs = gsc + 1024 + kRCapL * 8;
+    uint32_t* s_wm = reinterpret_cast<uint32_t*>(gs);                        // [8] max keys (incl. penalised)
+    uint32_t* s_wb = reinterpret_cast<uint32_t*>(gs + 32);                   // [8] bad flags
+    uint32_t* s_wt = reinterpret_cast<uint32_t*>(gs + 64);                   // [8] per-warp bounds
+    double* s_ws = reinterpret_cast<double*>(gs + 96);                       // [8] sums
+    uint64_t* s_wbest = reinterpret_cast<uint64_t*>(gs + 160);               // [8] greedy best
+    int* s_cnt = reinterpret_cast<int*>(gs + 224);                           // [2] candidate counters
+    int* s_ctl = reinterpret_cast<int*>(gs + 232);                           // [4] slow-path control
+    uint64_t* s_front = reinterpret_cast<uint64_t*>(gs + 248);               // [1] list frontier
     const int gid0 = a.voff + c0;
     const int nw = (nval + 31) >> 5;                 // bitmap words of the chunk
     const int wpt = (nw + kRGT - 1) / kRGT;          // words per thread (contiguous)
     const int w0 = min(nw, gt * wpt), w1 = min(nw, w0 + wpt);
+    const int nfull = nval / VEC;                    // vectors without a ragged tail
+    const uint32_t tailmask = (nvec > nfull) ? (~((1u << (nval - nfull * VEC)) - 1u) & ((1u << VEC) - 1u)) : 0u;
+    const uint4 kNegVec = make_uint4(VEC == 8 ? 0xFF80FF80u : 0xFF800000u, VEC == 8 ? 0xFF80FF80u : 0xFF800000u,
+                                     VEC == 8 ? 0xFF80FF80u : 0xFF800000u, VEC == 8 ? 0xFF80FF80u : 0xFF800000u);
+    // vector v of the chunk with its penalised ids (and the ragged tail) masked to -inf
+    auto ldv = [&](int v) -> uint4 {
+      uint4 u = buf4[v];
+      const uint32_t b = vec_bits<VEC>(bm, v) | (v == nfull ? tailmask : 0u);
+      if (b) u = RV<T>::mask(u, b);
+      return u;
+    };
     for (int it = g; it < nrows; it += kRNG) {
       const int par = (it / kRNG) & 1;
-      mbar_wait(full + g, (uint32_t)par);
+      mbar_wait_sleep(full + g, (uint32_t)par);
+      if (gt == 0) RTR(it, 2);
       const RowStage stc = *st;  // (the producer rewrites the stage once the buffer is released)
-      const sampling_params& prm = stc.prm;
-      const RowCfg rc = decode_row(prm, a.V, a.kcand);
+      const RowCfg rc = decode_row(stc.prm, a.V, a.kcand);
       const int keff = rc.keff;
       const float cf = __fdiv_rn((float)kLog2e, rc.tau);
       const int leader = it % C;
       const uint32_t* gme = a.hs.pmeta + (int64_t)stc.slot * a.hs.vls + c0;
-      // ---- penalised ids of the chunk: the set bits of the presence bitmap.  Index them (group
-      //      scan over contiguous word ranges) and gather their counts asynchronously (LDGSTS),
-      //      behind A1.
-      int mycnt = 0;
-      for (int w = w0; w < w1; ++w) mycnt += __popc(bmw[w]);
-      const int incl = warp_incl_scan_i(mycnt, lane);
-      if (lane == 31) s_ps[gw] = incl;
-      if (gt == 0) {
-        s_cnt[par] = 0;
-        // the leader's list for this row must be free before any candidate is pushed into it
-        if (it >= C) mbar_wait_cl(slotfree + leader, (uint32_t)((it / C - 1) & 1));
-      }
-      gbar(g);
-      int base = incl - mycnt, npen = 0;
-#pragma unroll
-      for (int j = 0; j < kRWG; ++j) {
-        base += (j < gw) ? s_ps[j] : 0;
-        npen += s_ps[j];
-      }
-      for (int w = w0, e = base; w < w1; ++w) {
-        wpre[w] = (uint32_t)e;
+      // ---- penalised ids of this thread's bitmap words: their counts gathered asynchronously
+      //      (LDGSTS) behind the pass; ids beyond kPT per thread are read synchronously after it
+      int pl[kPT];
+      int npt = 0;
+      for (int w = w0; w < w1; ++w) {
         uint32_t bits = bmw[w];
         while (bits) {
           const int l = w * 32 + __ffs(bits) - 1;
           bits &= bits - 1;
-          if (e < kRPen) {
-            pli[e] = l;
-            cp_async4(pme + e, gme + l);
+          if (npt < kPT) {
+#pragma unroll
+            for (int j = 0; j < kPT; ++j)
+              if (j == npt) pl[j] = l;
+            cp_async4(pme + npt, gme + l);
           }
-          ++e;
+          ++npt;
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      PenCtx pc;
-      pc.bmw = bmw;
-      pc.wpre = wpre;
-      pc.li = pli;
-      pc.pz = pz;
-      pc.gme = gme;
-      pc.npen = npen;
-      const bool ovf = npen > kRPen;  // (group-uniform) more penalised ids than staged: in-loop
-      if (ovf) gbar(g);               // wpre complete before any lookup
-      // ---- A1: max over the chunk (penalised ids and the tail masked; NaN-propagating)
-      float tmax = -INFINITY, pmax = -INFINITY;
-      uint32_t pbad = 0;
-      auto ovf_pen = [&](int v, uint32_t pb, auto&& use) {
-        while (pb) {
-          const int l = v * VEC + __ffs(pb) - 1;
-          pb &= pb - 1;
-          const int w = l >> 5;
-          const int e = (int)wpre[w] + __popc(bmw[w] & ((1u << (l & 31)) - 1u));
-          if (e >= kRPen) use(l, apply_penalty(RV<T>::at(buf, l), gme[l], prm, a.pen_mode));
+      // visit this thread's penalised ids beyond the staged ones: fn(l, z')
+      auto extra = [&](auto&& fn) {
+        int j = 0;
+        for (int w = w0; w < w1; ++w) {
+          uint32_t bits = bmw[w];
+          while (bits) {
+            const int l = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (j++ >= kPT) fn(l, apply_penalty(RV<T>::at(buf, l), gme[l], stc.prm, a.pen_mode));
+          }
         }
       };
-      if (VEC == 8) {
-        __nv_bfloat162 acc = __float2bfloat162_rn(-INFINITY);
-        for (int v = gt; v < nvec; v += kRGT) {
-          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
-          const uint32_t pb = vec_bits<VEC>(bm, v);
-          uint32_t b = pb;
-          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & 0xFFu;
-          if (b) {
-            u = RV<T>::mask(u, b);
-            if (ovf && pb)
-              ovf_pen(v, pb, [&](int, float zp) {
-                if (!(zp < INFINITY)) pbad = 1;
-                else pmax = fmaxf(pmax, zp);
-              });
+      // ---- the pass: one read of the chunk, 2 vectors (a "group", <= 16 elements) per iteration.
+      //      Per group: its max (NaN-propagating), kept as the group key for the candidate re-read
+      //      and in the lane's top-R maxima for the bound; the exp-sum of P:149's softmax
+      //      denominator relative to the thread's reference m_ref, rebased only when a group max
+      //      exceeds it by 8/c (every term <= 2^8).
+      float tmax = -INFINITY;
+      float mref = -INFINITY, thr = -INFINITY;
+      double ssum = 0.0;  // sum 2^((z - m_ref) c) of this thread
+      {
+        const float inv8 = __fdiv_rn(8.0f, cf);
+        uint64_t c2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cf), "f"(cf));
+        float acc = 0.f;
+        int nacc = 0;
+        for (int v = gt, k = gt; v < nvec; v += 2 * kRGT, k += kRGT) {
+          const uint4 u0 = ldv(v);
+          const uint4 u1 = (v + kRGT < nvec) ? ldv(v + kRGT) : kNegVec;
+          float gm;
+          if (VEC == 8) {
+            const __nv_bfloat162 m2 =
+                __hmax2_nan(RV<__nv_bfloat16>::vmax2_nan(u0), RV<__nv_bfloat16>::vmax2_nan(u1));
+            gm = fmax_nan(__low2float(m2), __high2float(m2));
+            reinterpret_cast<uint16_t*>(gk)[k] = (uint16_t)(__float_as_uint(gm) >> 16);
+          } else {
+            gm = fmax_nan(RV<float>::vmax_nan(u0), RV<float>::vmax_nan(u1));
+            gk[k] = __float_as_uint(gm);
           }
-          acc = __hmax2_nan(acc, RV<__nv_bfloat16>::vmax2_nan(u));
-        }
-        tmax = fmax_nan(__low2float(acc), __high2float(acc));
-      } else {
-        for (int v = gt; v < nvec; v += kRGT) {
-          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
-          const uint32_t pb = vec_bits<VEC>(bm, v);
-          uint32_t b = pb;
-          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & 0xFu;
-          if (b) {
-            u = RV<T>::mask(u, b);
-            if (ovf && pb)
-              ovf_pen(v, pb, [&](int, float zp) {
-                if (!(zp < INFINITY)) pbad = 1;
-                else pmax = fmaxf(pmax, zp);
-              });
+          tmax = fmax_nan(tmax, gm);
+          if (gm > thr) {  // (rare) rebase; also the thread's first finite group
+            if (acc != 0.f || ssum != 0.0) {
+              const float f = ex2f(__fmul_rn(mref - gm, cf));
+              ssum = (ssum + (double)acc) * (double)f;
+              acc = 0.f;
+              nacc = 0;
+            }
+            mref = gm;
+            thr = gm + inv8;
           }
-          tmax = fmax_nan(tmax, RV<float>::vmax_nan(u));
+          if (mref > -INFINITY) {
+            acc += RV<T>::esum(u0, -mref, cf, c2) + RV<T>::esum(u1, -mref, cf, c2);
+            if (++nacc == 8) {
+              ssum += (double)acc;
+              acc = 0.f;
+              nacc = 0;
+            }
+          }
         }
+        ssum += (double)acc;
       }
-      // ---- the staged penalised values (exact binary32 penalty, P:146 / P:371)
+      if (gt == 0) RTR(it, 3);
+      // ---- this thread's penalised values (exact binary32 penalty, P:146 / P:371)
       cp_async_wait_all();
-      gbar(g);
-      const int nst = min(npen, kRPen);
-      for (int e = gt; e < nst; e += kRGT) {
-        const float zp = apply_penalty(RV<T>::at(buf, pli[e]), pme[e], prm, a.pen_mode);
-        pz[e] = zp;
-        if (!(zp < INFINITY)) pbad = 1;  // NaN / +inf
-        else pmax = fmaxf(pmax, zp);
+      float zpv[kPT];
+      float pmax = -INFINITY;
+      uint32_t pbad = 0;
+#pragma unroll
+      for (int j = 0; j < kPT; ++j) {
+        zpv[j] = -INFINITY;
+        if (j < npt) {
+          zpv[j] = apply_penalty(RV<T>::at(buf, pl[j]), pme[j], stc.prm, a.pen_mode);
+          if (!(zpv[j] < INFINITY)) pbad = 1;  // NaN / +inf
+          else pmax = fmaxf(pmax, zpv[j]);
+        }
       }
+      if (npt > kPT)
+        extra([&](int, float zp) {
+          if (!(zp < INFINITY)) pbad = 1;
+          else pmax = fmaxf(pmax, zp);
+        });
+      if (gt == 0) RTR(it, 4);
+      // ---- group: chunk max (incl. penalised) and bad flag; the bound T_c.  Warp w takes
+      //      T_w = the ceil(keff / 8)-th largest of its 32 thread maxima (one ballot per bit); every
+      //      warp has that many elements >= T_w, so the 8 warps hold >= keff elements >= min_w T_w:
+      //      T_c = min_w T_w is a lower bound of the chunk's (hence the row's) keff-th largest z'.
       const uint32_t bad_t = (tmax != tmax || tmax == INFINITY) ? 1u : pbad;
-      // thread-max key for the bound (unpenalised elements; 0 = none); chunk max incl. penalised
-      s_key[gt] = (bad_t || !(tmax > -INFINITY)) ? 0u : f2key(tmax);
       const float mloc = fmaxf(bad_t ? -INFINITY : tmax, pmax);
       const uint32_t mk = __reduce_max_sync(kFull, f2key(mloc));
       const uint32_t bw = __reduce_or_sync(kFull, bad_t);
-      if (lane == 0) {
-        s_wm[gw] = mk;
-        s_wb[gw] = bw;
+      {
+        const uint32_t key = (bad_t || !(tmax > -INFINITY)) ? 0u : f2key(tmax);
+        const int kw = (keff + kRWG - 1) / kRWG;
+        uint32_t pre = 0;
+#pragma unroll 1
+        for (int bb = 31; bb >= (VEC == 8 ? 16 : 0); --bb) {
+          const uint32_t cand = pre | (1u << bb);
+          if (__popc(__ballot_sync(kFull, key >= cand)) >= kw) pre = cand;
+        }
+        if (lane == 0) {
+          s_wm[gw] = mk;
+          s_wb[gw] = bw;
+          s_wt[gw] = pre;  // 0: fewer than kw non-empty threads in this warp
+        }
       }
-      gbar(g);
-      uint32_t mkey = s_wm[0], badc = s_wb[0];
+      if (gt == 0) s_cnt[par] = 0;
+      gbar(g);  // ---- B1
+      uint32_t mkey = s_wm[0], badc = s_wb[0], tkey = 0xFFFFFFFFu;
+      int nzw = 0;
 #pragma unroll
-      for (int j = 1; j < kRWG; ++j) {
+      for (int j = 0; j < kRWG; ++j) {
         mkey = max(mkey, s_wm[j]);
         badc |= s_wb[j];
+        if (s_wt[j]) {
+          tkey = min(tkey, s_wt[j]);
+          ++nzw;
+        }
       }
+      // (warps with fewer than ceil(keff/8) non-empty threads contribute no bound: the others must
+      //  still hold keff elements, else every finite element is a candidate)
+      if (nzw * ((keff + kRWG - 1) / kRWG) < keff) tkey = 0u;
       const float mc = key2f(mkey);  // chunk max (-inf if empty)
-      // bound T_c: the keff-th largest thread max (0: fewer than keff non-empty threads -> all)
-      const uint32_t tkey = (VEC == 8) ? kth_key<16>(s_key, keff, lane) : kth_key<32>(s_key, keff, lane);
-      const float Tf = tkey ? key2f(tkey) : -INFINITY;
-      // ---- A2: exp-sum relative to the chunk max; candidates >= T pushed into the leader's list
-      const uint32_t rec_remote = cl_map(smem_u32(smem + L.rec), (uint32_t)leader) + rank * (uint32_t)(a.cap * 8);
-      double ssum = 0.0;
+      // ---- the row bound: every CTA's chunk bound to every CTA of the cluster (DSMEM), T = the max
+      //      (each chunk bound is a lower bound of the row's keff-th largest, so their max is too);
+      //      candidates are then only the row's elements >= T, about keff of them in the cluster
+      uint32_t* bs = reinterpret_cast<uint32_t*>(smem + L.bslot) + (g * 2 + par) * kRCMax;
+      if (gt < C) {
+        const uint32_t dst = cl_map(smem_u32(bs + rank), (uint32_t)gt);
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(dst), "r"(tkey) : "memory");
+        cl_arrive_remote(cl_map(smem_u32(bound + g), (uint32_t)gt));
+      }
+      if (gt == 0) RTR(it, 5);
+      mbar_wait_cl(bound + g, (uint32_t)par);
+      uint32_t rkey = 0;
+      bool any0 = false;
+      for (int c = 0; c < C; ++c) {
+        rkey = max(rkey, bs[c]);
+        any0 |= bs[c] == 0u;
+      }
+      (void)any0;
+      const float Tf = rkey ? key2f(rkey) : -INFINITY;
+      // ---- S_c relative to the chunk max; candidates: the groups whose key reaches the bound are
+      //      re-read, every element >= T pushed into the group's list
       uint64_t tbest = 0ull;
       const bool live = !badc && mc > -INFINITY;
       auto push = [&](float z, int gid) {
@@ -752,92 +827,80 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
           tbest = cmp > tbest ? cmp : tbest;
         } else {
           const int at = atomicAdd(&s_cnt[par], 1);
-          if (at < a.cap) cl_st64(rec_remote + (uint32_t)at * 8u, cmp);
+          if (at < kRCapL) lc[at] = cmp;
         }
       };
       if (live) {
-        const float nm = -mc;
-        uint64_t c2;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cf), "f"(cf));
-        float acc = 0.f;
-        int nacc = 0;
-        for (int v = gt; v < nvec; v += kRGT) {
-          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
-          const uint32_t pb = vec_bits<VEC>(bm, v);
-          uint32_t b = pb;
-          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
-          if (b) {
-            u = RV<T>::mask(u, b);
-            if (ovf && pb)
-              ovf_pen(v, pb, [&](int l, float zp) {
-                if (zp > -INFINITY) {
-                  ssum += (double)ex2f(__fmul_rn(__fsub_rn(zp, mc), cf));
-                  if (zp >= Tf) push(zp, gid0 + l);
-                }
-              });
-          }
-          acc += RV<T>::esum(u, nm, cf, c2);
-          if (++nacc == 8) {
-            ssum += (double)acc;
-            acc = 0.f;
-            nacc = 0;
-          }
-          if (RV<T>::vmax(u) >= Tf) {
+        ssum = (ssum != 0.0) ? ssum * (double)ex2f(__fmul_rn(mref - mc, cf)) : 0.0;
+        for (int v = gt, k = gt; v < nvec; v += 2 * kRGT, k += kRGT) {
+          const float gm = (VEC == 8) ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(gk)[k] << 16)
+                                      : __uint_as_float(gk[k]);
+          if (!(gm >= Tf && gm > -INFINITY)) continue;
+          for (int h = 0; h < 2; ++h) {
+            const int vv = v + h * kRGT;
+            if (vv >= nvec) break;
+            const uint4 u = ldv(vv);
 #pragma unroll
-            for (int t = 0; t < VEC; ++t) {
-              const float z = RV<T>::elem(u, t);
-              if (z >= Tf && z > -INFINITY) push(z, gid0 + v * VEC + t);
+            for (int tt = 0; tt < VEC; ++tt) {
+              const float z = RV<T>::elem(u, tt);
+              if (z >= Tf && z > -INFINITY) push(z, gid0 + vv * VEC + tt);
             }
           }
         }
-        ssum += (double)acc;
-        for (int e = gt; e < nst; e += kRGT) {
-          const float zp = pz[e];
+        auto pen_use = [&](int l, float zp) {
           if (zp > -INFINITY) {
             ssum += (double)ex2f(__fmul_rn(__fsub_rn(zp, mc), cf));
-            if (zp >= Tf) push(zp, gid0 + pli[e]);
+            if (zp >= Tf) push(zp, gid0 + l);
           }
-        }
+        };
+#pragma unroll
+        for (int j = 0; j < kPT; ++j)
+          if (j < npt) pen_use(pl[j], zpv[j]);
+        if (npt > kPT) extra(pen_use);
+      } else {
+        ssum = 0.0;
       }
-      // ---- reductions (fixed order)
+      if (gt == 0) RTR(it, 6);
       ssum = warp_sum_d(ssum);
       tbest = warp_max_u64(tbest);
       if (lane == 0) {
         s_ws[gw] = ssum;
         s_wbest[gw] = tbest;
       }
-      gbar(g);
+      // the leader's list for this row must be free before this chunk's list is written into it
+      if (gt == 0 && it >= C) mbar_wait_cl(slotfree + leader, (uint32_t)((it / C - 1) & 1));
+      gbar(g);  // ---- B2
       int cnt = s_cnt[par];
-      uint64_t front = tkey ? make_comp(Tf, 0x7FFFFFFF) : 0ull;
+      uint64_t front = rkey ? make_comp(Tf, 0x7FFFFFFF) : 0ull;
       if (live && !rc.greedy && cnt > a.cap) {
         // massive ties: the chunk's exact top-keff by composite, then the list again (rare)
-        const uint64_t kc = group_kth_comp<T>(buf, bm, nvec, nval, pc, prm, a.pen_mode, gid0, Tf, keff, s_key,
-                                              s_ctl, g);
+        const uint64_t kc = group_kth_comp<T>(buf, bm, nvec, nval, gme, stc.prm, a.pen_mode, gid0, Tf, keff,
+                                              s_hist, s_ctl, g);
         if (gt == 0) s_cnt[par] = 0;
         gbar(g);
         for (int v = gt; v < nvec; v += kRGT) {
-          uint4 u = reinterpret_cast<const uint4*>(buf)[v];
+          const uint4 u = ldv(v);
           const uint32_t pb = vec_bits<VEC>(bm, v);
-          uint32_t b = pb;
-          if ((v + 1) * VEC > nval) b |= ~((1u << (nval - v * VEC)) - 1u) & ((1u << VEC) - 1u);
-          if (b) u = RV<T>::mask(u, b);
 #pragma unroll
           for (int t = 0; t < VEC; ++t) {
             float z = RV<T>::elem(u, t);
-            if ((pb >> t) & 1u) z = pc.value<T>(v * VEC + t, buf, prm, a.pen_mode);
-            if (z >= Tf && z > -INFINITY && z < INFINITY && make_comp(z, gid0 + v * VEC + t) >= kc)
-              push(z, gid0 + v * VEC + t);
+            const int l = v * VEC + t;
+            if ((pb >> t) & 1u) z = apply_penalty(RV<T>::at(buf, l), gme[l], stc.prm, a.pen_mode);
+            if (z >= Tf && z > -INFINITY && z < INFINITY && make_comp(z, gid0 + l) >= kc) push(z, gid0 + l);
           }
         }
         gbar(g);
         cnt = s_cnt[par];
-        front = kc;
+        front = kc > front ? kc : front;
       }
       // the buffer is consumed
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + g);
-      cl_fence();  // this thread's list entries, before the leader is signalled
-      gbar(g);
+      // ---- this chunk's candidates into the leader's list (DSMEM stores), then the record
+      const int nout = rc.greedy ? 0 : min(cnt, a.cap);
+      const uint32_t rec_remote = cl_map(smem_u32(smem + L.rec), (uint32_t)leader) + rank * (uint32_t)(a.cap * 8);
+      for (int i = gt; i < nout; i += kRGT) cl_st64(rec_remote + (uint32_t)i * 8u, lc[i]);
+      gbar(g);  // ---- B3
       if (gt == 0) {
         RecC h;
         h.m = mc;
@@ -852,14 +915,19 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
         h.s = s;
         h.front = front;
         h.best = bb;
-        h.n = min(cnt, a.cap);
+        h.n = nout;
         h.pad[0] = h.pad[1] = h.pad[2] = 0;
         const uint32_t hr = cl_map(smem_u32(smem + L.hdr), (uint32_t)leader) + rank * (uint32_t)sizeof(RecC);
         const uint4* hv = reinterpret_cast<const uint4*>(&h);
 #pragma unroll
         for (int j = 0; j < (int)(sizeof(RecC) / 16); ++j) cl_st128(hr + 16 * j, hv[j]);
         if (rank == (uint32_t)leader) *reinterpret_cast<RowStage*>(smem + L.rinfo) = stc;  // for the decider
+        cl_fence();  // the group's list entries (ordered before this thread by the barrier) and the header
         cl_arrive_remote(cl_map(smem_u32(recfull), (uint32_t)leader));
+        RTR(it, 7);
+        RTV(it, 8, cnt);
+        RTV(it, 9, tkey);
+        RTV(it, 10, rkey);
       }
     }
   }

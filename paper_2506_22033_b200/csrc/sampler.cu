@@ -45,6 +45,7 @@ struct sampler {
   std::vector<sampling_params> h_params;
   std::string err;
   int32_t last_launches = 0;
+  uint64_t* d_trace = nullptr;  // SMP_TRACE builds only
   // per-kernel timing (sampler_set_timing)
   bool timing = false;
   cudaEvent_t tev[4] = {};
@@ -239,7 +240,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   for (int i = 0; i < 5; ++i) {
     const int C = 1 << i;
     const int Lc = (int)(((int64_t)c.vocab_local + C - 1) / C + kLcAlign - 1) / kLcAlign * kLcAlign;
-    const int cap = 256;
+    const int cap = SAMPLER_KCAND_MAX;  // sorted chunk lists hold at most max_top_k entries
     const int sm = rlayout(C, Lc, h->esz, cap).total;
     if (sm > smem_max) continue;
     h->rk_lc[i] = Lc;
@@ -278,6 +279,12 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     }
     h->rk_maxclus[i] = n;
   }
+#ifdef SMP_TRACE
+  if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * 16 * kTrRows * (size_t)(2 * h->sm_count)) != cudaSuccess)
+    h->d_trace = nullptr;
+  else
+    cudaMemset(h->d_trace, 0, sizeof(uint64_t) * 16 * kTrRows * (size_t)(2 * h->sm_count));
+#endif
   *out = h;
   return SAMPLER_OK;
 }
@@ -292,6 +299,7 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_info);
   cudaFree(h->d_scratch);
   cudaFree(h->d_pmask);
+  cudaFree(h->d_trace);
   for (auto& e : h->tev)
     if (e) cudaEventDestroy(e);
   delete h;
@@ -501,6 +509,7 @@ static int launch_rows(sampler* h, const void* logits, int64_t ld, int32_t B, co
   a.ro = ro;
   a.out_records = out_records;
   a.out_stride = h->rec_stride;
+  a.trace = h->d_trace;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.nclus * p.C));
   cfg.blockDim = dim3(kRThreads);
@@ -641,7 +650,10 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
 
 int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n) {
   if (!h || !host_out || n < 0) return SAMPLER_EINVAL;
-  return SAMPLER_EUNSUPPORTED;  // (no trace buffers in this build)
+  if (!h->d_trace) return SAMPLER_EUNSUPPORTED;  // (product builds carry no trace buffers)
+  const size_t m = std::min<size_t>((size_t)n, (size_t)16 * kTrRows * 2 * h->sm_count);
+  if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess) return SAMPLER_ECUDA;
+  return SAMPLER_OK;
 }
 
 int64_t sampler_record_bytes(const sampler* h, int32_t B) {

@@ -14,6 +14,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, kre, fn = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+by_inst = len(sys.argv) > 5 and sys.argv[5] == 'inst'
 
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kre}"],
                      capture_output=True, text=True).stdout
@@ -53,7 +54,8 @@ for r in d:
 tot = sum(S.values())
 srcs = {}
 print("samples", tot)
-for loc, v in S.most_common(top):
+for loc, v in (I if by_inst else S).most_common(top):
+    v = S[loc]
     path = os.path.join(ROOT, "paper_2506_22033_b200", "csrc", loc[0])
     if loc[0] not in srcs and os.path.exists(path):
         srcs[loc[0]] = open(path).read().splitlines()
