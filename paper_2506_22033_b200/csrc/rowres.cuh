@@ -35,16 +35,21 @@
 
 namespace smp {
 
-constexpr int kRNG = 2;                     // row groups (= chunk buffers) per CTA
-constexpr int kRWG = 8;                     // warps per row group
-constexpr int kRGT = kRWG * 32;             // threads per row group
-constexpr int kRThreads = kRNG * kRGT + 64; // + producer warp + decider warp
-constexpr int kRProdW = kRNG * kRWG;        // producer warp index
-constexpr int kRDecW = kRProdW + 1;         // decider warp index
-constexpr int kPT = 4;                      // penalised ids staged per thread and row (more: read synchronously)
-constexpr int kRCMax = 16;                  // max cluster size
-constexpr int kRCapL = 256;                 // local candidate list per row group
-constexpr int kLcAlign = 128;               // chunk length granularity (16-byte bitmap rows, 16-byte copies)
+constexpr int kRNB = 2;                      // chunk buffers per CTA
+constexpr int kSW = 12;                      // stream warps (the pass over each chunk)
+constexpr int kST = kSW * 32;                // stream threads
+constexpr int kNF = 2;                       // finisher groups (rows alternate between them)
+constexpr int kFW = 4;                       // warps per finisher group
+constexpr int kFT = kFW * 32;                // threads per finisher group
+constexpr int kNS = 3;                       // summary slots (rows passed, not yet finished)
+constexpr int kRProdW = kSW + kNF * kFW;     // producer warp index
+constexpr int kRDecW = kRProdW + 1;          // decider warp index
+constexpr int kRThreads = (kRDecW + 1) * 32;
+constexpr int kPT = 4;                       // penalised ids staged per stream thread and row
+constexpr int kPenS = 256;                   // penalised (id, z') entries per summary slot (more: slow path)
+constexpr int kRCMax = 16;                   // max cluster size
+constexpr int kRCapL = 256;                  // local candidate list per finisher group
+constexpr int kLcAlign = 128;                // chunk length granularity (16-byte bitmap rows, 16-byte copies)
 
 // per-row staging, written by the producer next to the bulk copies of the chunk
 struct __align__(16) RowStage {
@@ -105,10 +110,20 @@ constexpr int kTrRows = 64;
 #endif
 
 // ---- shared-memory layout (host and device) ----------------------------------------
-struct RLay {
-  int buf, bm, stg, pme, gk, rinfo, hdr, rec, pool, top, wv, byid, dscr, gscr, bslot, bar, total;
+// summary slot (one passed row): per stream thread t its max (incl. penalised), exp-sum reference and
+// sum; per group (2 vectors of one thread) its max key; the penalised (id, z') of the chunk; flags
+struct SlotHdr {
+  sampling_params prm;
+  int32_t slot, npen, bad, pad;
 };
-constexpr int kGScrBytes = 1024 + kRCapL * 8 + 256;
+__host__ __device__ inline int slot_bytes(int Lc, int esz) {
+  const int keys = (Lc / 16) * (esz == 2 ? 2 : 4);
+  return (int)sizeof(SlotHdr) + kST * 12 + (keys + 15) / 16 * 16 + kPenS * 8;
+}
+struct RLay {
+  int buf, bm, stg, pme, sl, slb, rinfo, hdr, rec, pool, top, wv, byid, dscr, fscr, bslot, bar, total;
+};
+constexpr int kFScrBytes = kRCapL * 8 + 256;
 __host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
   RLay l;
   int o = 0;
@@ -117,11 +132,12 @@ __host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
     o += (bytes + 127) / 128 * 128;
     return r;
   };
-  l.buf = A(kRNG * Lc * esz);
-  l.bm = A(kRNG * (Lc / 8));
-  l.stg = A(kRNG * (int)sizeof(RowStage));
-  l.pme = A(kRNG * kRGT * kPT * 4);
-  l.gk = A(kRNG * (Lc / 16) * 4);  // group keys: one per 2 vectors (<= 16 elements)
+  l.buf = A(kRNB * Lc * esz);
+  l.bm = A(kRNB * (Lc / 8));
+  l.stg = A(kRNB * (int)sizeof(RowStage));
+  l.pme = A(kST * kPT * 4);
+  l.slb = (slot_bytes(Lc, esz) + 127) / 128 * 128;
+  l.sl = A(kNS * l.slb);
   l.rinfo = A((int)sizeof(RowStage));
   l.hdr = A(C * (int)sizeof(RecC));
   l.rec = A(C * cap * 8);
@@ -130,9 +146,9 @@ __host__ __device__ inline RLay rlayout(int C, int Lc, int esz, int cap) {
   l.wv = A((SAMPLER_KCAND_MAX + 64) * 8);  // (also warp_topk's survivor scratch)
   l.byid = A(SAMPLER_KCAND_MAX * 8);
   l.dscr = A(512);
-  l.gscr = A(kRNG * kGScrBytes);
-  l.bslot = A(kRNG * 2 * kRCMax * 4);  // row bounds exchanged between the cluster's CTAs
-  l.bar = A((3 * kRNG + 1 + kRCMax) * 8);
+  l.fscr = A(kNF * kFScrBytes);
+  l.bslot = A(kNF * 2 * kRCMax * 4);  // row bounds exchanged between the cluster's CTAs
+  l.bar = A((2 * kRNB + 2 * kNS + kNF + 1 + kRCMax) * 8);
   l.total = o;
   return l;
 }
@@ -199,8 +215,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// named barrier of one row group (ids 1..kRNG)
-__device__ __forceinline__ void gbar(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kRGT) : "memory"); }
+// named barrier of one finisher group (ids 1..kNF)
+__device__ __forceinline__ void fbar(int f) { asm volatile("bar.sync %0, %1;" ::"r"(f + 1), "n"(kFT) : "memory"); }
 
 // ---- element formats ----------------------------------------------------------------
 template <typename T>
@@ -302,76 +318,6 @@ __device__ __forceinline__ uint32_t vec_bits(const uint8_t* bm, int v) {
   return (bm[v >> 1] >> ((v & 1) * 4)) & 0xFu;
 }
 
-// keff-th largest of the kRGT keys s_key[] (one warp, every warp of the group redundantly): MSB
-// first, the largest x with |{keys >= x}| >= keff.  Keys of bf16 values are exact in their top 16
-// bits (NB = 16); fp32 keys use all 32.  Returns 0 when fewer than keff keys are non-zero.
-template <int NB>
-__device__ __forceinline__ uint32_t kth_key(const uint32_t* s_key, int keff, int lane) {
-  uint32_t k[kRGT / 32];
-#pragma unroll
-  for (int i = 0; i < kRGT / 32; ++i) k[i] = s_key[lane + 32 * i];
-  uint32_t pre = 0;
-#pragma unroll 1
-  for (int b = 31; b >= 32 - NB; --b) {
-    const uint32_t cand = pre | (1u << b);
-    uint32_t c = 0;
-#pragma unroll
-    for (int i = 0; i < kRGT / 32; ++i) c += (k[i] >= cand) ? 1u : 0u;
-    if ((int)__reduce_add_sync(kFull, c) >= keff) pre = cand;
-  }
-  return pre;
-}
-
-// Exact top-keff of a chunk whose candidates overflow the list (massive ties): radix select of
-// the keff-th largest composite among the elements >= Tf (8-bit digits, MSB first), over the
-// chunk in shared memory (penalised ids re-evaluated from their counts).  One row group.
-template <typename T>
-__device__ __noinline__ uint64_t group_kth_comp(const uint8_t* buf, const uint8_t* bm, int nvec, int nval,
-                                                const uint32_t* gme, const sampling_params& prm, int pen_mode,
-                                                int gid0, float Tf, int keff, uint32_t* hist, int* ctl, int g) {
-  constexpr int VEC = RV<T>::N;
-  const int tid = threadIdx.x - g * kRGT;
-  const int nfull = nval / VEC;
-  const uint32_t tailmask = (nvec > nfull) ? (~((1u << (nval - nfull * VEC)) - 1u) & ((1u << VEC) - 1u)) : 0u;
-  uint64_t pre = 0;
-  int need = keff;
-  for (int d = 56; d >= 0; d -= 8) {
-    for (int i = tid; i < 256; i += kRGT) hist[i] = 0;
-    gbar(g);
-    for (int v = tid; v < nvec; v += kRGT) {
-      uint4 u = reinterpret_cast<const uint4*>(buf)[v];
-      const uint32_t pb = vec_bits<VEC>(bm, v);
-      const uint32_t b = pb | (v == nfull ? tailmask : 0u);
-      if (b) u = RV<T>::mask(u, b);
-#pragma unroll
-      for (int t = 0; t < VEC; ++t) {
-        float z = RV<T>::elem(u, t);
-        const int l = v * VEC + t;
-        if ((pb >> t) & 1u) z = apply_penalty(RV<T>::at(buf, l), gme[l], prm, pen_mode);
-        if (z >= Tf && z > -INFINITY && z < INFINITY) {
-          const uint64_t c = make_comp(z, gid0 + l);
-          if (d == 56 || (c >> (d + 8)) == pre) atomicAdd(&hist[(c >> d) & 255], 1u);
-        }
-      }
-    }
-    gbar(g);
-    if (tid == 0) {  // the digit: running count from the top
-      int run = 0, dg = 255;
-      for (; dg > 0; --dg) {
-        if (run + (int)hist[dg] >= need) break;
-        run += (int)hist[dg];
-      }
-      ctl[0] = dg;
-      ctl[1] = run;
-    }
-    gbar(g);
-    need -= ctl[1];
-    pre = (pre << 8) | (uint64_t)ctl[0];
-    gbar(g);
-  }
-  return pre;
-}
-
 // The keff largest of pool[0..n) (unique composites) into top[0..min(n, keff)), sorted descending;
 // one warp.  The keff-th largest value key by bitwise radix select (ballot counts; the bits above
 // the first one where the largest and smallest key differ are common to all), the survivors (key
@@ -447,25 +393,40 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
   const uint32_t rank = cl_rank(), q = cl_id(), nclus = cl_num();
   const int C = a.C;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* full = bar;                 // [kRNG]
-  uint64_t* empty = bar + kRNG;         // [kRNG]
-  uint64_t* recfull = bar + 2 * kRNG;   // [1]
-  uint64_t* slotfree = recfull + 1;     // [kRCMax]: leader l has consumed our last list
-  uint64_t* bound = slotfree + kRCMax;  // [kRNG]: the C chunk bounds of the group's current row
+  uint64_t* full = bar;                  // [kRNB] chunk landed
+  uint64_t* empty = full + kRNB;         // [kRNB] chunk consumed by the stream warps
+  uint64_t* spass = empty + kRNB;        // [kNS] summary slot written (stream warps)
+  uint64_t* sfree = spass + kNS;         // [kNS] summary slot released (finisher)
+  uint64_t* bound = sfree + kNS;         // [kNF] the C chunk bounds of the finisher's current row
+  uint64_t* recfull = bound + kNF;       // [1] the C chunk records of a row this CTA leads
+  uint64_t* slotfree = recfull + 1;      // [kRCMax] leader l has consumed our last list
   const int nrows = (a.B > (int)q) ? (a.B - (int)q + (int)nclus - 1) / (int)nclus : 0;  // rows of this cluster
   const int c0 = (int)rank * a.Lc;                                // first local id of this CTA's chunk
   const int nval = max(0, min(a.Lc, a.vloc - c0));                // valid elements of the chunk
   const int nvec = (nval + VEC - 1) / VEC;
+  const int nfull = nval / VEC;                                   // vectors without a ragged tail
+  const uint32_t tailmask = (nvec > nfull) ? (~((1u << (nval - nfull * VEC)) - 1u) & ((1u << VEC) - 1u)) : 0u;
+  const int nw = (nval + 31) >> 5;                                // bitmap words of the chunk
+  const uint8_t* lg = reinterpret_cast<const uint8_t*>(a.logits);
 
   if (tid == 0) {
-    for (int g = 0; g < kRNG; ++g) {
-      mbar_init(full + g, 1);
-      mbar_init(empty + g, kRWG);
+    for (int b = 0; b < kRNB; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(empty + b, kSW);
     }
+    for (int s2 = 0; s2 < kNS; ++s2) {
+      mbar_init(spass + s2, kSW);
+      mbar_init(sfree + s2, 1);
+    }
+    for (int f = 0; f < kNF; ++f) mbar_init(bound + f, C);
     mbar_init(recfull, C);
     for (int l = 0; l < kRCMax; ++l) mbar_init(slotfree + l, 1);
-    for (int g = 0; g < kRNG; ++g) mbar_init(bound + g, C);
     fence_mbar_init();
+  }
+  for (int i = tid; i < kNS; i += blockDim.x) {  // summary slots start empty
+    SlotHdr* sh = reinterpret_cast<SlotHdr*>(smem + L.sl + i * L.slb);
+    sh->npen = 0;
+    sh->bad = 0;
   }
   // the previous kernel of the stream (the last step, which appended to the histories) is complete
   // before any memory access; the next step may be scheduled as this grid retires
@@ -476,26 +437,26 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
   if (warp == kRProdW) {
     // ================= producer: bulk copies of this CTA's chunk of each row =================
     if (lane == 0 && nrows > 0) {
-      const uint64_t pol = l2_evict_first_policy();
-      const uint8_t* lg = reinterpret_cast<const uint8_t*>(a.logits);
+      // L2 evict-normal: the finishers re-read the few candidate groups of a chunk from L2
       const uint32_t dbytes = (uint32_t)((nval * ESZ + 15) / 16 * 16);
       const uint32_t bmb = (uint32_t)((nval + 127) / 128 * 16);
       for (int it = 0; it < nrows; ++it) {
-        const int g = it % kRNG;
-        if (it >= kRNG) mbar_wait_sleep(empty + g, (uint32_t)((it / kRNG - 1) & 1));
+        const int b = it % kRNB;
+        if (it >= kRNB) mbar_wait_sleep(empty + b, (uint32_t)((it / kRNB - 1) & 1));
         RTR(it, 0);
         const int64_t r = (int64_t)q + (int64_t)it * nclus;
-        RowStage* st = reinterpret_cast<RowStage*>(smem + L.stg) + g;
+        RowStage* st = reinterpret_cast<RowStage*>(smem + L.stg) + b;
         if (nval > 0) {  // the logits first: they do not depend on the slot
-          mbar_expect_tx(full + g, dbytes + bmb);
-          bulk_g2s(smem + L.buf + g * a.Lc * ESZ, lg + (r * a.ld + c0) * ESZ, dbytes, full + g, pol);
+          mbar_expect_tx(full + b, dbytes + bmb);
+          bulk_g2s_nohint(smem + L.buf + b * a.Lc * ESZ, lg + (r * a.ld + c0) * ESZ, dbytes, full + b);
         }
         const int slot = a.slots ? a.slots[r] : (int)r;
         if (nval > 0)
-          bulk_g2s(smem + L.bm + g * (a.Lc / 8), a.hs.pmask + (int64_t)slot * a.hs.pmw + c0 / 32, bmb, full + g, pol);
+          bulk_g2s_nohint(smem + L.bm + b * (a.Lc / 8), a.hs.pmask + (int64_t)slot * a.hs.pmw + c0 / 32, bmb,
+                          full + b);
         st->prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
         st->slot = slot;
-        mbar_arrive(full + g);  // (release: the staged row info above)
+        mbar_arrive(full + b);  // (release: the staged row info above)
         RTR(it, 1);
       }
     }
@@ -534,6 +495,7 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
       const double S = warp_sum_d(term);
       uint64_t F = warp_max_u64(has ? h.front : 0ull);
       const bool bad = __any_sync(kFull, has && (h.flags & 1u));
+      const bool ovf = __any_sync(kFull, has && (h.flags & 2u));  // a chunk list overflowed (massive ties)
       const uint64_t best = warp_max_u64(has ? h.best : 0ull);
       // the candidates of the C chunks (every element of the row >= the row bound, unsorted) into the
       // pool, then the exact top-keff by rank counting (composites are unique)
@@ -576,13 +538,13 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
           o.R = (double)M * rc.c_d;
           o.n = (uint32_t)n;
           o.rsv = 0;
-          o.frontier = F;
+          o.frontier = ovf ? ~0ull : F;
           *reinterpret_cast<RecHdr*>(out) = o;
         }
         __syncwarp();
         continue;
       }
-      if (!bounded) {  // exact.cuh finishes the row from {M, S}
+      if (!bounded || ovf) {  // exact.cuh finishes the row from {M, S}
         if (lane == 0) {
           RowInfo o;
           o.M = M;
@@ -608,57 +570,44 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
       if (lane == 0) RTR(it, 14);
       __syncwarp();
     }
-  } else {
-    // ================= row groups: rows it = g, g + kRNG, ... =================
-    const int g = warp / kRWG;
-    const int gt = tid - g * kRGT, gw = gt >> 5;
-    const uint8_t* buf = smem + L.buf + g * a.Lc * ESZ;
-    const uint4* buf4 = reinterpret_cast<const uint4*>(buf);
-    const uint8_t* bm = smem + L.bm + g * (a.Lc / 8);
-    const uint32_t* bmw = reinterpret_cast<const uint32_t*>(bm);
-    const RowStage* st = reinterpret_cast<const RowStage*>(smem + L.stg) + g;
-    uint32_t* pme = reinterpret_cast<uint32_t*>(smem + L.pme) + g * kRGT * kPT + gt * kPT;  // this thread's
-    uint32_t* gk = reinterpret_cast<uint32_t*>(smem + L.gk + g * (a.Lc / 16) * 4);        // group keys
-    uint8_t* gsc = smem + L.gscr + g * kGScrBytes;
-    uint32_t* s_hist = reinterpret_cast<uint32_t*>(gsc);                     // [256] slow-path histogram
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(gsc);                      // [kRGT] thread-max keys (aliases)
-    uint64_t* lc = reinterpret_cast<uint64_t*>(gsc + 1024);                  // [kRCapL] local candidates
-    uint8_t* gs = gsc + 1024 + kRCapL * 8;
-    uint32_t* s_wm = reinterpret_cast<uint32_t*>(gs);                        // [8] max keys (incl. penalised)
-    uint32_t* s_wb = reinterpret_cast<uint32_t*>(gs + 32);                   // [8] bad flags
-    uint32_t* s_wt = reinterpret_cast<uint32_t*>(gs + 64);                   // [8] per-warp bounds
-    double* s_ws = reinterpret_cast<double*>(gs + 96);                       // [8] sums
-    uint64_t* s_wbest = reinterpret_cast<uint64_t*>(gs + 160);               // [8] greedy best
-    int* s_cnt = reinterpret_cast<int*>(gs + 224);                           // [2] candidate counters
-    int* s_ctl = reinterpret_cast<int*>(gs + 232);                           // [4] slow-path control
-    uint64_t* s_front = reinterpret_cast<uint64_t*>(gs + 248);               // [1] list frontier
-    const int gid0 = a.voff + c0;
-    const int nw = (nval + 31) >> 5;                 // bitmap words of the chunk
-    const int wpt = (nw + kRGT - 1) / kRGT;          // words per thread (contiguous)
-    const int w0 = min(nw, gt * wpt), w1 = min(nw, w0 + wpt);
-    const int nfull = nval / VEC;                    // vectors without a ragged tail
-    const uint32_t tailmask = (nvec > nfull) ? (~((1u << (nval - nfull * VEC)) - 1u) & ((1u << VEC) - 1u)) : 0u;
+  } else if (warp < kSW) {
+    // ================= stream warps: the pass over each chunk (no block barrier) =================
+    const int t = tid;
     const uint4 kNegVec = make_uint4(VEC == 8 ? 0xFF80FF80u : 0xFF800000u, VEC == 8 ? 0xFF80FF80u : 0xFF800000u,
                                      VEC == 8 ? 0xFF80FF80u : 0xFF800000u, VEC == 8 ? 0xFF80FF80u : 0xFF800000u);
-    // vector v of the chunk with its penalised ids (and the ragged tail) masked to -inf
-    auto ldv = [&](int v) -> uint4 {
-      uint4 u = buf4[v];
-      const uint32_t b = vec_bits<VEC>(bm, v) | (v == nfull ? tailmask : 0u);
-      if (b) u = RV<T>::mask(u, b);
-      return u;
-    };
-    for (int it = g; it < nrows; it += kRNG) {
-      const int par = (it / kRNG) & 1;
-      mbar_wait_sleep(full + g, (uint32_t)par);
-      if (gt == 0) RTR(it, 2);
-      const RowStage stc = *st;  // (the producer rewrites the stage once the buffer is released)
-      const RowCfg rc = decode_row(stc.prm, a.V, a.kcand);
-      const int keff = rc.keff;
-      const float cf = __fdiv_rn((float)kLog2e, rc.tau);
-      const int leader = it % C;
-      const uint32_t* gme = a.hs.pmeta + (int64_t)stc.slot * a.hs.vls + c0;
-      // ---- penalised ids of this thread's bitmap words: their counts gathered asynchronously
-      //      (LDGSTS) behind the pass; ids beyond kPT per thread are read synchronously after it
+    uint32_t* pme = reinterpret_cast<uint32_t*>(smem + L.pme) + t * kPT;  // this thread's staged counts
+    const int wpt = (nw + kST - 1) / kST;                                  // bitmap words per thread
+    const int w0 = min(nw, t * wpt), w1 = min(nw, w0 + wpt);
+    for (int it = 0; it < nrows; ++it) {
+      const int b = it % kRNB, sidx = it % kNS;
+      const uint8_t* buf = smem + L.buf + b * a.Lc * ESZ;
+      const uint4* buf4 = reinterpret_cast<const uint4*>(buf);
+      const uint8_t* bm = smem + L.bm + b * (a.Lc / 8);
+      const uint32_t* bmw = reinterpret_cast<const uint32_t*>(bm);
+      uint8_t* sl = smem + L.sl + sidx * L.slb;
+      SlotHdr* sh = reinterpret_cast<SlotHdr*>(sl);
+      float* s_tmax = reinterpret_cast<float*>(sl + sizeof(SlotHdr));
+      float* s_mref = s_tmax + kST;
+      float* s_ssum = s_mref + kST;
+      uint8_t* s_keys = reinterpret_cast<uint8_t*>(s_ssum + kST);
+      int2* s_pen = reinterpret_cast<int2*>(s_keys + ((a.Lc / 16) * (ESZ == 2 ? 2 : 4) + 15) / 16 * 16);
+      // the summary slot must be released by the finisher of the row kNS before
+      if (it >= kNS) mbar_wait_sleep(sfree + sidx, (uint32_t)((it / kNS - 1) & 1));
+      mbar_wait_sleep(full + b, (uint32_t)((it / kRNB) & 1));
+      if (t == 0) RTR(it, 2);
+      const RowStage* st = reinterpret_cast<const RowStage*>(smem + L.stg) + b;
+      const sampling_params prm = st->prm;
+      const int slot = st->slot;
+      if (t == 0) {
+        sh->prm = prm;
+        sh->slot = slot;
+      }
+      const float temp = prm.temperature;
+      const float tau = (temp < kGreedyEps) ? 1.0f : temp;
+      const float cf = __fdiv_rn((float)kLog2e, tau);
+      const float inv8 = __fdiv_rn(8.0f, cf);
+      const uint32_t* gme = a.hs.pmeta + (int64_t)slot * a.hs.vls + c0;
+      // penalised ids of this thread's bitmap words: counts gathered behind the pass (LDGSTS)
       int pl[kPT];
       int npt = 0;
       for (int w = w0; w < w1; ++w) {
@@ -676,244 +625,278 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      // visit this thread's penalised ids beyond the staged ones: fn(l, z')
-      auto extra = [&](auto&& fn) {
+      // ---- the pass: 2 vectors (a "group", <= 16 elements) per iteration.  Per group its max
+      //      (NaN-propagating; its key kept for the finisher's candidate re-read); the exp-sum of
+      //      P:149's softmax denominator relative to the thread's reference m_ref, rebased only
+      //      when a group max exceeds it by 8/c (every term <= 2^8).  Penalised ids and the
+      //      ragged tail are masked to -inf (the penalised ones enter below as exact values).
+      float tmax = -INFINITY, mref = -INFINITY, thr = -INFINITY;
+      float ssum = 0.f;
+      uint32_t bad = 0;
+      {
+        uint64_t c2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cf), "f"(cf));
+        for (int v = t, k = t; v < nvec; v += 2 * kST, k += kST) {
+          uint4 u0 = buf4[v];
+          uint4 u1 = (v + kST < nvec) ? buf4[v + kST] : kNegVec;
+          const uint32_t b0 = vec_bits<VEC>(bm, v) | (v == nfull ? tailmask : 0u);
+          const uint32_t b1 = (v + kST < nvec) ? (vec_bits<VEC>(bm, v + kST) | (v + kST == nfull ? tailmask : 0u)) : 0u;
+          if (b0) u0 = RV<T>::mask(u0, b0);
+          if (b1) u1 = RV<T>::mask(u1, b1);
+          float gm;
+          if (VEC == 8) {
+            const __nv_bfloat162 m2 =
+                __hmax2_nan(RV<__nv_bfloat16>::vmax2_nan(u0), RV<__nv_bfloat16>::vmax2_nan(u1));
+            gm = fmax_nan(__low2float(m2), __high2float(m2));
+            reinterpret_cast<uint16_t*>(s_keys)[k] = (uint16_t)(__float_as_uint(gm) >> 16);
+          } else {
+            gm = fmax_nan(RV<float>::vmax_nan(u0), RV<float>::vmax_nan(u1));
+            reinterpret_cast<uint32_t*>(s_keys)[k] = __float_as_uint(gm);
+          }
+          tmax = fmax_nan(tmax, gm);
+          if (gm > thr) {  // (rare) rebase; also the thread's first finite group
+            if (ssum != 0.f) ssum *= ex2f(__fmul_rn(mref - gm, cf));
+            mref = gm;
+            thr = gm + inv8;
+          }
+          if (mref > -INFINITY) ssum += RV<T>::esum(u0, -mref, cf, c2) + RV<T>::esum(u1, -mref, cf, c2);
+        }
+      }
+      if (t == 0) RTR(it, 3);
+      // ---- this thread's penalised values (exact binary32 penalty, P:146 / P:371): into the max,
+      //      the sum and the slot's penalised list
+      cp_async_wait_all();
+      auto pen = [&](int l, float zp) {
+        if (!(zp < INFINITY)) {  // NaN / +inf
+          bad = 1;
+          return;
+        }
+        if (zp > -INFINITY) {
+          tmax = fmaxf(tmax, zp);
+          if (zp > thr) {
+            if (ssum != 0.f) ssum *= ex2f(__fmul_rn(mref - zp, cf));
+            mref = zp;
+            thr = zp + inv8;
+          }
+          ssum += ex2f(__fmul_rn(__fsub_rn(zp, mref), cf));
+        }
+        const int e = atomicAdd(&sh->npen, 1);
+        if (e < kPenS) s_pen[e] = make_int2(a.voff + c0 + l, __float_as_int(zp));
+      };
+#pragma unroll
+      for (int j = 0; j < kPT; ++j)
+        if (j < npt) pen(pl[j], apply_penalty(RV<T>::at(buf, pl[j]), pme[j], prm, a.pen_mode));
+      if (npt > kPT) {
         int j = 0;
         for (int w = w0; w < w1; ++w) {
           uint32_t bits = bmw[w];
           while (bits) {
             const int l = w * 32 + __ffs(bits) - 1;
             bits &= bits - 1;
-            if (j++ >= kPT) fn(l, apply_penalty(RV<T>::at(buf, l), gme[l], stc.prm, a.pen_mode));
+            if (j++ >= kPT) pen(l, apply_penalty(RV<T>::at(buf, l), gme[l], prm, a.pen_mode));
           }
         }
-      };
-      // ---- the pass: one read of the chunk, 2 vectors (a "group", <= 16 elements) per iteration.
-      //      Per group: its max (NaN-propagating), kept as the group key for the candidate re-read
-      //      and in the lane's top-R maxima for the bound; the exp-sum of P:149's softmax
-      //      denominator relative to the thread's reference m_ref, rebased only when a group max
-      //      exceeds it by 8/c (every term <= 2^8).
-      float tmax = -INFINITY;
-      float mref = -INFINITY, thr = -INFINITY;
-      double ssum = 0.0;  // sum 2^((z - m_ref) c) of this thread
-      {
-        const float inv8 = __fdiv_rn(8.0f, cf);
-        uint64_t c2;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cf), "f"(cf));
-        float acc = 0.f;
-        int nacc = 0;
-        for (int v = gt, k = gt; v < nvec; v += 2 * kRGT, k += kRGT) {
-          const uint4 u0 = ldv(v);
-          const uint4 u1 = (v + kRGT < nvec) ? ldv(v + kRGT) : kNegVec;
-          float gm;
-          if (VEC == 8) {
-            const __nv_bfloat162 m2 =
-                __hmax2_nan(RV<__nv_bfloat16>::vmax2_nan(u0), RV<__nv_bfloat16>::vmax2_nan(u1));
-            gm = fmax_nan(__low2float(m2), __high2float(m2));
-            reinterpret_cast<uint16_t*>(gk)[k] = (uint16_t)(__float_as_uint(gm) >> 16);
-          } else {
-            gm = fmax_nan(RV<float>::vmax_nan(u0), RV<float>::vmax_nan(u1));
-            gk[k] = __float_as_uint(gm);
-          }
-          tmax = fmax_nan(tmax, gm);
-          if (gm > thr) {  // (rare) rebase; also the thread's first finite group
-            if (acc != 0.f || ssum != 0.0) {
-              const float f = ex2f(__fmul_rn(mref - gm, cf));
-              ssum = (ssum + (double)acc) * (double)f;
-              acc = 0.f;
-              nacc = 0;
-            }
-            mref = gm;
-            thr = gm + inv8;
-          }
-          if (mref > -INFINITY) {
-            acc += RV<T>::esum(u0, -mref, cf, c2) + RV<T>::esum(u1, -mref, cf, c2);
-            if (++nacc == 8) {
-              ssum += (double)acc;
-              acc = 0.f;
-              nacc = 0;
-            }
-          }
-        }
-        ssum += (double)acc;
       }
-      if (gt == 0) RTR(it, 3);
-      // ---- this thread's penalised values (exact binary32 penalty, P:146 / P:371)
-      cp_async_wait_all();
-      float zpv[kPT];
-      float pmax = -INFINITY;
-      uint32_t pbad = 0;
+      if (tmax != tmax || tmax == INFINITY) bad = 1;
+      if (__any_sync(kFull, bad) && lane == 0) atomicOr(&sh->bad, 1);
+      s_tmax[t] = tmax;
+      s_mref[t] = mref;
+      s_ssum[t] = ssum;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(empty + b);    // the chunk buffer is free for the producer
+        mbar_arrive(spass + sidx); // (release: this warp's summary entries)
+      }
+    }
+  } else {
+    // ================= finisher groups: rows it = f, f + kNF, ... ==========================
+    const int f = (warp - kSW) / kFW;
+    const int ft = tid - (kSW + f * kFW) * 32, fw = ft >> 5;
+    uint8_t* fsc = smem + L.fscr + f * kFScrBytes;
+    uint64_t* lc = reinterpret_cast<uint64_t*>(fsc);           // [kRCapL] candidates
+    uint8_t* fs = fsc + kRCapL * 8;
+    uint32_t* f_m = reinterpret_cast<uint32_t*>(fs);           // [4] max keys
+    uint32_t* f_t = reinterpret_cast<uint32_t*>(fs + 16);      // [1] the chunk bound
+    double* f_s = reinterpret_cast<double*>(fs + 32);          // [4] sums
+    uint64_t* f_b = reinterpret_cast<uint64_t*>(fs + 64);      // [4] greedy best
+    int* f_cnt = reinterpret_cast<int*>(fs + 96);              // [1] candidate count
+    const int pmw = a.hs.pmw;
+    for (int it = f; it < nrows; it += kNF) {
+      const int sidx = it % kNS, par = (it / kNF) & 1;
+      const int r = (int)q + it * (int)nclus;
+      const int leader = it % C;
+      uint8_t* sl = smem + L.sl + sidx * L.slb;
+      SlotHdr* sh = reinterpret_cast<SlotHdr*>(sl);
+      const float* s_tmax = reinterpret_cast<const float*>(sl + sizeof(SlotHdr));
+      const float* s_mref = s_tmax + kST;
+      const float* s_ssum = s_mref + kST;
+      const uint8_t* s_keys = reinterpret_cast<const uint8_t*>(s_ssum + kST);
+      const int2* s_pen = reinterpret_cast<const int2*>(s_keys + ((a.Lc / 16) * (ESZ == 2 ? 2 : 4) + 15) / 16 * 16);
+      mbar_wait_sleep(spass + sidx, (uint32_t)((it / kNS) & 1));
+      if (ft == 0) RTR(it, 4);
+      const sampling_params prm = sh->prm;
+      const int slot = sh->slot;
+      const RowCfg rc = decode_row(prm, a.V, a.kcand);
+      const int keff = rc.keff;
+      const float cf = __fdiv_rn((float)kLog2e, rc.tau);
+      const bool badc = sh->bad != 0;
+      // ---- chunk max (the stream threads' maxima include the penalised values)
+      float tm[kST / kFT];
+      float mloc = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < kPT; ++j) {
-        zpv[j] = -INFINITY;
-        if (j < npt) {
-          zpv[j] = apply_penalty(RV<T>::at(buf, pl[j]), pme[j], stc.prm, a.pen_mode);
-          if (!(zpv[j] < INFINITY)) pbad = 1;  // NaN / +inf
-          else pmax = fmaxf(pmax, zpv[j]);
+      for (int j = 0; j < kST / kFT; ++j) {
+        tm[j] = s_tmax[ft + j * kFT];
+        mloc = fmaxf(mloc, tm[j]);
+      }
+      const uint32_t mk = __reduce_max_sync(kFull, f2key(mloc));
+      if (lane == 0) f_m[fw] = mk;
+      if (ft == 0) *f_cnt = 0;
+      fbar(f);
+      uint32_t mkey = f_m[0];
+#pragma unroll
+      for (int j = 1; j < kFW; ++j) mkey = max(mkey, f_m[j]);
+      const float mc = key2f(mkey);  // chunk max (-inf if empty)
+      const bool live = !badc && mc > -INFINITY;
+      // ---- S_c relative to the chunk max (fixed order: deterministic)
+      double ss = 0.0;
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < kST / kFT; ++j) {
+          const int tt = ft + j * kFT;
+          const float sv = s_ssum[tt];
+          if (sv != 0.f) ss += (double)sv * (double)ex2f(__fmul_rn(s_mref[tt] - mc, cf));
         }
       }
-      if (npt > kPT)
-        extra([&](int, float zp) {
-          if (!(zp < INFINITY)) pbad = 1;
-          else pmax = fmaxf(pmax, zp);
-        });
-      if (gt == 0) RTR(it, 4);
-      // ---- group: chunk max (incl. penalised) and bad flag; the bound T_c.  Warp w takes
-      //      T_w = the ceil(keff / 8)-th largest of its 32 thread maxima (one ballot per bit); every
-      //      warp has that many elements >= T_w, so the 8 warps hold >= keff elements >= min_w T_w:
-      //      T_c = min_w T_w is a lower bound of the chunk's (hence the row's) keff-th largest z'.
-      const uint32_t bad_t = (tmax != tmax || tmax == INFINITY) ? 1u : pbad;
-      const float mloc = fmaxf(bad_t ? -INFINITY : tmax, pmax);
-      const uint32_t mk = __reduce_max_sync(kFull, f2key(mloc));
-      const uint32_t bw = __reduce_or_sync(kFull, bad_t);
-      {
-        const uint32_t key = (bad_t || !(tmax > -INFINITY)) ? 0u : f2key(tmax);
-        const int kw = (keff + kRWG - 1) / kRWG;
+      ss = warp_sum_d(ss);
+      if (lane == 0) f_s[fw] = ss;
+      // ---- the chunk bound T_c = the keff-th largest stream-thread max (keff distinct elements are
+      //      >= T_c; a lower bound of the row's keff-th largest z'): warp 0, bitwise radix select
+      if (fw == 0) {
+        uint32_t k[kST / 32];
+#pragma unroll
+        for (int j = 0; j < kST / 32; ++j) {
+          const float x = s_tmax[lane + 32 * j];
+          k[j] = (live && x > -INFINITY && x < INFINITY) ? f2key(x) : 0u;
+        }
         uint32_t pre = 0;
 #pragma unroll 1
-        for (int bb = 31; bb >= (VEC == 8 ? 16 : 0); --bb) {
+        for (int bb = 31; bb >= 0; --bb) {
           const uint32_t cand = pre | (1u << bb);
-          if (__popc(__ballot_sync(kFull, key >= cand)) >= kw) pre = cand;
-        }
-        if (lane == 0) {
-          s_wm[gw] = mk;
-          s_wb[gw] = bw;
-          s_wt[gw] = pre;  // 0: fewer than kw non-empty threads in this warp
-        }
-      }
-      if (gt == 0) s_cnt[par] = 0;
-      gbar(g);  // ---- B1
-      uint32_t mkey = s_wm[0], badc = s_wb[0], tkey = 0xFFFFFFFFu;
-      int nzw = 0;
+          uint32_t c = 0;
 #pragma unroll
-      for (int j = 0; j < kRWG; ++j) {
-        mkey = max(mkey, s_wm[j]);
-        badc |= s_wb[j];
-        if (s_wt[j]) {
-          tkey = min(tkey, s_wt[j]);
-          ++nzw;
+          for (int j = 0; j < kST / 32; ++j) c += (k[j] >= cand) ? 1u : 0u;
+          if ((int)__reduce_add_sync(kFull, c) >= keff) pre = cand;
         }
+        if (lane == 0) *f_t = pre;
       }
-      // (warps with fewer than ceil(keff/8) non-empty threads contribute no bound: the others must
-      //  still hold keff elements, else every finite element is a candidate)
-      if (nzw * ((keff + kRWG - 1) / kRWG) < keff) tkey = 0u;
-      const float mc = key2f(mkey);  // chunk max (-inf if empty)
+      fbar(f);
+      const uint32_t tkey = *f_t;
       // ---- the row bound: every CTA's chunk bound to every CTA of the cluster (DSMEM), T = the max
-      //      (each chunk bound is a lower bound of the row's keff-th largest, so their max is too);
-      //      candidates are then only the row's elements >= T, about keff of them in the cluster
-      uint32_t* bs = reinterpret_cast<uint32_t*>(smem + L.bslot) + (g * 2 + par) * kRCMax;
-      if (gt < C) {
-        const uint32_t dst = cl_map(smem_u32(bs + rank), (uint32_t)gt);
+      //      (each is a lower bound of the row's keff-th largest, so the max is too); candidates are
+      //      then only the row's elements >= T, about keff of them in the cluster
+      uint32_t* bs = reinterpret_cast<uint32_t*>(smem + L.bslot) + (f * 2 + par) * kRCMax;
+      if (ft < C) {
+        const uint32_t dst = cl_map(smem_u32(bs + rank), (uint32_t)ft);
         asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(dst), "r"(tkey) : "memory");
-        cl_arrive_remote(cl_map(smem_u32(bound + g), (uint32_t)gt));
+        cl_arrive_remote(cl_map(smem_u32(bound + f), (uint32_t)ft));
       }
-      if (gt == 0) RTR(it, 5);
-      mbar_wait_cl(bound + g, (uint32_t)par);
+      mbar_wait_cl(bound + f, (uint32_t)par);
+      if (ft == 0) RTR(it, 5);
       uint32_t rkey = 0;
-      bool any0 = false;
-      for (int c = 0; c < C; ++c) {
-        rkey = max(rkey, bs[c]);
-        any0 |= bs[c] == 0u;
-      }
-      (void)any0;
+      for (int c = 0; c < C; ++c) rkey = max(rkey, bs[c]);
       const float Tf = rkey ? key2f(rkey) : -INFINITY;
-      // ---- S_c relative to the chunk max; candidates: the groups whose key reaches the bound are
-      //      re-read, every element >= T pushed into the group's list
+      // ---- candidates: the stream threads whose max reaches T, their groups whose key reaches T
+      //      re-read from L2 (the chunk buffer is already refilled), every element >= T listed
       uint64_t tbest = 0ull;
-      const bool live = !badc && mc > -INFINITY;
       auto push = [&](float z, int gid) {
         const uint64_t cmp = make_comp(z, gid);
         if (rc.greedy) {
           tbest = cmp > tbest ? cmp : tbest;
         } else {
-          const int at = atomicAdd(&s_cnt[par], 1);
+          const int at = atomicAdd(f_cnt, 1);
           if (at < kRCapL) lc[at] = cmp;
         }
       };
       if (live) {
-        ssum = (ssum != 0.0) ? ssum * (double)ex2f(__fmul_rn(mref - mc, cf)) : 0.0;
-        for (int v = gt, k = gt; v < nvec; v += 2 * kRGT, k += kRGT) {
-          const float gm = (VEC == 8) ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(gk)[k] << 16)
-                                      : __uint_as_float(gk[k]);
-          if (!(gm >= Tf && gm > -INFINITY)) continue;
-          for (int h = 0; h < 2; ++h) {
-            const int vv = v + h * kRGT;
-            if (vv >= nvec) break;
-            const uint4 u = ldv(vv);
+        const uint8_t* grow = lg + ((int64_t)r * a.ld + c0) * ESZ;
+        const uint32_t* gpm = a.hs.pmask + (int64_t)slot * pmw + c0 / 32;
 #pragma unroll
-            for (int tt = 0; tt < VEC; ++tt) {
-              const float z = RV<T>::elem(u, tt);
-              if (z >= Tf && z > -INFINITY) push(z, gid0 + vv * VEC + tt);
+        for (int j = 0; j < kST / kFT; ++j) {
+          if (!(tm[j] >= Tf)) continue;
+          const int tt = ft + j * kFT;
+          for (int v = tt, k = tt; v < nvec; v += 2 * kST, k += kST) {
+            const float gm = (ESZ == 2) ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(s_keys)[k] << 16)
+                                        : __uint_as_float(reinterpret_cast<const uint32_t*>(s_keys)[k]);
+            if (!(gm >= Tf && gm > -INFINITY)) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int vv = v + h * kST;
+              if (vv >= nvec) continue;
+              uint4 u = *reinterpret_cast<const uint4*>(grow + (int64_t)vv * 16);
+              const int e0 = vv * VEC;
+              uint32_t pb = (gpm[e0 >> 5] >> (e0 & 31)) & ((1u << VEC) - 1u);
+              if (vv == nfull) pb |= tailmask;
+              if (pb) u = RV<T>::mask(u, pb);
+#pragma unroll
+              for (int q2 = 0; q2 < VEC; ++q2) {
+                const float z = RV<T>::elem(u, q2);
+                if (z >= Tf && z > -INFINITY) push(z, a.voff + c0 + e0 + q2);
+              }
             }
           }
         }
-        auto pen_use = [&](int l, float zp) {
-          if (zp > -INFINITY) {
-            ssum += (double)ex2f(__fmul_rn(__fsub_rn(zp, mc), cf));
-            if (zp >= Tf) push(zp, gid0 + l);
+        const int npen = sh->npen;
+        if (npen <= kPenS) {
+          for (int e = ft; e < npen; e += kFT) {
+            const int2 pe = s_pen[e];
+            const float zp = __int_as_float(pe.y);
+            if (zp >= Tf && zp > -INFINITY) push(zp, pe.x);
           }
-        };
-#pragma unroll
-        for (int j = 0; j < kPT; ++j)
-          if (j < npt) pen_use(pl[j], zpv[j]);
-        if (npt > kPT) extra(pen_use);
-      } else {
-        ssum = 0.0;
-      }
-      if (gt == 0) RTR(it, 6);
-      ssum = warp_sum_d(ssum);
-      tbest = warp_max_u64(tbest);
-      if (lane == 0) {
-        s_ws[gw] = ssum;
-        s_wbest[gw] = tbest;
-      }
-      // the leader's list for this row must be free before this chunk's list is written into it
-      if (gt == 0 && it >= C) mbar_wait_cl(slotfree + leader, (uint32_t)((it / C - 1) & 1));
-      gbar(g);  // ---- B2
-      int cnt = s_cnt[par];
-      uint64_t front = rkey ? make_comp(Tf, 0x7FFFFFFF) : 0ull;
-      if (live && !rc.greedy && cnt > a.cap) {
-        // massive ties: the chunk's exact top-keff by composite, then the list again (rare)
-        const uint64_t kc = group_kth_comp<T>(buf, bm, nvec, nval, gme, stc.prm, a.pen_mode, gid0, Tf, keff,
-                                              s_hist, s_ctl, g);
-        if (gt == 0) s_cnt[par] = 0;
-        gbar(g);
-        for (int v = gt; v < nvec; v += kRGT) {
-          const uint4 u = ldv(v);
-          const uint32_t pb = vec_bits<VEC>(bm, v);
-#pragma unroll
-          for (int t = 0; t < VEC; ++t) {
-            float z = RV<T>::elem(u, t);
-            const int l = v * VEC + t;
-            if ((pb >> t) & 1u) z = apply_penalty(RV<T>::at(buf, l), gme[l], stc.prm, a.pen_mode);
-            if (z >= Tf && z > -INFINITY && z < INFINITY && make_comp(z, gid0 + l) >= kc) push(z, gid0 + l);
+        } else {  // long histories: every penalised id of the chunk again, from global memory
+          const uint32_t* gme = a.hs.pmeta + (int64_t)slot * a.hs.vls + c0;
+          for (int w = ft; w < nw; w += kFT) {
+            uint32_t bits = gpm[w];
+            while (bits) {
+              const int l = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const float x = (ESZ == 2) ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(grow)[l] << 16)
+                                         : reinterpret_cast<const float*>(grow)[l];
+              const float zp = apply_penalty(x, gme[l], prm, a.pen_mode);
+              if (zp >= Tf && zp > -INFINITY && zp < INFINITY) push(zp, a.voff + c0 + l);
+            }
           }
         }
-        gbar(g);
-        cnt = s_cnt[par];
-        front = kc > front ? kc : front;
       }
-      // the buffer is consumed
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + g);
-      // ---- this chunk's candidates into the leader's list (DSMEM stores), then the record
-      const int nout = rc.greedy ? 0 : min(cnt, a.cap);
+      tbest = warp_max_u64(tbest);
+      if (lane == 0) f_b[fw] = tbest;
+      // the leader's list for this row must be free before this chunk's list is written into it
+      if (ft == 0 && it >= C) mbar_wait_cl(slotfree + leader, (uint32_t)((it / C - 1) & 1));
+      fbar(f);
+      // the summary slot is consumed
+      if (ft == 0) {
+        sh->npen = 0;
+        sh->bad = 0;
+        mbar_arrive(sfree + sidx);
+      }
+      const int cnt = *f_cnt;
+      const bool over = !rc.greedy && cnt > a.cap;  // (massive ties: exact.cuh finishes the row)
+      const int nout = (rc.greedy || over) ? 0 : cnt;
       const uint32_t rec_remote = cl_map(smem_u32(smem + L.rec), (uint32_t)leader) + rank * (uint32_t)(a.cap * 8);
-      for (int i = gt; i < nout; i += kRGT) cl_st64(rec_remote + (uint32_t)i * 8u, lc[i]);
-      gbar(g);  // ---- B3
-      if (gt == 0) {
+      for (int i = ft; i < nout; i += kFT) cl_st64(rec_remote + (uint32_t)i * 8u, lc[i]);
+      fbar(f);
+      if (ft == 0) {
         RecC h;
         h.m = mc;
-        h.flags = badc ? 1u : 0u;
-        double s = 0.0;
+        h.flags = (badc ? 1u : 0u) | (over ? 2u : 0u);
+        double s2 = 0.0;
         uint64_t bb = 0ull;
 #pragma unroll
-        for (int j = 0; j < kRWG; ++j) {
-          s += s_ws[j];
-          bb = s_wbest[j] > bb ? s_wbest[j] : bb;
+        for (int j = 0; j < kFW; ++j) {
+          s2 += f_s[j];
+          bb = f_b[j] > bb ? f_b[j] : bb;
         }
-        h.s = s;
-        h.front = front;
+        h.s = s2;
+        h.front = rkey ? make_comp(Tf, 0x7FFFFFFF) : 0ull;
         h.best = bb;
         h.n = nout;
         h.pad[0] = h.pad[1] = h.pad[2] = 0;
@@ -921,7 +904,11 @@ __global__ void __launch_bounds__(kRThreads, 1) row_kernel(const __grid_constant
         const uint4* hv = reinterpret_cast<const uint4*>(&h);
 #pragma unroll
         for (int j = 0; j < (int)(sizeof(RecC) / 16); ++j) cl_st128(hr + 16 * j, hv[j]);
-        if (rank == (uint32_t)leader) *reinterpret_cast<RowStage*>(smem + L.rinfo) = stc;  // for the decider
+        if (rank == (uint32_t)leader) {  // the row's params / slot for the decider
+          RowStage* rs = reinterpret_cast<RowStage*>(smem + L.rinfo);
+          rs->prm = prm;
+          rs->slot = slot;
+        }
         cl_fence();  // the group's list entries (ordered before this thread by the barrier) and the header
         cl_arrive_remote(cl_map(smem_u32(recfull), (uint32_t)leader));
         RTR(it, 7);

@@ -570,6 +570,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
   tmark(h, 1, st);
   h->last_launches = 1;
   // exact multi-pass kernel only if some row can be unresolved by the one-pass candidates
+  // (a chunk list can also overflow on massive ties, rare: then the row is pending too)
   bool need = params_dev != nullptr;
   if (!need) {
     const int n = slots_dev ? h->cfg.max_batch : B;

@@ -48,8 +48,8 @@ tt = t.copy(); tt[:, :, 8:11] = 0
 nz = tt[tt > 0]
 t0 = nz.min()
 rel = np.where(tt > 0, tt - t0, -1)
-names = {0: "p:slot-free", 1: "p:issued", 2: "g:landed", 3: "g:A1", 4: "g:pen-in", 5: "g:bound", 6: "g:A2",
-         7: "g:sent", 12: "d:recs-in", 13: "d:topk", 14: "d:decided"}
+names = {0: "p:buf-free", 1: "p:issued", 2: "s:landed", 3: "s:passed", 4: "f:start", 5: "f:bound-xchg",
+         7: "f:sent", 12: "d:recs-in", 13: "d:topk", 14: "d:decided"}
 print("end of step (last stamp): %.2f us" % ((nz.max() - t0) / 1e3))
 for ev, nm in names.items():
     v = rel[:, :, ev]
@@ -60,10 +60,10 @@ v = t[:, :, 8][t[:, :, 2] > 0]
 print("candidates per chunk: mean %.1f max %d" % (v.mean(), v.max()))
 print("tkey/rkey row0 CTA0..3:", [(hex(int(t[c, 0, 9])), hex(int(t[c, 0, 10]))) for c in range(4)])
 # per-row phase durations (CTA 0's rows)
-print("CTA 0 rows (us): it: landed A1 pen bound A2 sent | dec: in topk decided")
+print("CTA 0 rows (us): it: landed passed | fin-start bound-xchg sent | dec: in topk decided")
 for it in range(min(12, 64)):
     r = rel[0, it]
     if r[2] < 0:
         break
     f = lambda e: ("%7.2f" % (r[e] / 1e3)) if r[e] >= 0 else "      -"
-    print(it, " ".join(f(e) for e in (2, 3, 4, 5, 6, 7)), "|", " ".join(f(e) for e in (12, 13, 14)))
+    print(it, " ".join(f(e) for e in (2, 3)), "|", " ".join(f(e) for e in (4, 5, 7)), "|", " ".join(f(e) for e in (12, 13, 14)))
