@@ -408,7 +408,6 @@ def main():
     algo = algorithmic_bytes(wl, uniq0, esize) if not vocab_mode else (B * (hi - lo) * esize + 8 * sum(uniq0))
     # the dominant kernel is phase A (stream_kernel): it moves the logits, the kernel-timed roofline
     # divides the step's algorithmic bytes by its own mean duration; the whole step is reported too
-    knames = ["row_kernel", "exact_kernel"]
     kern_s = (kt[0] / 1000.0) if kt else ms_step / 1000.0
     achieved = algo / kern_s / 1e9
     step_gbs = algo / (ms_step / 1000.0) / 1e9
@@ -427,10 +426,11 @@ def main():
         "gbs": step_gbs,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": load_traffic(a.config),
-                     "peak_source": peak_src, "kernel": "row_kernel",
+                     "peak_source": peak_src, "kernel": "stream_kernel",
                      "algorithmic_bytes_per_launch": algo,
                      "kernel_time_s": kern_s,
-                     "kernel_times_us": ({knames[i]: kt[i] * 1e3 for i in range(len(kt))} if kt else None),
+                     "kernel_times_us": ({"stream_kernel": kt[0] * 1e3, "select_rows_kernel": kt[1] * 1e3}
+                                         if kt else None),
                      "step_gbs": step_gbs, "step_frac": step_gbs / peak},
         "clocks": clocks,
         "e2e": {"value": rows_total / (ms_e2e / 1000.0), "unit": UNIT,

@@ -26,8 +26,16 @@ constexpr double kLn2 = 0.69314718055994530941723212145818;
 struct SlotMeta {
   int32_t n_prompt;
   int32_t n_out;
-  int32_t rsv;
+  int32_t n_uniq;
   int32_t flags;  // bit0: history overflow happened (append dropped)
+};
+
+// Unique-token penalty entry: id ascending; meta = (count_in_output << 1) | in_prompt.
+// This is the device form of the paper's incremental penalty buffer f: only the
+// entries of tokens that occurred are stored (sparse), updated in place on append.
+struct __align__(8) UniqEntry {
+  int32_t id;
+  uint32_t meta;
 };
 
 // ---- partial-reduction record (piece / rank) ----------------------------------------

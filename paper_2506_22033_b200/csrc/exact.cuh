@@ -317,22 +317,18 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   }
   __syncthreads();
   {
-    // penalised ids: the set bits of the slot's presence bitmap, counts from its per-id table
-    const uint32_t* pm = a.hs.pmask + (int64_t)slot * a.hs.pmw;
-    const uint32_t* pme = a.hs.pmeta + (int64_t)slot * a.hs.vls;
-    for (int w = tid; w < a.hs.pmw; w += kExThreads) {
-      uint32_t bits = pm[w];
-      while (bits) {
-        const int j = w * 32 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        if (j >= a.vloc) break;
-        float x;
-        if (sizeof(T) == 2)
-          x = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(lrow)[j] << 16);
-        else
-          x = reinterpret_cast<const float*>(lrow)[j];
-        zs[j] = apply_penalty(x, pme[j], prm, a.pen_mode);
-      }
+    const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
+    const int nu = a.hs.meta[slot].n_uniq;
+    for (int i = tid; i < nu; i += kExThreads) {
+      const UniqEntry e = ut[i];
+      const int j = e.id - a.voff;
+      if (j < 0 || j >= a.vloc) continue;
+      float x;
+      if (sizeof(T) == 2)
+        x = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(lrow)[j] << 16);
+      else
+        x = reinterpret_cast<const float*>(lrow)[j];
+      zs[j] = apply_penalty(x, e.meta, prm, a.pen_mode);
     }
   }
   __threadfence_block();
@@ -601,7 +597,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     s.ints[5] = tok;
   }
   __syncthreads();
-  if (a.append && tid == 0) hist_append(a.hs, slot, s.ints[5]);
+  if (a.append && tid < 32) warp_append_token(a.hs, slot, s.ints[5], tid);
 }
 
 // Debug: q[b, v] = final filtered distribution (w_v / W over K3; one-hot for greedy rows).
@@ -615,6 +611,8 @@ __global__ void debug_q_kernel(const void* logits, int64_t ld, int V, int voff, 
   const int slot = slots ? slots[r] : r;
   const sampling_params prm = params_dev ? params_dev[r] : params_tab[slot];
   const RowCfg rc = decode_row(prm, V, 1);
+  const UniqEntry* ut = hs.uniq + (int64_t)slot * hs.L;
+  const int nu = hs.meta[slot].n_uniq;
   const uint8_t* lrow = reinterpret_cast<const uint8_t*>(logits) + (int64_t)r * ld * sizeof(T);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < vloc; j += gridDim.x * blockDim.x) {
     float out = 0.0f;
@@ -625,7 +623,13 @@ __global__ void debug_q_kernel(const void* logits, int64_t ld, int V, int voff, 
         float x = sizeof(T) == 2
                       ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(lrow)[j] << 16)
                       : reinterpret_cast<const float*>(lrow)[j];
-        if (pmask_test(hs, slot, j)) x = apply_penalty(x, hs.pmeta[(int64_t)slot * hs.vls + j], prm, pen_mode);
+        // penalty lookup (binary search; debug only)
+        int lo = 0, hi = nu;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (ut[mid].id < voff + j) lo = mid + 1; else hi = mid;
+        }
+        if (lo < nu && ut[lo].id == voff + j) x = apply_penalty(x, ut[lo].meta, prm, pen_mode);
         if (x > -INFINITY && make_comp(x, voff + j) >= ri.cutoff)
           out = (float)(exp(((double)x - (double)ri.M) / (double)rc.tau) / ri.W);
       }

@@ -28,49 +28,36 @@ struct RowOut {
   RowInfo* info;     // per-row hand-off / debug
 };
 
-// Per-slot history state: the device form of the paper's incremental penalty buffers f,
-// kept sparse in what is read and O(1) in what is updated:
-//   meta[slot]             lengths + overflow flag;
-//   tokens[slot][..]       prompt then output tokens (export / checkpoint);
-//   pmask[slot][pmw]       presence bitmap, natural order: local id le -> word le/32, bit le%32, set
-//                          for every id of prompt u output inside this handle's vocabulary slice;
-//   pmeta[slot][vls]       per local id: (count in the output << 1) | in_prompt (0 unless the bit is
-//                          set; only read at set bits).
-// Appending a sampled token ("only the B elements ... incrementally updated") is one
-// increment, one bit and one token store.
+// Per-slot history state.  pmask[slot] is the slot's penalty presence bitmap (the set of ids in
+// prompt u output — the support of the paper's penalty buffers f, kept as bits and
+// updated incrementally on append) in phase A's step-lane order: local element le, v = le / vec,
+// step k = v / 128, d = v % 128  ->  word k * 32 + (d % 32), bit (d / 32) * vec + le % vec.
+// Phase A bulk-copies the words of each tile next to the logits and masks those elements.
 struct HistState {
   SlotMeta* meta;
+  UniqEntry* uniq;
   int32_t* tokens;
-  int L;            // max_history (capacity)
-  int Ls;           // per-slot stride of tokens
-  uint32_t* pmask;  // [max_batch][pmw]
-  int pmw;          // bitmap words per slot (multiple of 4: 16-byte rows)
-  uint32_t* pmeta;  // [max_batch][vls]
-  int vls;          // per-slot stride of pmeta
+  int L;
+  uint32_t* pmask;  // [max_batch][spr * 32]
+  int spr;          // steps per row of the local slice
+  int vec;          // elements per 16-byte vector (8 bf16 / 4 f32)
   int voff, vloc;
 };
 
-__host__ __device__ inline int pmask_words(int vloc) { return ((vloc + 31) / 32 + 3) / 4 * 4; }
-
-__device__ __forceinline__ bool pmask_test(const HistState& hs, int slot, int le) {
-  return (hs.pmask[(int64_t)slot * hs.pmw + (le >> 5)] >> (le & 31)) & 1u;
+__host__ __device__ inline void pmask_pos(int le, int vec, int* word, uint32_t* bit) {
+  const int v = le / vec, k = v / 128, d = v % 128;
+  *word = k * 32 + (d & 31);
+  *bit = 1u << ((d >> 5) * vec + le % vec);
 }
 
-// Append one sampled token to a slot (one thread; one writer per slot per call).
-__device__ __forceinline__ void hist_append(const HistState& hs, int slot, int32_t tok) {
-  SlotMeta* sm = hs.meta + slot;
-  const int np = sm->n_prompt, no = sm->n_out;
-  if (np + no + 1 > hs.L) {
-    sm->flags |= 1;
-    return;
-  }
-  hs.tokens[(int64_t)slot * hs.Ls + np + no] = tok;
-  sm->n_out = no + 1;
+// a token entered the slot's history: its presence bit (idempotent)
+__device__ __forceinline__ void pmask_set(const HistState& hs, int slot, int32_t tok) {
   const int le = tok - hs.voff;
-  if (le >= 0 && le < hs.vloc) {
-    hs.pmeta[(int64_t)slot * hs.vls + le] += 2u;
-    hs.pmask[(int64_t)slot * hs.pmw + (le >> 5)] |= 1u << (le & 31);
-  }
+  if (le < 0 || le >= hs.vloc) return;
+  int w;
+  uint32_t b;
+  pmask_pos(le, hs.vec, &w, &b);
+  atomicOr(hs.pmask + (int64_t)slot * hs.spr * 32 + w, b);
 }
 
 struct MergeSmem {
@@ -83,6 +70,49 @@ struct MergeSmem {
   BlockScratch bs;
 };
 constexpr int kMergeSmemBytes = kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8 + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12;
+
+// Incremental penalty-table update for one appended token ("only the B elements of f
+// that correspond to the newly generated token IDs are incrementally updated").  One warp.
+__device__ __forceinline__ void warp_append_token(const HistState& hs, int slot, int32_t tok, int lane) {
+  SlotMeta* sm = hs.meta + slot;
+  const int np = sm->n_prompt, no = sm->n_out, nu = sm->n_uniq;
+  if (np + no + 1 > hs.L) {
+    if (lane == 0) sm->flags |= 1;
+    return;
+  }
+  UniqEntry* u = hs.uniq + (int64_t)slot * hs.L;
+  int less = 0;
+  for (int i = lane; i < nu; i += 32) less += (u[i].id < tok) ? 1 : 0;
+  less = warp_sum_i(less);
+  const bool found = (less < nu) && (u[less].id == tok);
+  __syncwarp();
+  if (found) {
+    if (lane == 0) u[less].meta += 2u;
+  } else {
+    for (int top = nu; top > less; top -= 32) {
+      const int i = top - 1 - lane;
+      UniqEntry e;
+      const bool act = i >= less;
+      if (act) e = u[i];
+      __syncwarp();
+      if (act) u[i + 1] = e;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      UniqEntry e;
+      e.id = tok;
+      e.meta = 2u;
+      u[less] = e;
+    }
+    if (lane == 0) pmask_set(hs, slot, tok);
+  }
+  if (lane == 0) {
+    hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
+    sm->n_out = no + 1;
+    if (!found) sm->n_uniq = nu + 1;
+  }
+  __syncwarp();
+}
 
 // Final decision for one row by one warp (R6-R11): top-k -> top-p (renormalised over
 // the top-k survivors) -> min-p over the candidates top[0..n) (sorted by pi), exact down to the
@@ -314,8 +344,22 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
     ms.pool[i] = rec_entries(recs + (int64_t)rr * pitch)[i - rr * keff];
   }
   if (tid < nrec) ms.hdr[tid] = *reinterpret_cast<const RecHdr*>(recs + (int64_t)tid * pitch);
+  SlotMeta smeta = {0, 0, 0, 0};
+  if (do_app) smeta = hs.meta[slot];
   cbar();
   MTR(2);
+  // ---- the slot's unique-token table into registers (used by the append after the decision)
+  constexpr int kUR = 4;
+  const int nu = smeta.n_uniq;
+  const bool reg_app = do_app && nu <= kBT * kUR;
+  UniqEntry ue[kUR];
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    ue[q].id = 0x7FFFFFFF;
+    ue[q].meta = 0;
+    if (reg_app && i < nu) ue[q] = hs.uniq[(int64_t)slot * hs.L + i];
+  }
   // ---- rank merge: element q of list r has rank q + sum_{o != r} |{entries of o > c}|
   int U = 0;
   for (int o = 0; o < nrec; ++o) U += min((int)ms.hdr[o].n, keff);
@@ -387,10 +431,49 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
   }
   MTR(4);
   cbar();
-  // ---- history append (P:371 incremental update): one warp
+  // ---- history append (P:371 incremental update), whole block; the table is in registers
   const int32_t tok = ms.bs.i[1];
   if (!do_app || tok < 0) return;
-  if (tid == 0) hist_append(hs, slot, tok);
+  if (!reg_app) {  // very long unique tables: one warp, chunked shift through global memory
+    if (tid < 32) warp_append_token(hs, slot, tok, lane);
+    return;
+  }
+  const int np = smeta.n_prompt, no = smeta.n_out;
+  if (np + no + 1 > hs.L) {
+    if (tid == 0) hs.meta[slot].flags |= 1;
+    return;
+  }
+  int cl = 0;
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    if (i < nu) cl += (ue[q].id < tok ? 1 : 0) + (ue[q].id == tok ? (1 << 20) : 0);
+  }
+  const int cs = block_sum_i(cl, ms.bs);
+  const int less = cs & ((1 << 20) - 1);
+  const bool found = (cs >> 20) != 0;
+  UniqEntry* u = hs.uniq + (int64_t)slot * hs.L;
+#pragma unroll
+  for (int q = 0; q < kUR; ++q) {
+    const int i = tid + q * kBT;
+    if (i < nu) {
+      if (found && i == less) u[i].meta = ue[q].meta + 2u;
+      if (!found && i >= less) u[i + 1] = ue[q];
+    }
+  }
+  if (tid == 0) {
+    if (!found) {
+      UniqEntry e;
+      e.id = tok;
+      e.meta = 2u;
+      u[less] = e;
+    }
+    hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
+    SlotMeta m2 = smeta;
+    m2.n_out = no + 1;
+    if (!found) m2.n_uniq = nu + 1;
+    hs.meta[slot] = m2;
+  }
   MTR(5);
 #undef MTR
 }

@@ -2,8 +2,8 @@
 //
 // Owns per-handle device state (params table, per-slot history + incremental unique-token
 // penalty table, workspace), validates every call on the host before any launch, and enqueues
-// the sm_100a kernels on the caller's stream: the row-resident cluster kernel (rowres.cuh,
-// programmatic dependent launch so consecutive steps overlap their launch latency), the exact
+// the sm_100a kernels on the caller's stream: phase A (stream.cuh), phase B (select.cuh, launched
+// with programmatic dependent launch so its prologue overlaps phase A's tail), the exact
 // multi-pass kernel (exact.cuh) only when some row can stay unresolved, and the sharded merge
 // (merge.cuh).
 #include <algorithm>
@@ -18,7 +18,8 @@
 #include "common.cuh"
 #include "exact.cuh"
 #include "merge.cuh"
-#include "rowres.cuh"
+#include "select.cuh"
+#include "stream.cuh"
 
 using namespace smp;
 
@@ -27,25 +28,29 @@ struct sampler {
   int sm_count = 0;
   int Vp = 0;    // vocab_local rounded up to the vector width
   int vec = 8;   // elements per 16 bytes
-  int esz = 2;
-  int Ls = 0;    // per-slot stride of the history tables (max_history rounded up to even)
+  int64_t Vq = 0;  // padded row length in vectors (piece.cuh)
+  int max_ctas = 0;
   int64_t rec_stride = 0;
-  // row kernel geometry per cluster size C = 1 << i (rowres.cuh); lc = 0: infeasible
-  int rk_lc[5] = {}, rk_cap[5] = {}, rk_smem[5] = {}, rk_maxclus[5] = {};
   // device state
   sampling_params* d_params = nullptr;
   SlotMeta* d_meta = nullptr;
+  UniqEntry* d_uniq = nullptr;
   int32_t* d_hist = nullptr;
-  uint32_t* d_pmeta = nullptr;  // [max_batch][vls] per-id (count << 1 | in_prompt) (HistState::pmeta)
-  int vls = 0;
+  uint8_t* d_records = nullptr;
+  int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
   float* d_scratch = nullptr;
-  uint32_t* d_pmask = nullptr;  // [max_batch][pmw] penalty presence bitmaps (HistState::pmask)
+  uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
+  PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
+  RowHand* d_hand = nullptr;    // [max_batch] phase A -> B hand-off
+  PenEnt* d_pent = nullptr;     // [max_batch][max_history] penalised entries (hand-off)
+  uint16_t* d_gkeys = nullptr;  // [max_batch][Vq/4] group keys (phase A -> phase B)
+  uint64_t* d_trace = nullptr;
+  int dbg = 0;                  // SAMPLER_DBG development switches (stream.cuh)  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
   // host mirror
   std::vector<sampling_params> h_params;
   std::string err;
   int32_t last_launches = 0;
-  uint64_t* d_trace = nullptr;  // SMP_TRACE builds only
   // per-kernel timing (sampler_set_timing)
   bool timing = false;
   cudaEvent_t tev[4] = {};
@@ -66,16 +71,19 @@ static void tmark(sampler* h, int k, cudaStream_t st) {
 static HistState hist_state(const sampler* h) {
   HistState s;
   s.meta = h->d_meta;
+  s.uniq = h->d_uniq;
   s.tokens = h->d_hist;
   s.L = h->cfg.max_history;
-  s.Ls = h->Ls;
   s.pmask = h->d_pmask;
-  s.pmw = pmask_words(h->cfg.vocab_local);
-  s.pmeta = h->d_pmeta;
-  s.vls = h->vls;
+  s.spr = (int)(h->Vq / kStepVec);
+  s.vec = h->vec;
   s.voff = h->cfg.vocab_offset;
   s.vloc = h->cfg.vocab_local;
   return s;
+}
+
+static int64_t trace_a_len(const sampler* h) {  // phase-A trace entries (64 per CTA, worst-case grid)
+  return 64 * ((int64_t)h->cfg.max_batch * (h->Vq / kStepVec) / kTileSteps + 1);
 }
 
 static thread_local std::string g_create_err;
@@ -122,10 +130,10 @@ static bool row_may_pend(const sampling_params& p, int V, int kcand) {
 extern "C" {
 
 const char* sampler_version(void) {
-  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a); row-resident cluster kernel (rows in "
-         "DSMEM via 1-D bulk copies, penalty presence bitmap + prefix-indexed history, packed bf16 exp-sum, "
-         "thread-max bound, DSMEM candidate lists, decider warp: exact top-k, float64 top-p/min-p, "
-         "Philox4x32-10 draw); exact multi-pass fallback";
+  return "paper_2506_22033_b200 sampler: sm_100a (compute_100a); phase A: persistent warp-specialised "
+         "stream (1-D bulk-copy ring, penalty presence bitmap, packed bf16 exp-sum, group/step keys); "
+         "phase B: per-row step-key bound, group re-read, exact top-k, candidate-parallel decision, "
+         "Philox4x32-10; exact multi-pass fallback";
 }
 
 const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
@@ -179,21 +187,23 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   h->cfg = c;
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, c.device);
   h->vec = (c.logits_dtype == SAMPLER_BF16) ? 8 : 4;
-  h->esz = (c.logits_dtype == SAMPLER_BF16) ? 2 : 4;
   h->Vp = (c.vocab_local + h->vec - 1) / h->vec * h->vec;
-  h->Ls = (c.max_history + 1) / 2 * 2;
+  h->max_ctas = h->sm_count;
+  h->Vq = vq_of(c.vocab_local, h->vec);
   h->rec_stride = (rec_stride_bytes(c.max_top_k) + 127) / 128 * 128;
-  const int64_t B = c.max_batch, Ls = h->Ls;
-  const int pmw = pmask_words(c.vocab_local);
-  h->vls = (c.vocab_local + 3) / 4 * 4;
+  const int64_t B = c.max_batch, L = c.max_history;
+  // records: candidate records (sharded exchange) and one warp record per (warp, row) sub-piece
+  const int64_t nrec = B + 1;
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
-            al((void**)&h->d_meta, sizeof(SlotMeta) * B) &&
-            al((void**)&h->d_hist, sizeof(int32_t) * B * Ls) &&
-            al((void**)&h->d_pmeta, sizeof(uint32_t) * B * h->vls) &&
-            al((void**)&h->d_info, sizeof(RowInfo) * B) &&
+            al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
+            al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_records, h->rec_stride * nrec) &&
+            al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
             al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
-            al((void**)&h->d_pmask, sizeof(uint32_t) * B * pmw);
+            al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
+            al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&
+            al((void**)&h->d_hand, sizeof(RowHand) * B) &&  al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
+            al((void**)&h->d_parts, sizeof(PartRec) * B * kCW * ((h->Vq / kStepVec + kTileSteps - 1) / kTileSteps + 1));
   if (!ok) {
     cudaGetLastError();
     sampler_destroy(h);
@@ -217,11 +227,19 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   if (cudaMemcpy(h->d_params, h->h_params.data(), sizeof(sampling_params) * B, cudaMemcpyHostToDevice) !=
           cudaSuccess ||
       cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
-      cudaMemset(h->d_pmeta, 0, sizeof(uint32_t) * B * h->vls) != cudaSuccess ||
-      cudaMemset(h->d_pmask, 0, sizeof(uint32_t) * B * pmw) != cudaSuccess ||
+      cudaMemset(h->d_pmask, 0, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) != cudaSuccess ||
+      cudaMemset(h->d_tickets, 0, sizeof(int32_t) * B) != cudaSuccess ||
       cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
+      cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kStreamSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem) !=
+          cudaSuccess ||
       cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kExactSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(select_rows_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSelectSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(select_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelectSmem) !=
+          cudaSuccess ||
       cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExactSmem) !=
           cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
@@ -229,62 +247,19 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
     sampler_destroy(h);
     return fail(nullptr, SAMPLER_ECUDA, "device init failed: %s", m);
   }
-  // row kernel geometry for every cluster size: chunk length, list capacity, shared memory, and
-  // how many clusters of that size can be resident at once
-  int smem_max = 0;
-  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
-  const void* rk = (c.logits_dtype == SAMPLER_BF16) ? (const void*)row_kernel<__nv_bfloat16>
-                                                     : (const void*)row_kernel<float>;
-  cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  int need_smem = 0;
-  for (int i = 0; i < 5; ++i) {
-    const int C = 1 << i;
-    const int Lc = (int)(((int64_t)c.vocab_local + C - 1) / C + kLcAlign - 1) / kLcAlign * kLcAlign;
-    const int cap = SAMPLER_KCAND_MAX;  // sorted chunk lists hold at most max_top_k entries
-    const int sm = rlayout(C, Lc, h->esz, cap).total;
-    if (sm > smem_max) continue;
-    h->rk_lc[i] = Lc;
-    h->rk_cap[i] = cap;
-    h->rk_smem[i] = sm;
-    need_smem = std::max(need_smem, sm);
-  }
-  if (need_smem == 0) {
-    sampler_destroy(h);
-    return fail(nullptr, SAMPLER_EUNSUPPORTED, "vocab_local too large for the row-resident kernel");
-  }
-  if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, need_smem) != cudaSuccess) {
-    const char* m = cudaGetErrorString(cudaGetLastError());
-    sampler_destroy(h);
-    return fail(nullptr, SAMPLER_ECUDA, "row kernel attributes: %s", m);
-  }
-  for (int i = 0; i < 5; ++i) {
-    if (!h->rk_lc[i]) continue;
-    const int C = 1 << i;
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)(C * std::max(1, h->sm_count / C)));
-    lc.blockDim = dim3(kRThreads);
-    lc.dynamicSmemBytes = h->rk_smem[i];
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, rk, &lc) != cudaSuccess || n < 1) {
-      cudaGetLastError();
-      h->rk_lc[i] = 0;
-      continue;
-    }
-    h->rk_maxclus[i] = n;
-  }
-#ifdef SMP_TRACE
-  if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * 16 * kTrRows * (size_t)(2 * h->sm_count)) != cudaSuccess)
-    h->d_trace = nullptr;
-  else
-    cudaMemset(h->d_trace, 0, sizeof(uint64_t) * 16 * kTrRows * (size_t)(2 * h->sm_count));
+#ifdef SMP_CARVEOUT
+  // one L1/shared split for every kernel of the step: no reconfiguration at the kernel boundaries
+  cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(select_rows_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(select_rows_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
+  cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
 #endif
+  if (getenv("SAMPLER_DBG")) h->dbg = atoi(getenv("SAMPLER_DBG"));
+  if (getenv("SAMPLER_TRACE")) {
+    if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;
+  }
   *out = h;
   return SAMPLER_OK;
 }
@@ -294,12 +269,18 @@ int sampler_destroy(sampler* h) {
   cudaSetDevice(h->cfg.device);
   cudaFree(h->d_params);
   cudaFree(h->d_meta);
+  cudaFree(h->d_uniq);
   cudaFree(h->d_hist);
-  cudaFree(h->d_pmeta);
+  cudaFree(h->d_records);
+  cudaFree(h->d_tickets);
   cudaFree(h->d_info);
   cudaFree(h->d_scratch);
-  cudaFree(h->d_pmask);
   cudaFree(h->d_trace);
+  cudaFree(h->d_gkeys);
+  cudaFree(h->d_pmask);
+  cudaFree(h->d_parts);
+  cudaFree(h->d_hand);
+  cudaFree(h->d_pent);
   for (auto& e : h->tev)
     if (e) cudaEventDestroy(e);
   delete h;
@@ -315,7 +296,6 @@ int sampler_set_params(sampler* h, int32_t n, const int32_t* slots, const sampli
     if (e) return fail(h, SAMPLER_EINVAL, "params[%d]: %s", i, e);
   }
   CK(h, cudaSetDevice(h->cfg.device));
-  CK(h, cudaDeviceSynchronize());  // no in-flight sample may still read the table (sampler.h)
   for (int32_t i = 0; i < n; ++i) {
     h->h_params[slots[i]] = params[i];
     CK(h, cudaMemcpy(h->d_params + slots[i], &params[i], sizeof(sampling_params), cudaMemcpyHostToDevice));
@@ -325,30 +305,42 @@ int sampler_set_params(sampler* h, int32_t n, const int32_t* slots, const sampli
 
 static int upload_slot(sampler* h, int slot, const std::vector<int32_t>& prompt, const std::vector<int32_t>& output,
                        int32_t flags) {
-  const int64_t Ls = h->Ls;
-  const int vloc = h->cfg.vocab_local, voff = h->cfg.vocab_offset;
+  const int L = h->cfg.max_history;
+  std::map<int32_t, uint32_t> m;
+  for (int32_t t : prompt) m[t] |= 1u;
+  for (int32_t t : output) m[t] += 2u;
+  std::vector<UniqEntry> u;
+  u.reserve(m.size());
+  for (auto& kv : m) {
+    UniqEntry e;
+    e.id = kv.first;
+    e.meta = kv.second;
+    u.push_back(e);
+  }
   std::vector<int32_t> toks(prompt);
   toks.insert(toks.end(), output.begin(), output.end());
   SlotMeta sm;
   sm.n_prompt = (int32_t)prompt.size();
   sm.n_out = (int32_t)output.size();
-  sm.rsv = 0;
+  sm.n_uniq = (int32_t)u.size();
   sm.flags = flags;
-  // presence bitmap (natural order) and per-id meta of the slot's vocabulary slice (HistState)
-  const int pmw = pmask_words(vloc);
-  std::vector<uint32_t> pm(pmw, 0u), me(h->vls, 0u);
-  for (int32_t t : prompt)
-    if (t >= voff && t - voff < vloc) me[t - voff] |= 1u;
-  for (int32_t t : output)
-    if (t >= voff && t - voff < vloc) me[t - voff] += 2u;
-  for (int le = 0; le < vloc; ++le)
-    if (me[le]) pm[le >> 5] |= 1u << (le & 31);
   CK(h, cudaSetDevice(h->cfg.device));
-  CK(h, cudaDeviceSynchronize());  // no in-flight sample may still append to this slot (sampler.h)
+  if (!u.empty())
+    CK(h, cudaMemcpy(h->d_uniq + (int64_t)slot * L, u.data(), sizeof(UniqEntry) * u.size(), cudaMemcpyHostToDevice));
   if (!toks.empty())
-    CK(h, cudaMemcpy(h->d_hist + (int64_t)slot * Ls, toks.data(), sizeof(int32_t) * toks.size(), cudaMemcpyHostToDevice));
-  CK(h, cudaMemcpy(h->d_pmask + (int64_t)slot * pmw, pm.data(), sizeof(uint32_t) * pmw, cudaMemcpyHostToDevice));
-  CK(h, cudaMemcpy(h->d_pmeta + (int64_t)slot * h->vls, me.data(), sizeof(uint32_t) * h->vls, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->d_hist + (int64_t)slot * L, toks.data(), sizeof(int32_t) * toks.size(), cudaMemcpyHostToDevice));
+  // penalty presence bitmap of the slot (HistState::pmask)
+  const int64_t nw = (h->Vq / kStepVec) * 32;
+  std::vector<uint32_t> pm(nw, 0u);
+  for (const UniqEntry& e : u) {
+    const int le = e.id - h->cfg.vocab_offset;
+    if (le < 0 || le >= h->cfg.vocab_local) continue;
+    int w;
+    uint32_t b;
+    pmask_pos(le, h->vec, &w, &b);
+    pm[w] |= b;
+  }
+  CK(h, cudaMemcpy(h->d_pmask + (int64_t)slot * nw, pm.data(), sizeof(uint32_t) * nw, cudaMemcpyHostToDevice));
   CK(h, cudaMemcpy(h->d_meta + slot, &sm, sizeof(SlotMeta), cudaMemcpyHostToDevice));
   return SAMPLER_OK;
 }
@@ -369,28 +361,21 @@ int sampler_set_history(sampler* h, int32_t slot, const int32_t* prompt, int32_t
   return upload_slot(h, slot, p, o, 0);
 }
 
-// the slot's lengths, tokens and (id, count, in_prompt) table of its vocabulary slice, ids ascending
-struct SlotView {
-  SlotMeta sm;
-  std::vector<int32_t> toks, ids, counts, inp;
-};
-static int read_slot(sampler* h, int slot, SlotView* v, bool table) {
+static int read_slot(sampler* h, int slot, SlotMeta* sm, std::vector<int32_t>* toks, std::vector<UniqEntry>* u) {
+  const int L = h->cfg.max_history;
   CK(h, cudaSetDevice(h->cfg.device));
-  CK(h, cudaMemcpy(&v->sm, h->d_meta + slot, sizeof(SlotMeta), cudaMemcpyDeviceToHost));
-  v->toks.resize(v->sm.n_prompt + v->sm.n_out);
-  if (!v->toks.empty())
-    CK(h, cudaMemcpy(v->toks.data(), h->d_hist + (int64_t)slot * h->Ls, sizeof(int32_t) * v->toks.size(),
-                     cudaMemcpyDeviceToHost));
-  if (table) {
-    std::vector<uint32_t> me(h->vls);
-    CK(h, cudaMemcpy(me.data(), h->d_pmeta + (int64_t)slot * h->vls, sizeof(uint32_t) * h->vls,
-                     cudaMemcpyDeviceToHost));
-    for (int le = 0; le < h->cfg.vocab_local; ++le)
-      if (me[le]) {
-        v->ids.push_back(le + h->cfg.vocab_offset);
-        v->counts.push_back((int32_t)(me[le] >> 1));
-        v->inp.push_back((int32_t)(me[le] & 1u));
-      }
+  CK(h, cudaMemcpy(sm, h->d_meta + slot, sizeof(SlotMeta), cudaMemcpyDeviceToHost));
+  if (toks) {
+    toks->resize(sm->n_prompt + sm->n_out);
+    if (!toks->empty())
+      CK(h, cudaMemcpy(toks->data(), h->d_hist + (int64_t)slot * L, sizeof(int32_t) * toks->size(),
+                       cudaMemcpyDeviceToHost));
+  }
+  if (u) {
+    u->resize(sm->n_uniq);
+    if (!u->empty())
+      CK(h, cudaMemcpy(u->data(), h->d_uniq + (int64_t)slot * L, sizeof(UniqEntry) * u->size(),
+                       cudaMemcpyDeviceToHost));
   }
   return SAMPLER_OK;
 }
@@ -415,12 +400,13 @@ int sampler_append_tokens(sampler* h, int32_t n, const int32_t* slots, const int
       return fail(h, SAMPLER_ERANGE, "slot %d would exceed max_history", kv.first);
   }
   for (int32_t i = 0; i < n; ++i) {
-    SlotView v;
-    int rc = read_slot(h, slots[i], &v, false);
+    SlotMeta sm;
+    std::vector<int32_t> toks;
+    int rc = read_slot(h, slots[i], &sm, &toks, nullptr);
     if (rc) return rc;
-    std::vector<int32_t> p(v.toks.begin(), v.toks.begin() + v.sm.n_prompt), o(v.toks.begin() + v.sm.n_prompt, v.toks.end());
+    std::vector<int32_t> p(toks.begin(), toks.begin() + sm.n_prompt), o(toks.begin() + sm.n_prompt, toks.end());
     o.push_back(tokens[i]);
-    rc = upload_slot(h, slots[i], p, o, v.sm.flags);
+    rc = upload_slot(h, slots[i], p, o, sm.flags);
     if (rc) return rc;
   }
   return SAMPLER_OK;
@@ -433,20 +419,23 @@ int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_
   if (slot < 0 || slot >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot out of range");
   CK(h, cudaSetDevice(h->cfg.device));
   CK(h, cudaDeviceSynchronize());
-  SlotView v;
-  int rc = read_slot(h, slot, &v, true);
+  SlotMeta sm;
+  std::vector<int32_t> toks;
+  std::vector<UniqEntry> u;
+  int rc = read_slot(h, slot, &sm, &toks, &u);
   if (rc) return rc;
-  if (n_prompt) *n_prompt = v.sm.n_prompt;
-  if (n_output) *n_output = v.sm.n_out;
-  if (prompt_out) std::copy(v.toks.begin(), v.toks.begin() + v.sm.n_prompt, prompt_out);
-  if (output_out) std::copy(v.toks.begin() + v.sm.n_prompt, v.toks.end(), output_out);
-  if (n_unique) *n_unique = (int32_t)v.ids.size();
-  for (size_t i = 0; i < v.ids.size(); ++i) {
-    if (uniq_ids) uniq_ids[i] = v.ids[i];
-    if (uniq_counts) uniq_counts[i] = v.counts[i];
-    if (uniq_in_prompt) uniq_in_prompt[i] = v.inp[i];
+  if (n_prompt) *n_prompt = sm.n_prompt;
+  if (n_output) *n_output = sm.n_out;
+  if (prompt_out) std::copy(toks.begin(), toks.begin() + sm.n_prompt, prompt_out);
+  if (output_out) std::copy(toks.begin() + sm.n_prompt, toks.end(), output_out);
+  if (n_unique) *n_unique = sm.n_uniq;
+  for (size_t i = 0; i < u.size(); ++i) {
+    if (uniq_ids) uniq_ids[i] = u[i].id;
+    if (uniq_counts) uniq_counts[i] = (int32_t)(u[i].meta >> 1);
+    if (uniq_in_prompt) uniq_in_prompt[i] = (int32_t)(u[i].meta & 1u);
   }
-  if (v.sm.flags & 1) h->err = "history overflow occurred on this slot";
+  // overflow flag is reported through the sign of n_output? keep a separate path:
+  if (sm.flags & 1) h->err = "history overflow occurred on this slot";
   return SAMPLER_OK;
 }
 
@@ -460,76 +449,134 @@ static int check_logits(sampler* h, const void* logits, int64_t ld, int32_t B) {
   return SAMPLER_OK;
 }
 
-// Row-kernel geometry for a call of B rows: the cluster size C with the smallest estimated time
-// ceil(B / clusters) x (chunk + per-row overhead), clusters = min(B, resident clusters of size C).
-struct RPlan {
-  int C, Lc, cap, smem, nclus;
+struct LaunchPlan {
+  int spr;         // steps (2 KB of one row) per row
+  int span;        // steps per CTA
+  int rpr;         // CTA record blocks per row
+  int64_t nsteps;  // B * spr
+  int grid;
 };
-static RPlan rplan(const sampler* h, int32_t B) {
-  RPlan best{0, 0, 0, 0, 0};
-  int64_t best_cost = INT64_MAX;
-  constexpr int64_t kRowOverhead = 4096;  // elements-equivalent of the per-row fixed work
-  for (int i = 0; i < 5; ++i) {
-    if (!h->rk_lc[i]) continue;
-    const int nclus = std::min<int>(B, h->rk_maxclus[i]);
-    const int64_t cost = ((int64_t)(B + nclus - 1) / nclus) * ((int64_t)h->rk_lc[i] + kRowOverhead);
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = RPlan{1 << i, h->rk_lc[i], h->rk_cap[i], h->rk_smem[i], nclus};
-    }
-  }
-  return best;
+
+// Phase A geometry (stream.cuh): equal contiguous spans of the padded step space, one persistent
+// CTA per SM; a span is >= one tile (16 steps) and covers at most kMaxSeg - 2 whole rows.
+static LaunchPlan plan(const sampler* h, int32_t B) {
+  LaunchPlan p;
+  p.spr = (int)(h->Vq / kStepVec);
+  p.nsteps = (int64_t)B * p.spr;
+  const int64_t nctas = (int64_t)h->sm_count * kStreamCtasPerSm;
+  int64_t span = (p.nsteps + nctas - 1) / nctas;
+  span = std::max<int64_t>(span, kTileSteps);
+  span = std::min<int64_t>(span, (int64_t)(kMaxSeg - 2) * p.spr);
+  p.span = (int)span;
+  p.grid = (int)((p.nsteps + span - 1) / span);
+  p.rpr = (p.spr + p.span - 1) / p.span + 1;
+  return p;
 }
 
-static int launch_rows(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
-                       const sampling_params* params_dev, const uint64_t* seeds, uint64_t step, int append, int mode,
-                       const RowOut& ro, uint8_t* out_records, cudaStream_t st) {
-  const RPlan p = rplan(h, B);
-  if (!p.C) return fail(h, SAMPLER_EUNSUPPORTED, "no feasible row-kernel geometry");
-  RArgs a{};
+static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
+                              const sampling_params* params_dev, const LaunchPlan& lp) {
+  StreamArgs a{};
   a.logits = logits;
   a.ld = ld;
   a.B = B;
   a.V = h->cfg.vocab_size;
   a.voff = h->cfg.vocab_offset;
   a.vloc = h->cfg.vocab_local;
-  a.C = p.C;
-  a.Lc = p.Lc;
-  a.cap = p.cap;
+  a.Vq = h->Vq;
+  a.spr = lp.spr;
+  a.span = lp.span;
+  a.rpr = lp.rpr;
+  a.nsteps = lp.nsteps;
   a.slots = slots;
   a.params_dev = params_dev;
   a.params_tab = h->d_params;
-  a.seeds = seeds;
-  a.step = step;
-  a.kcand = h->cfg.max_top_k;
   a.pen_mode = h->cfg.penalty_mode;
-  a.mode = mode;
-  a.append = append;
   a.hs = hist_state(h);
-  a.ro = ro;
-  a.out_records = out_records;
-  a.out_stride = h->rec_stride;
+  a.parts = h->d_parts;
+  a.hand = h->d_hand;
+  a.pent = h->d_pent;
+  a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
+  a.dbg = h->dbg;
+  return a;
+}
+
+static int launch_stream(sampler* h, const StreamArgs& a, int grid, cudaStream_t st) {
+  if (h->d_trace)
+    CK(h, cudaMemsetAsync(h->d_trace, 0, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)h->cfg.max_batch), st));
+  // programmatic dependent launch: the grid may be scheduled while the previous kernel of the
+  // stream finishes (the kernel waits for it before touching memory, stream.cuh)
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(p.nclus * p.C));
-  cfg.blockDim = dim3(kRThreads);
-  cfg.dynamicSmemBytes = p.smem;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.dynamicSmemBytes = kStreamSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  // programmatic dependent launch: this grid may be scheduled while the previous kernel of the
-  // stream finishes (the kernel waits for it before touching memory, rowres.cuh)
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   if (h->cfg.logits_dtype == SAMPLER_BF16)
-    CK(h, cudaLaunchKernelEx(&cfg, row_kernel<__nv_bfloat16>, a));
+    CK(h, cudaLaunchKernelEx(&cfg, stream_kernel<__nv_bfloat16>, a));
   else
-    CK(h, cudaLaunchKernelEx(&cfg, row_kernel<float>, a));
+    CK(h, cudaLaunchKernelEx(&cfg, stream_kernel<float>, a));
+  return SAMPLER_OK;
+}
+
+static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
+                              const sampling_params* params_dev, const uint64_t* seeds, uint64_t step, int append,
+                              const RowOut& ro, const LaunchPlan& lp) {
+  SelectArgs s{};
+  s.logits = logits;
+  s.ld = ld;
+  s.B = B;
+  s.V = h->cfg.vocab_size;
+  s.voff = h->cfg.vocab_offset;
+  s.vloc = h->cfg.vocab_local;
+  s.Vq = h->Vq;
+  s.spr = lp.spr;
+  s.span = lp.span;
+  s.rpr = lp.rpr;
+  s.slots = slots;
+  s.params_dev = params_dev;
+  s.params_tab = h->d_params;
+  s.seeds = seeds;
+  s.step = step;
+  s.kcand = h->cfg.max_top_k;
+  s.pen_mode = h->cfg.penalty_mode;
+  s.mode = 0;
+  s.append = append;
+  s.pending_ok = 1;
+  s.hs = hist_state(h);
+  s.parts = h->d_parts;
+  s.hand = h->d_hand;
+  s.dbg = h->dbg;
+  s.pent = h->d_pent;
+  s.gkeys = h->d_gkeys;
+  s.ro = ro;
+  s.out_records = nullptr;
+  s.out_stride = h->rec_stride;
+  s.trace = h->d_trace ? h->d_trace + trace_a_len(h) : nullptr;
+  return s;
+}
+
+// phase B with programmatic dependent launch: its CTAs may start (prologue) while phase A's last
+// CTAs run; griddepcontrol.wait in the kernel orders every read of phase A's outputs
+static int launch_select(sampler* h, const SelectArgs& s, int B, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)B);
+  cfg.blockDim = dim3(kBT);
+  cfg.dynamicSmemBytes = kSelectSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    CK(h, cudaLaunchKernelEx(&cfg, select_rows_kernel<__nv_bfloat16>, s));
+  else
+    CK(h, cudaLaunchKernelEx(&cfg, select_rows_kernel<float>, s));
   return SAMPLER_OK;
 }
 
@@ -550,7 +597,7 @@ static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_par
   m.append = append;
   m.hs = hist_state(h);
   m.ro = ro;
-  m.trace = nullptr;
+  m.trace = h->d_trace ? h->d_trace + trace_a_len(h) : nullptr;
   return m;
 }
 
@@ -563,14 +610,18 @@ static int launch_merge(sampler* h, const MergeArgs& m, int B, cudaStream_t st) 
 static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots_dev,
                      const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step, int32_t append,
                      int32_t* tokens, float* logprobs, float* flogprobs, int32_t* status, cudaStream_t st) {
+  const LaunchPlan lp = plan(h, B);
+  const StreamArgs a = stream_args(h, logits, ld, B, slots_dev, params_dev, lp);
   RowOut ro{tokens, logprobs, flogprobs, status, h->d_info};
   tmark(h, 0, st);
-  int rc = launch_rows(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append, 0, ro, nullptr, st);
+  int rc = launch_stream(h, a, lp.grid, st);
   if (rc) return rc;
   tmark(h, 1, st);
-  h->last_launches = 1;
+  rc = launch_select(h, select_args(h, logits, ld, B, slots_dev, params_dev, seeds_dev, step, append, ro, lp), B, st);
+  if (rc) return rc;
+  tmark(h, 2, st);
+  h->last_launches = 2;
   // exact multi-pass kernel only if some row can be unresolved by the one-pass candidates
-  // (a chunk list can also overflow on massive ties, rare: then the row is pending too)
   bool need = params_dev != nullptr;
   if (!need) {
     const int n = slots_dev ? h->cfg.max_batch : B;
@@ -592,7 +643,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     e.step = step;
     e.append = append;
     e.pen_mode = h->cfg.penalty_mode;
-    e.hs = hist_state(h);
+    e.hs = a.hs;
     e.scratch = h->d_scratch;
     e.ro = ro;
     if (h->cfg.logits_dtype == SAMPLER_BF16)
@@ -600,8 +651,8 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     else
       exact_kernel<float><<<B, kExThreads, kExactSmem, st>>>(e);
     CK(h, cudaGetLastError());
-    tmark(h, 2, st);
-    h->last_launches = 2;
+    tmark(h, 3, st);
+    h->last_launches = 3;
   }
   return SAMPLER_OK;
 }
@@ -651,9 +702,10 @@ int sampler_debug_distribution(sampler* h, const void* logits, int64_t ld, int32
 
 int sampler_debug_trace(const sampler* h, uint64_t* host_out, int32_t n) {
   if (!h || !host_out || n < 0) return SAMPLER_EINVAL;
-  if (!h->d_trace) return SAMPLER_EUNSUPPORTED;  // (product builds carry no trace buffers)
-  const size_t m = std::min<size_t>((size_t)n, (size_t)16 * kTrRows * 2 * h->sm_count);
-  if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess) return SAMPLER_ECUDA;
+  if (!h->d_trace) return SAMPLER_EUNSUPPORTED;
+  const int64_t m = std::min<int64_t>(n, trace_a_len(h) + 32 * (int64_t)h->cfg.max_batch);
+  if (cudaMemcpy(host_out, h->d_trace, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SAMPLER_ECUDA;
   return SAMPLER_OK;
 }
 
@@ -671,12 +723,19 @@ int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32
   if (((uintptr_t)records_dev) % 16) return fail(h, SAMPLER_EINVAL, "records_dev must be 16-byte aligned");
   CK(h, cudaSetDevice(h->cfg.device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
+  const LaunchPlan lp = plan(h, B);
   tmark(h, 0, st);
-  rc = launch_rows(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, 1, ro, (uint8_t*)records_dev, st);
+  rc = launch_stream(h, stream_args(h, logits_slice, ld, B, slots_dev, params_dev, lp), lp.grid, st);
   if (rc) return rc;
   tmark(h, 1, st);
-  h->last_launches = 1;
+  RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
+  SelectArgs s = select_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, ro, lp);
+  s.mode = 1;
+  s.out_records = (uint8_t*)records_dev;
+  rc = launch_select(h, s, B, st);
+  if (rc) return rc;
+  tmark(h, 2, st);
+  h->last_launches = 2;
   return SAMPLER_OK;
 }
 

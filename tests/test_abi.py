@@ -26,10 +26,9 @@ def test_library_exports_every_header_symbol():
     assert sorted(EXPORTED) == syms
 
 
-def test_sass_is_sm100a_with_bulk_copies_and_clusters():
-    """The built library contains sm_100a SASS; the row kernel stages rows with 1-D bulk copies
-    (TMA engine: UBLKCP), synchronises its thread-block cluster (UCGABAR), takes the chunk max with
-    packed bf16 max (HMNMX2) and the exponentials on the MUFU (MUFU.EX2)."""
+def test_sass_is_sm100a_with_streaming_loads():
+    """The built library contains sm_100a SASS; the streaming pass uses 16-byte read-only
+    no-L1-allocate loads (LDG.E.NA.128.CONSTANT) and the hardware exp2 (MUFU.EX2)."""
     import shutil
     import subprocess
     from paper_2506_22033_b200.sampler import LIB_PATH
@@ -39,10 +38,8 @@ def test_sass_is_sm100a_with_bulk_copies_and_clusters():
     out = subprocess.run([cuobjdump, "-lelf", LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run([cuobjdump, "-sass", LIB_PATH], capture_output=True, text=True).stdout
-    fn = sass[sass.index("row_kernelI13__nv_bfloat16"):]
-    fn = fn[:fn.find("Function :")] if "Function :" in fn else fn
-    for mnem in ("UBLKCP", "UCGABAR_ARV", "UCGABAR_WAIT", "HMNMX2", "MUFU.EX2", "SYNCS.PHASECHK"):
-        assert mnem in fn, mnem
+    assert "LDG.E.NA.128.CONSTANT" in sass
+    assert "MUFU.EX2" in sass
 
 
 def test_param_struct_layout():
