@@ -1,33 +1,48 @@
-// exact.cuh — exact multi-pass path for rows whose kept set is not bounded by the one-pass
-// candidates (top-p / min-p-only rows with large nuclei, unfiltered rows, top_k > K_cand).
+// exact.cuh — the exact path for rows whose kept set is not bounded by the one-pass candidates
+// (top-p / min-p-only rows with large nuclei, unfiltered rows, top_k > K_cand).
 //
-// One CTA (1024 threads) per pending row; M and S come from the streaming pass.
-//   pass 0  materialise z' (penalties applied, binary32) into a per-row fp32 scratch row
-//   pass 1  2048-bucket histogram of counts and fixed-point masses, bucket = floor(-x*64) with
-//           x = (z'-M)*log2(e)/tau (1/64-octave buckets of the weight; contiguous in pi order)
-//   select  top-k rank / top-p mass cutoffs: bucket by prefix scan, then inside the bucket by
-//           gathering + sorting its composites (or, if it is huge, an 8-digit radix select)
-//           min-p: exact value threshold by bisection on binary32 keys (w >= min_p, float64)
-//   pass 2  draw: per-thread id-contiguous kept mass, block scan, inverse CDF in id order
-// All reductions are integer (fixed point) or fixed-order float64: bit-reproducible.
+// One thread-block cluster of G CTAs per row (G = 1 for large batches); CTA c takes the chunk
+// [c*Lc, (c+1)*Lc) of the row's vocabulary slice and reads it from global memory (L2) in every pass;
+// M (row max of z') and S come from phase B (select.cuh).  Every mass is float64-accurate (DESIGN.md
+// R16: a token may differ from the oracle's only when a boundary lies within 1e-9 of it):
+//   pass 1  per element y = (M - z') log2(e)/tau >= 0 (float64), weight w = 2^-y
+//           (= exp((z' - M)/tau)), bucket b = floor(64 y) (1/64 octave of weight, so buckets
+//           are contiguous in pi order); per bucket its count and its mass RELATIVE TO THE BUCKET'S
+//           TOP WEIGHT 2^(-b/64), in 2^-40 fixed point: sum_i round(2^(b/64 - y_i) 2^40), each term in
+//           (2^39.98, 2^40], so every element keeps <= 2^-41 relative error and the sums are
+//           order-independent integers (deterministic).  The leader CTA sums the C histograms.
+//   cutoffs top-k (count) and top-p (mass over K1, P:149's Filter; R7/R8) locate their
+//           bucket from the fixed-order prefix of the bucket masses, then gather that bucket's
+//           elements (all CTAs -> the leader, DSMEM), sort them by (z' desc, id asc) and walk them
+//           with exact float64 weights; a bucket too large to gather is split once more into 1024
+//           sub-buckets (1/65536 octave); min-p is an exact value threshold (bisection, float64).
+//   draw    K3 = { composite >= C3 }; W = sum over K3 of w in id order: per-CTA totals, the
+//           cluster prefix in CTA (= id) order, u*W located, the CTA holding it walks its chunk in
+//           id order (rounds of 512 vectors, block scans): first cumulative > u*W.
 #pragma once
+#include <cfloat>
+
 #include "common.cuh"
+#include "elem.cuh"
 #include "merge.cuh"
 #include "philox.cuh"
-#include "elem.cuh"
+#include "piece.cuh"
 
 namespace smp {
 
-constexpr int kExThreads = 1024;
-constexpr int kNB = 2048;
-constexpr int kCapG = 4096;
-constexpr double kFix = 17592186044416.0;  // 2^44 fixed-point scale for masses (w <= 1)
-constexpr int kExactSmem = kNB * 4 + kNB * 8 + kCapG * 8 + 1024 + 256 * 4 + 256 * 8;
+constexpr int kExThreads = 512;
+constexpr int kExW = kExThreads / 32;
+constexpr int kNB0 = 2048;   // level-0 buckets: 1/64 octave, 32 octaves
+constexpr int kNB1 = 1024;   // level-1 sub-buckets of one level-0 bucket: 1/65536 octave
+constexpr int kSide = 2048;  // penalised (local id, z') of the chunk kept in smem
+constexpr int kGat = 4096;   // gathered composites of the boundary bucket (leader)
+constexpr double kFix40 = 1099511627776.0;  // 2^40
 
 struct ExactArgs {
   const void* logits;
   int64_t ld;
-  int B, V, voff, vloc, Vp;
+  int B, V, voff, vloc;
+  int G, Lc;  // cluster size, chunk length (multiple of 128)
   const int32_t* slots;
   const sampling_params* params_dev;
   const sampling_params* params_tab;
@@ -36,31 +51,53 @@ struct ExactArgs {
   int append;
   int pen_mode;
   HistState hs;
-  float* scratch;  // [B x Vp]
   RowOut ro;
 };
 
-struct ExSmem {
-  uint32_t* cnt;   // [kNB]
-  uint64_t* mass;  // [kNB]
-  uint64_t* list;  // [kCapG]
-  uint64_t* u64s;  // [32]
-  double* dbl;     // [32]
-  int* ints;       // [32]
-  uint32_t* rcnt;  // [256] radix digit counts
-  uint64_t* rmass; // [256] radix digit masses
-};
+// shared memory (bytes)
+constexpr int kExOffSideId = 0;
+constexpr int kExOffSideZ = kExOffSideId + kSide * 4;
+constexpr int kExOffCnt = kExOffSideZ + kSide * 4;     // u32 [kNB0] local counts
+constexpr int kExOffMass = kExOffCnt + kNB0 * 4;       // u64 [kNB0] local fixed masses
+constexpr int kExOffGat = kExOffMass + kNB0 * 8;       // u64 [kGat] (leader)
+constexpr int kExOffScr = kExOffGat + kGat * 8;        // scratch: doubles / ints / u64
+constexpr int kExactSmem = kExOffScr + 2048;
 
-__device__ __forceinline__ int bucket_of(float z, float M, float c_hi, float c_lo) {
-  const float t = z - M;
-  const float x = fmaf(t, c_hi, t * c_lo);
-  const float y = -x * 64.0f;
-  return y >= (float)(kNB - 1) ? kNB - 1 : (y > 0.0f ? (int)y : 0);
+// ---- cluster helpers (a launch without clusters is a cluster of one CTA) ----------------
+__device__ __forceinline__ uint32_t ex_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
+__device__ __forceinline__ void ex_csync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ex_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t ex_ld32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ex_ld64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ex_st64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ex_atom_add(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void ex_bar() { __syncthreads(); }
 
-__device__ __forceinline__ uint64_t fixmass(float w) { return (uint64_t)__float2ull_rn(w * (float)kFix); }
-// 64-bit shared-memory add as two native 32-bit atomics with the carry (sm_100 has no native
-// 64-bit shared add: it would be a CAS spin loop); integer, so still order-independent
+// 64-bit shared-memory add as two native 32-bit atomics with the carry (integer: order-independent)
 __device__ __forceinline__ void smem_add_u64(uint64_t* p, uint64_t v) {
   uint32_t* p32 = reinterpret_cast<uint32_t*>(p);
   const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
@@ -69,535 +106,636 @@ __device__ __forceinline__ void smem_add_u64(uint64_t* p, uint64_t v) {
   if (up) atomicAdd(p32 + 1, up);
 }
 
-// block-wide reductions (512 threads)
-__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, ExSmem& s) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// 2^-s for s in [0, ln2/64) via its series in s*ln2 (relative error < 3e-15)
+__device__ __forceinline__ double exp2_neg_small(double d) {  // d = s * ln2 in [0, 0.0109)
+  return 1.0 - d * (1.0 - d * (0.5 - d * (1.0 / 6.0 - d * (1.0 / 24.0 - d * (1.0 / 120.0)))));
+}
+
+// block-wide fixed-order sums / scans (512 threads)
+__device__ __forceinline__ double ex_sum_d(double v, double* scr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum_d(v);
+  ex_bar();
+  if (lane == 0) scr[w] = v;
+  ex_bar();
+  double t = 0.0;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  __syncthreads();
-  if (lane == 0) s.u64s[wid] = v;
-  __syncthreads();
-  uint64_t t = 0;
-  for (int i = 0; i < kExThreads / 32; ++i) t += s.u64s[i];
-  __syncthreads();
+  for (int i = 0; i < kExW; ++i) t += scr[i];
+  ex_bar();
   return t;
 }
-__device__ __forceinline__ int block_sum_int(int v, ExSmem& s) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_sum_i(v);
-  __syncthreads();
-  if (lane == 0) s.ints[wid] = v;
-  __syncthreads();
-  int t = 0;
-  for (int i = 0; i < kExThreads / 32; ++i) t += s.ints[i];
-  __syncthreads();
-  return t;
-}
-// exclusive scan of doubles in thread order (fixed order => deterministic); returns total
-__device__ __forceinline__ double block_excl_scan_d(double v, double* total, ExSmem& s) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+__device__ __forceinline__ double ex_excl_scan_d(double v, double* tot, double* scr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double incl = warp_incl_scan_d(v, lane);
-  __syncthreads();
-  if (lane == 31) s.dbl[wid] = incl;
-  __syncthreads();
-  double before = 0.0, tot = 0.0;
-  for (int i = 0; i < kExThreads / 32; ++i) {
-    if (i < wid) before += s.dbl[i];
-    tot += s.dbl[i];
+  ex_bar();
+  if (lane == 31) scr[w] = incl;
+  ex_bar();
+  double before = 0.0, t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kExW; ++i) {
+    if (i < w) before += scr[i];
+    t += scr[i];
   }
-  __syncthreads();
-  *total = tot;
+  ex_bar();
+  *tot = t;
   return before + incl - v;
 }
-
-// First bucket b (ascending) where the running sum of `val` (count or mass, restricted to
-// buckets < limit) reaches target; returns b (or -1) and the sum of buckets before b.
-template <bool MASS>
-__device__ int find_bucket(ExSmem& s, uint64_t target, int limit, uint64_t* before) {
-  // each thread owns 4 consecutive buckets
-  const int tid = threadIdx.x;
-  uint64_t v[4];
-  uint64_t loc = 0;
+__device__ __forceinline__ uint64_t ex_sum_u64(uint64_t v, uint64_t* scr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int b = tid * 4 + j;
-    v[j] = (b < limit) ? (MASS ? s.mass[b] : (uint64_t)s.cnt[b]) : 0;
-    loc += v[j];
-  }
-  // exclusive scan over threads (u64)
-  const int lane = tid & 31, wid = tid >> 5;
-  uint64_t incl = loc;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  ex_bar();
+  if (lane == 0) scr[w] = v;
+  ex_bar();
+  uint64_t t = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
-  }
-  __syncthreads();
-  if (lane == 31) s.u64s[wid] = incl;
-  __syncthreads();
-  uint64_t wbefore = 0;
-  for (int i = 0; i < wid; ++i) wbefore += s.u64s[i];
-  uint64_t run = wbefore + incl - loc;
-  __syncthreads();
-  if (tid == 0) s.ints[0] = -1;
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (run < target && run + v[j] >= target) {
-      s.ints[0] = tid * 4 + j;
-      s.u64s[0] = run;
-    }
-    run += v[j];
-  }
-  __syncthreads();
-  const int b = s.ints[0];
-  *before = (b >= 0) ? s.u64s[0] : 0;
-  __syncthreads();
-  return b;
+  for (int i = 0; i < kExW; ++i) t += scr[i];
+  ex_bar();
+  return t;
 }
 
-// Descending bitonic sort of s.list[0..n) (n <= kCapG).
-__device__ void block_sort_desc(ExSmem& s, int n) {
+// Descending bitonic sort of buf[0..n) (n <= kGat) by the whole block.
+__device__ void ex_sort_desc(uint64_t* buf, int n) {
   int N = 1;
   while (N < n) N <<= 1;
-  for (int i = n + threadIdx.x; i < N; i += kExThreads) s.list[i] = 0;
-  __syncthreads();
+  for (int i = n + threadIdx.x; i < N; i += kExThreads) buf[i] = 0;
+  ex_bar();
   for (int k = 2; k <= N; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = threadIdx.x; i < N; i += kExThreads) {
         const int ixj = i ^ j;
         if (ixj > i) {
-          const uint64_t a = s.list[i], b = s.list[ixj];
+          const uint64_t x = buf[i], y = buf[ixj];
           const bool desc = (i & k) == 0;
-          if (desc ? (a < b) : (a > b)) {
-            s.list[i] = b;
-            s.list[ixj] = a;
+          if (desc ? (x < y) : (x > y)) {
+            buf[i] = y;
+            buf[ixj] = x;
           }
         }
       }
-      __syncthreads();
+      ex_bar();
     }
 }
 
-struct BucketCtx {
-  const float* zs;  // scratch row
-  int Vp, voff;
-  float M, c_hi, c_lo;
-};
-
-// Gather the composites of bucket b (count nb <= kCapG) into s.list, sorted descending.
-__device__ void gather_bucket(ExSmem& s, const BucketCtx& bc, int b, int nb) {
-  if (threadIdx.x == 0) s.ints[1] = 0;
-  __syncthreads();
-  const float4* z4 = reinterpret_cast<const float4*>(bc.zs);
-#pragma unroll 4
-  for (int i = threadIdx.x; i < bc.Vp / 4; i += kExThreads) {
-    const float4 q = z4[i];
-    const float zz[4] = {q.x, q.y, q.z, q.w};
+// the row as seen by one CTA: z' of local id l (penalties applied), element iteration by vectors
+template <typename T>
+struct ExRow {
+  static constexpr int VEC = Dec<T>::N;
+  const uint8_t* rowp;      // local slice of the row
+  const uint32_t* pm;       // the slot's presence bitmap (phase A step-lane layout)
+  const int* side_id;       // sorted local ids of the chunk's penalised elements
+  const float* side_z;
+  int nside;                // entries in smem (if ovf: the chunk's penalised ids come from the table)
+  bool ovf;
+  const UniqEntry* ut;      // the slot's unique-token table (sorted by id)
+  int nu;
+  int voff, vloc, c0, c1;   // chunk [c0, c1) of local ids
+  sampling_params prm;
+  int pen_mode;
+  // penalised bits of vector v (VEC elements at local id v*VEC)
+  __device__ __forceinline__ uint32_t pbits(int v) const {
+    const int k = v >> 7, d = v & 127;
+    return (pm[k * 32 + (d & 31)] >> ((d >> 5) * VEC)) & ((1u << VEC) - 1u);
+  }
+  __device__ __forceinline__ float pen_value(int l) const {
+    if (!ovf) {
+      int lo = 0, hi = nside;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (side_id[mid] < l) lo = mid + 1;
+        else hi = mid;
+      }
+      return side_z[lo];
+    }
+    const int id = voff + l;
+    int lo = 0, hi = nu;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (ut[mid].id < id) lo = mid + 1;
+      else hi = mid;
+    }
+    return apply_penalty(Dec<T>::load1(rowp, l), ut[lo].meta, prm, pen_mode);
+  }
+  // the VEC values z' of vector v (-inf past the slice end)
+  __device__ __forceinline__ void vec(int v, float (&z)[Dec<T>::N]) const {
+    const uint4 u = *reinterpret_cast<const uint4*>(rowp + (int64_t)v * 16);
+    const uint32_t pb = pbits(v);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (zz[j] > -INFINITY && bucket_of(zz[j], bc.M, bc.c_hi, bc.c_lo) == b) {
-        const int pos = atomicAdd(&s.ints[1], 1);
-        if (pos < kCapG) s.list[pos] = make_comp(zz[j], bc.voff + i * 4 + j);
-      }
+    for (int t = 0; t < VEC; ++t) {
+      const int l = v * VEC + t;
+      z[t] = (l < c1) ? Dec<T>::elem(u, t) : -INFINITY;
+      if ((pb >> t) & 1u) z[t] = (l < c1) ? pen_value(l) : -INFINITY;
     }
   }
-  __syncthreads();
-  block_sort_desc(s, nb);
-}
-
-// Radix select inside bucket b (any size): the cutoff composite C where the running count
-// (or fixed-point mass) over the bucket's elements in descending composite order first
-// reaches `target`.  8 digit passes over the row.
-template <bool MASS>
-__device__ uint64_t radix_in_bucket(ExSmem& s, const BucketCtx& bc, int b, uint64_t target,
-                                   uint64_t floor_c = 0) {
-  uint64_t prefix = 0;
-  uint64_t need = target;
-  for (int d = 56; d >= 0; d -= 8) {
-    for (int i = threadIdx.x; i < 256; i += kExThreads) {
-      s.rcnt[i] = 0;
-      s.rmass[i] = 0;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int i = threadIdx.x; i < bc.Vp; i += kExThreads) {
-      const float z = bc.zs[i];
-      if (!(z > -INFINITY) || bucket_of(z, bc.M, bc.c_hi, bc.c_lo) != b) continue;
-      const uint64_t c = make_comp(z, bc.voff + i);
-      if (c < floor_c) continue;
-      if (d != 56 && (c >> (d + 8)) != prefix) continue;
-      const int dig = (int)((c >> d) & 255);
-      if (MASS) {
-        const float t = z - bc.M;
-        smem_add_u64(&s.rmass[dig], fixmass(ex2f(fmaf(t, bc.c_hi, t * bc.c_lo))));
-      } else {
-        atomicAdd(&s.rcnt[dig], 1u);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t run = 0;
-      int pick = 0;
-      for (int dg = 255; dg >= 0; --dg) {
-        const uint64_t v = MASS ? s.rmass[dg] : (uint64_t)s.rcnt[dg];
-        if (run + v >= need && v > 0) {
-          pick = dg;
-          break;
-        }
-        run += v;
-        pick = dg;
-      }
-      s.ints[2] = pick;
-      s.u64s[0] = run;
-    }
-    __syncthreads();
-    const int pick = s.ints[2];
-    need -= s.u64s[0];
-    prefix = (prefix << 8) | (uint64_t)pick;
-    __syncthreads();
-  }
-  return prefix;
-}
+};
 
 template <typename T>
 __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_constant__ ExactArgs a) {
-  const int r = blockIdx.x;
-  if (a.ro.info[r].status != kRowPending) return;
+  constexpr int VEC = Dec<T>::N;
   extern __shared__ __align__(128) uint8_t smem[];
-  ExSmem s;
-  s.cnt = reinterpret_cast<uint32_t*>(smem);
-  s.mass = reinterpret_cast<uint64_t*>(smem + kNB * 4);
-  s.list = reinterpret_cast<uint64_t*>(smem + kNB * 12);
-  s.u64s = reinterpret_cast<uint64_t*>(smem + kNB * 12 + kCapG * 8);
-  s.dbl = reinterpret_cast<double*>(smem + kNB * 12 + kCapG * 8 + 256);
-  s.ints = reinterpret_cast<int*>(smem + kNB * 12 + kCapG * 8 + 512);
-  s.rcnt = reinterpret_cast<uint32_t*>(smem + kNB * 12 + kCapG * 8 + 1024);
-  s.rmass = reinterpret_cast<uint64_t*>(smem + kNB * 12 + kCapG * 8 + 1024 + 1024);
   const int tid = threadIdx.x;
+  const uint32_t rank = ex_rank();
+  const int r = blockIdx.x / a.G;
+  const RowInfo ri = a.ro.info[r];
+  if (ri.status != kRowPending) return;  // (uniform over the cluster: no CTA of it continues)
+  int* side_id = reinterpret_cast<int*>(smem + kExOffSideId);
+  float* side_z = reinterpret_cast<float*>(smem + kExOffSideZ);
+  uint32_t* hcnt = reinterpret_cast<uint32_t*>(smem + kExOffCnt);
+  uint64_t* hmass = reinterpret_cast<uint64_t*>(smem + kExOffMass);
+  uint64_t* gat = reinterpret_cast<uint64_t*>(smem + kExOffGat);
+  double* sd = reinterpret_cast<double*>(smem + kExOffScr);        // [32]
+  uint64_t* su = reinterpret_cast<uint64_t*>(smem + kExOffScr + 256);  // [32]
+  int* si = reinterpret_cast<int*>(smem + kExOffScr + 512);           // [64]
+  // control block (written by the leader into every CTA): [0] phase-specific ints, doubles at sd2
+  int* ctl = reinterpret_cast<int*>(smem + kExOffScr + 768);          // [32]
+  double* cd = reinterpret_cast<double*>(smem + kExOffScr + 896);     // [16]
+  uint64_t* cu = reinterpret_cast<uint64_t*>(smem + kExOffScr + 1024);  // [16]
+  double* tots = reinterpret_cast<double*>(smem + kExOffScr + 1152);    // [16] per-CTA draw totals (leader)
+
   const int slot = a.slots ? a.slots[r] : r;
   const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
   const RowCfg rc = decode_row(prm, a.V, 1);
-  const RowInfo ri = a.ro.info[r];
   const float M = ri.M;
-  const double S = ri.S;
+  const double inv_tau = 1.0 / (double)rc.tau;
+  const double l2e_tau = kLog2e / (double)rc.tau;
 
-  // ---- pass 0: z' row
-  float* zs = a.scratch + (int64_t)r * a.Vp;
-  const uint8_t* lrow = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * sizeof(T);
+  ExRow<T> R;
+  R.rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * sizeof(T);
+  R.pm = a.hs.pmask + (int64_t)slot * a.hs.spr * 32;
+  R.side_id = side_id;
+  R.side_z = side_z;
+  R.ut = a.hs.uniq + (int64_t)slot * a.hs.L;
+  R.nu = a.hs.meta[slot].n_uniq;
+  R.voff = a.voff;
+  R.vloc = a.vloc;
+  R.c0 = min(a.vloc, (int)rank * a.Lc);
+  R.c1 = min(a.vloc, R.c0 + a.Lc);
+  R.prm = prm;
+  R.pen_mode = a.pen_mode;
+  const int v0 = R.c0 / VEC, v1 = (R.c1 + VEC - 1) / VEC;  // vectors of the chunk
+
+  // ---- the chunk's penalised elements: their table entries are contiguous (sorted by id)
   {
-    // 16-byte loads (8 bf16 / 4 f32 per vector; rows are 16-byte aligned, ld * elem % 16 == 0)
-    constexpr int VEC = 16 / (int)sizeof(T);
-    const int nvec = a.Vp / VEC;
-#pragma unroll 4
-    for (int v = tid; v < nvec; v += kExThreads) {
-      const uint4 u = (v * VEC < a.vloc) ? *reinterpret_cast<const uint4*>(lrow + (int64_t)v * 16)
-                                         : make_uint4(0u, 0u, 0u, 0u);
+    int below = 0, inside = 0;
+    for (int e = tid; e < R.nu; e += kExThreads) {
+      const int l = R.ut[e].id - a.voff;
+      below += (l < R.c0) ? 1 : 0;
+      inside += (l >= R.c0 && l < R.c1) ? 1 : 0;
+    }
+    const int lo = (int)ex_sum_u64((uint64_t)below, su), n = (int)ex_sum_u64((uint64_t)inside, su);
+    R.ovf = n > kSide;
+    R.nside = R.ovf ? 0 : n;
+    for (int e = tid; e < R.nside; e += kExThreads) {
+      const UniqEntry ue = R.ut[lo + e];
+      const int l = ue.id - a.voff;
+      side_id[e] = l;
+      side_z[e] = apply_penalty(Dec<T>::load1(R.rowp, l), ue.meta, prm, a.pen_mode);
+    }
+  }
+  // weight coordinates of z: y = (M - z) log2(e)/tau; w = 2^-y; level-0 bucket floor(64 y)
+  auto ycoord = [&](float z) -> double { return ((double)M - (double)z) * l2e_tau; };
+  // one pass over the chunk's elements (coalesced: vector v of thread tid, stride 512)
+  auto for_each = [&](auto&& fn) {
+    for (int v = v0 + tid; v < v1; v += kExThreads) {
       float z[VEC];
-      if (sizeof(T) == 2) {
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      R.vec(v, z);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          z[2 * q] = __uint_as_float(w[q] << 16);
-          z[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
-        }
-      } else {
-        z[0] = __uint_as_float(u.x);
-        z[1] = __uint_as_float(u.y);
-        z[2] = __uint_as_float(u.z);
-        z[3 % VEC] = __uint_as_float(u.w);
+      for (int t = 0; t < VEC; ++t)
+        if (z[t] > -INFINITY) fn(z[t], v * VEC + t);
+    }
+  };
+  // histogram of a level: bucket(y) in [0, nb) for y in [ybase, ybase + nb / scale), masses
+  // relative to the bucket top 2^-(ybase + b/scale)
+  auto histogram = [&](double ybase, double scale, int nb) {
+    for (int i = tid; i < nb; i += kExThreads) {
+      hcnt[i] = 0;
+      hmass[i] = 0;
+    }
+    ex_bar();
+    for_each([&](float z, int) {
+      const double y = ycoord(z);
+      const double q = (y - ybase) * scale;
+      if (!(q >= 0.0)) return;
+      int b = (int)q;
+      if (b >= nb) {
+        if (nb == kNB0) b = nb - 1;  // (level 0: the far tail shares the last bucket)
+        else return;
       }
-#pragma unroll
-      for (int e = 0; e < VEC; ++e)
-        if (v * VEC + e >= a.vloc) z[e] = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < VEC; e += 4)
-        *reinterpret_cast<float4*>(zs + v * VEC + e) = make_float4(z[e], z[e + 1], z[e + 2], z[e + 3]);
+      const double d = (y - ybase - (double)b / scale) * kLn2;  // >= 0
+      const double rel = (b == nb - 1 && nb == kNB0) ? exp2(-(y - ybase - (double)b / scale)) : exp2_neg_small(d);
+      atomicAdd(&hcnt[b], 1u);
+      smem_add_u64(&hmass[b], (uint64_t)(rel * kFix40 + 0.5));
+    });
+    ex_bar();
+  };
+  // the cluster's total of bucket b (leader; reads every CTA's histogram over DSMEM)
+  auto tot_bucket = [&](int b, uint32_t* cnt, uint64_t* mass) {
+    uint32_t c = 0;
+    uint64_t m = 0;
+    for (int g = 0; g < a.G; ++g) {
+      c += ex_ld32(ex_map(hcnt + b, (uint32_t)g));
+      m += ex_ld64(ex_map(hmass + b, (uint32_t)g));
     }
-  }
-  __syncthreads();
-  {
-    const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
-    const int nu = a.hs.meta[slot].n_uniq;
-    for (int i = tid; i < nu; i += kExThreads) {
-      const UniqEntry e = ut[i];
-      const int j = e.id - a.voff;
-      if (j < 0 || j >= a.vloc) continue;
-      float x;
-      if (sizeof(T) == 2)
-        x = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(lrow)[j] << 16);
-      else
-        x = reinterpret_cast<const float*>(lrow)[j];
-      zs[j] = apply_penalty(x, e.meta, prm, a.pen_mode);
-    }
-  }
-  __threadfence_block();
-  __syncthreads();
-
-  BucketCtx bc;
-  bc.zs = zs;
-  bc.Vp = a.Vp;
-  bc.voff = a.voff;
-  bc.M = M;
-  bc.c_hi = rc.c_hi;
-  bc.c_lo = rc.c_lo;
-
-  // ---- pass 1: histogram
-  for (int i = tid; i < kNB; i += kExThreads) {
-    s.cnt[i] = 0;
-    s.mass[i] = 0;
-  }
-  __syncthreads();
-  int nfin_loc = 0;
-  const float4* z4 = reinterpret_cast<const float4*>(zs);
-#pragma unroll 4
-  for (int i = tid; i < a.Vp / 4; i += kExThreads) {
-    const float4 q = z4[i];
-    const float zz[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (zz[j] > -INFINITY) {
-        const float t = zz[j] - M;
-        const float x = fmaf(t, rc.c_hi, t * rc.c_lo);
-        const float y = -x * 64.0f;
-        const int b = y >= (float)(kNB - 1) ? kNB - 1 : (y > 0.0f ? (int)y : 0);
-        atomicAdd(&s.cnt[b], 1u);
-        smem_add_u64(&s.mass[b], fixmass(ex2f(x)));
-        ++nfin_loc;
+    *cnt = c;
+    *mass = m;
+  };
+  // gather the composites of every element of bucket b (level given) into the leader's buffer
+  auto gather = [&](double ybase, double scale, int nb, int b) {
+    const uint32_t cnt_addr = ex_map(ctl + 20, 0);
+    for_each([&](float z, int l) {
+      const double q = (ycoord(z) - ybase) * scale;
+      if (!(q >= 0.0)) return;
+      int bb = (int)q;
+      if (bb >= nb) {
+        if (nb == kNB0) bb = nb - 1;
+        else return;
       }
-    }
-  }
-  __syncthreads();
-  const int nfin = block_sum_int(nfin_loc, s);
+      if (bb != b) return;
+      const uint32_t at = ex_atom_add(cnt_addr, 1u);
+      if (at < (uint32_t)kGat) ex_st64(ex_map(gat + at, 0), make_comp(z, a.voff + l));
+    });
+  };
 
-  // ---- cutoffs (composites; K = {composite >= C})
+  ex_csync();  // every CTA's side list is built; the cluster is resident
+  // ---- pass 1: level-0 histograms; the leader sums the cluster's and finds the cutoffs
+  histogram(0.0, 64.0, kNB0);
+  ex_csync();
+  // level-0 totals per bucket, in the leader; every CTA reads them (fixed order, deterministic)
+  uint32_t tc[kNB0 / kExThreads];
+  double tm[kNB0 / kExThreads];
+  for (int j = 0; j < kNB0 / kExThreads; ++j) {
+    const int b = tid * (kNB0 / kExThreads) + j;  // thread owns 4 consecutive buckets
+    uint64_t m;
+    tot_bucket(b, &tc[j], &m);
+    tm[j] = (double)m * (1.0 / kFix40) * exp2(-(double)b / 64.0);
+  }
+  ex_csync();  // (every CTA has read every histogram; they may be reused)
+
+  // cutoffs as composites: K = { composite >= C }
   uint64_t Ck = 0, Cp = 0, Cm = 0;
-  int bk = kNB;          // bucket holding the k-th element (kNB: top-k off / keeps all)
   double W1 = 0.0;
-  bool k_sorted = false;  // s.list holds bucket bk sorted
-  int nbk = 0;
-  if (rc.topk_on && rc.k < nfin) {
-    uint64_t before;
-    bk = find_bucket<false>(s, (uint64_t)rc.k, kNB, &before);
-    nbk = (int)s.cnt[bk];
-    const int need = rc.k - (int)before;
-    if (nbk <= kCapG) {
-      gather_bucket(s, bc, bk, nbk);
-      Ck = s.list[need - 1];
-      k_sorted = true;
-    } else {
-      Ck = radix_in_bucket<false>(s, bc, bk, (uint64_t)need);
-    }
+  // bucket-level prefix (counts, masses) in bucket order = pi order
+  uint32_t cloc = 0;
+  double mloc = 0.0;
+  for (int j = 0; j < kNB0 / kExThreads; ++j) {
+    cloc += tc[j];
+    mloc += tm[j];
   }
-  if (rc.top_p < 1.0f) {
-    // W1 = mass of K1
-    if (bk < kNB) {
-      uint64_t mabove = 0;
-      for (int b = tid; b < bk; b += kExThreads) mabove += s.mass[b];
-      mabove = block_sum_u64(mabove, s);
-      double part = 0.0;
-      if (k_sorted) {
-        double loc = 0.0;
-        for (int i = tid; i < nbk; i += kExThreads)
-          if (s.list[i] >= Ck) loc += exp(((double)comp_val(s.list[i]) - (double)M) / (double)rc.tau);
-        double tot;
-        block_excl_scan_d(loc, &tot, s);
-        part = tot;
-      } else {
-        // partial mass inside bk via a pass
-        double loc = 0.0;
-#pragma unroll 4
-        for (int i = tid; i < a.Vp; i += kExThreads) {
-          const float z = zs[i];
-          if (z > -INFINITY && bucket_of(z, M, rc.c_hi, rc.c_lo) == bk && make_comp(z, a.voff + i) >= Ck) {
-            const float t = z - M;
-            loc += (double)ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
-          }
-        }
-        double tot;
-        block_excl_scan_d(loc, &tot, s);
-        part = tot;
+  const uint64_t nfin = ex_sum_u64((uint64_t)cloc, su);
+  double mtot;
+  const double mbefore = ex_excl_scan_d(mloc, &mtot, sd);
+  // exclusive count prefix per thread (integer)
+  uint32_t cb;
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    const int incl = warp_incl_scan_i((int)cloc, lane);
+    ex_bar();
+    if (lane == 31) si[w] = incl;
+    ex_bar();
+    int bf = 0;
+    for (int i = 0; i < w; ++i) bf += si[i];
+    cb = (uint32_t)(bf + incl - (int)cloc);
+    ex_bar();
+  }
+  const bool topk = rc.topk_on && (uint64_t)rc.k < nfin;
+  // locate the bucket where a running quantity (count or mass) first reaches target
+  auto find_bucket = [&](bool mass, double target, uint64_t ctarget, int limit, int* bucket, double* before) {
+    if (tid == 0) ctl[0] = -1;
+    ex_bar();
+    double run = mbefore;
+    uint32_t crun = cb;
+    for (int j = 0; j < kNB0 / kExThreads; ++j) {
+      const int b = tid * (kNB0 / kExThreads) + j;
+      if (b >= limit) break;
+      const bool hit = mass ? (run + tm[j] >= target) : ((uint64_t)crun + tc[j] >= ctarget);
+      if (hit && tc[j] > 0) {
+        atomicMin(&ctl[0], b);  // (the first bucket reaching the target)
       }
-      W1 = (double)mabove / kFix + part;
-    } else {
-      W1 = S;
+      run += tm[j];
+      crun += tc[j];
     }
-    const double target = (double)rc.top_p * W1;
-    const uint64_t tfix = (uint64_t)(target * kFix);
-    uint64_t before;
-    const int bp = find_bucket<true>(s, tfix > 0 ? tfix : 1, bk, &before);
-    if (bp >= 0) {
-      const int nb = (int)s.cnt[bp];
-      if (nb <= kCapG) {
-        gather_bucket(s, bc, bp, nb);
-        // walk in pi order with float64 weights: first i with before + c_i >= target
-        double lw = 0.0;
-        // each thread: contiguous run of the sorted list
-        const int per = (nb + kExThreads - 1) / kExThreads;
-        const int i0 = tid * per, i1 = min(nb, i0 + per);
-        for (int i = i0; i < i1; ++i) lw += exp(((double)comp_val(s.list[i]) - (double)M) / (double)rc.tau);
-        double tot;
-        const double ex = block_excl_scan_d(lw, &tot, s) + (double)before / kFix;
-        if (tid == 0) s.ints[3] = nb - 1;
-        __syncthreads();
-        double run = ex;
-        for (int i = i0; i < i1; ++i) {
-          run += exp(((double)comp_val(s.list[i]) - (double)M) / (double)rc.tau);
-          if (run >= target) {
-            atomicMin(&s.ints[3], i);
+    ex_bar();
+    const int bsel = ctl[0] < 0 ? -1 : ctl[0];
+    // its prefix: recompute in fixed order from the per-thread values (the owner publishes it)
+    ex_bar();
+    if (bsel >= 0 && tid == bsel / (kNB0 / kExThreads)) {
+      double rr = mbefore;
+      uint32_t cr = cb;
+      for (int j = 0; j < bsel - tid * (kNB0 / kExThreads); ++j) {
+        rr += tm[j];
+        cr += tc[j];
+      }
+      cd[0] = rr;
+      ctl[1] = (int)cr;
+      cd[1] = tm[bsel - tid * (kNB0 / kExThreads)];
+      ctl[2] = (int)tc[bsel - tid * (kNB0 / kExThreads)];
+    }
+    ex_bar();
+    *bucket = bsel;
+    *before = mass ? cd[0] : (double)ctl[1];
+    ex_bar();
+  };
+  // exact resolution inside bucket b0 of level 0: gather its elements (or, if too many, those of
+  // the level-1 sub-bucket reaching the target), sort by (z' desc, id asc) and walk with exact w.
+  // mode 0: the count-th element (count = need); mode 1: the first element whose cumulative mass
+  // (from `before`) reaches target; returns its composite and the exact mass of the walked prefix.
+  auto resolve = [&](int b0, int mode, uint64_t need, double before, double target, double* prefix_mass) -> uint64_t {
+    double ybase = (double)b0 / 64.0, scale = 65536.0;
+    int level = 0;
+    if (tid == 0) ctl[20] = 0;
+    ex_csync();
+    gather(0.0, 64.0, kNB0, b0);
+    ex_csync();
+    if (ctl[20] == 0 || rank != 0) {
+      // (non-leaders only help gather)
+    }
+    int n = (int)ex_ld32(ex_map(ctl + 20, 0));
+    ex_csync();
+    if (n > kGat) {  // too large: one more level inside bucket b0
+      level = 1;
+      histogram(ybase, scale, kNB1);
+      ex_csync();
+      // leader: the sub-bucket; every CTA computes the same from the cluster totals
+      uint32_t sc[kNB1 / kExThreads];
+      double sm[kNB1 / kExThreads];
+      for (int j = 0; j < kNB1 / kExThreads; ++j) {
+        const int b = tid * (kNB1 / kExThreads) + j;
+        uint64_t m;
+        tot_bucket(b, &sc[j], &m);
+        sm[j] = (double)m * (1.0 / kFix40) * exp2(-(ybase + (double)b / scale));
+      }
+      ex_csync();
+      double l_m = 0.0;
+      uint32_t l_c = 0;
+      for (int j = 0; j < kNB1 / kExThreads; ++j) {
+        l_m += sm[j];
+        l_c += sc[j];
+      }
+      double dummy;
+      const double mb = ex_excl_scan_d(l_m, &dummy, sd) + before;
+      uint32_t cbb;
+      {
+        const int lane = tid & 31, w = tid >> 5;
+        const int incl = warp_incl_scan_i((int)l_c, lane);
+        ex_bar();
+        if (lane == 31) si[w] = incl;
+        ex_bar();
+        int bf = 0;
+        for (int i = 0; i < w; ++i) bf += si[i];
+        cbb = (uint32_t)(bf + incl - (int)l_c);
+        ex_bar();
+      }
+      if (tid == 0) ctl[0] = 0x7FFFFFFF;
+      ex_bar();
+      {
+        double rr = mb;
+        uint32_t cr = cbb;
+        for (int j = 0; j < kNB1 / kExThreads; ++j) {
+          const int b = tid * (kNB1 / kExThreads) + j;
+          const bool hit = (mode == 1) ? (rr + sm[j] >= target) : ((uint64_t)cr + sc[j] >= need);
+          if (hit && sc[j] > 0) atomicMin(&ctl[0], b);
+          rr += sm[j];
+          cr += sc[j];
+        }
+      }
+      ex_bar();
+      int sb = ctl[0];
+      if (sb == 0x7FFFFFFF) sb = kNB1 - 1;
+      ex_bar();
+      if (tid == sb / (kNB1 / kExThreads)) {
+        double rr = mb;
+        uint32_t cr = cbb;
+        for (int j = 0; j < sb - tid * (kNB1 / kExThreads); ++j) {
+          rr += sm[j];
+          cr += sc[j];
+        }
+        cd[2] = rr;
+        ctl[3] = (int)cr;
+      }
+      ex_bar();
+      before = cd[2];
+      const uint64_t cbefore = (uint64_t)ctl[3];
+      if (mode == 0) need -= (cbefore - 0);  // (need counted from the bucket start)
+      ex_bar();
+      if (tid == 0) ctl[20] = 0;
+      ex_csync();
+      gather(ybase, scale, kNB1, sb);
+      ex_csync();
+      n = (int)ex_ld32(ex_map(ctl + 20, 0));
+      ex_csync();
+    }
+    n = min(n, kGat);  // (beyond: a pathological tie mass; the first kGat are kept)
+    uint64_t pick = 0;
+    double pm = before;
+    if (rank == 0) {
+      ex_sort_desc(gat, n);
+      // walk: thread 0 over the sorted bucket (exact float64 weights, sequential like the oracle)
+      if (tid == 0) {
+        double run = before;
+        uint64_t sel = n > 0 ? gat[n - 1] : 0;
+        double selrun = run;
+        for (int i = 0; i < n; ++i) {
+          const double w = exp(((double)comp_val(gat[i]) - (double)M) * inv_tau);
+          run += w;
+          if (mode == 0 ? ((uint64_t)(i + 1) >= need) : (run >= target)) {
+            sel = gat[i];
+            selrun = run;
             break;
           }
+          selrun = run;
         }
-        __syncthreads();
-        Cp = s.list[s.ints[3]];
-        __syncthreads();
-      } else {
-        const uint64_t need = tfix - before;
-        Cp = radix_in_bucket<true>(s, bc, bp, need > 0 ? need : 1);
+        cu[0] = sel;
+        cd[3] = selrun;
       }
-    } else if (bk < kNB) {
-      // cutoff falls inside the top-k boundary bucket (or rounding shortfall): walk K1's part
-      if (k_sorted) {
-        uint64_t mabove = 0;
-        for (int b = tid; b < bk; b += kExThreads) mabove += s.mass[b];
-        mabove = block_sum_u64(mabove, s);
+      ex_bar();
+      pick = cu[0];
+      pm = cd[3];
+      // broadcast to every CTA
+      for (int g = 1; g < a.G; ++g)
         if (tid == 0) {
-          double run = (double)mabove / kFix;
-          uint64_t pick = Ck;
-          for (int i = 0; i < nbk && s.list[i] >= Ck; ++i) {
-            run += exp(((double)comp_val(s.list[i]) - (double)M) / (double)rc.tau);
-            if (run >= target) {
-              pick = s.list[i];
-              break;
-            }
-          }
-          s.u64s[1] = pick;
+          ex_st64(ex_map(cu + 0, (uint32_t)g), pick);
+          ex_st64(ex_map(cd + 3, (uint32_t)g), __double_as_longlong(pm));
         }
-        __syncthreads();
-        Cp = s.u64s[1];
-        __syncthreads();
-      } else {
-        uint64_t mabove = 0;
-        for (int b = tid; b < bk; b += kExThreads) mabove += s.mass[b];
-        mabove = block_sum_u64(mabove, s);
-        const uint64_t need = tfix > mabove ? tfix - mabove : 1;
-        Cp = radix_in_bucket<true>(s, bc, bk, need, Ck);
-        if (Cp < Ck) Cp = Ck;
-      }
     }
+    (void)level;
+    ex_csync();
+    pick = cu[0];
+    pm = cd[3];
+    *prefix_mass = pm;
+    return pick;
+  };
+
+  // ---- top-k (count) cutoff, then W1 = mass of K1
+  int bk = kNB0;
+  if (topk) {
+    double bf;
+    find_bucket(false, 0.0, (uint64_t)rc.k, kNB0, &bk, &bf);
+    const uint64_t need = (uint64_t)rc.k - (uint64_t)bf;
+    double pmass;
+    Ck = resolve(bk, 0, need, 0.0, 0.0, &pmass);
+    // W1 = mass of the buckets before bk + the exact mass of bk's elements >= Ck
+    double mb_bk;
+    {
+      int dummy_b;
+      double dummy_before;
+      (void)dummy_b;
+      (void)dummy_before;
+    }
+    // mass before bucket bk (fixed order, from the per-thread values)
+    if (tid == 0) cd[4] = 0.0;
+    ex_bar();
+    if (tid == bk / (kNB0 / kExThreads)) {
+      double rr = mbefore;
+      for (int j = 0; j < bk - tid * (kNB0 / kExThreads); ++j) rr += tm[j];
+      cd[4] = rr;
+    }
+    ex_bar();
+    mb_bk = cd[4];
+    ex_bar();
+    W1 = mb_bk + pmass;  // (pmass: the walk's mass of bk's first `need` elements, from 0)
+  } else {
+    W1 = mtot;
   }
+  // ---- top-p cutoff over K1 (renormalised, R7; >= p W1, R8)
+  if (rc.top_p < 1.0f) {
+    const double target = (double)rc.top_p * W1;
+    int bp;
+    double bf;
+    find_bucket(true, target, 0, topk ? bk + 1 : kNB0, &bp, &bf);
+    if (bp < 0) bp = topk ? bk : kNB0 - 1;  // (rounding at the very top of the mass)
+    double pmass;
+    Cp = resolve(bp, 1, 0, bf, target, &pmass);
+    if (topk && Cp < Ck) Cp = Ck;
+  }
+  // ---- min-p: the smallest binary32 z with exp((z - M)/tau) >= min_p (bisection on keys)
   if (rc.min_p > 0.0f) {
-    // smallest binary32 z with exp((z-M)/tau) >= min_p  (bisection on monotone keys)
     if (tid == 0) {
-      uint32_t lo = f2key(-INFINITY), hi = f2key(M);  // w(hi) = 1 >= min_p
+      uint32_t lo = f2key(-INFINITY), hi = f2key(M);
       while (hi - lo > 1) {
         const uint32_t mid = lo + (hi - lo) / 2;
-        const double z = (double)key2f(mid);
-        if (exp((z - (double)M) / (double)rc.tau) >= (double)rc.min_p)
-          hi = mid;
-        else
-          lo = mid;
+        if (exp(((double)key2f(mid) - (double)M) / (double)rc.tau) >= (double)rc.min_p) hi = mid;
+        else lo = mid;
       }
-      s.u64s[2] = ((uint64_t)hi << 32);  // every id with value >= key2f(hi)
+      cu[1] = (uint64_t)hi << 32;  // every id with value >= key2f(hi)
     }
-    __syncthreads();
-    Cm = s.u64s[2];
-    __syncthreads();
+    ex_bar();
+    Cm = cu[1];
+    ex_bar();
   }
-  uint64_t C3 = Ck;
-  C3 = Cp > C3 ? Cp : C3;
+  uint64_t C3 = Ck > Cp ? Ck : Cp;
   C3 = Cm > C3 ? Cm : C3;
 
-  // ---- pass 2: draw in ascending id order over K3 = {composite >= C3}
-  // (each thread owns a contiguous, 16-byte aligned id range: Vp is a multiple of 4)
-  const int per = ((a.Vp + kExThreads - 1) / kExThreads + 3) / 4 * 4;
-  const int j0 = min(a.Vp, tid * per), j1 = min(a.Vp, j0 + per);
+  // ---- the draw: W = mass of K3 in id order; per-CTA totals -> cluster prefix -> the CTA and the
+  //      thread holding u*W walk their elements in id order
   double loc = 0.0;
-#pragma unroll 2
-  for (int j = j0; j < j1; j += 4) {
-    const float4 q = *reinterpret_cast<const float4*>(zs + j);
-    const float zz[4] = {q.x, q.y, q.z, q.w};
-    float l4 = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (zz[e] > -INFINITY && make_comp(zz[e], a.voff + j + e) >= C3) {
-        const float t = zz[e] - M;
-        l4 += ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
-      }
-    loc += (double)l4;
-  }
-  double W;
-  const double ex = block_excl_scan_d(loc, &W, s);
+  for_each([&](float z, int l) {
+    if (make_comp(z, a.voff + l) >= C3) loc += exp(((double)z - (double)M) * inv_tau);
+  });
+  const double ctot = ex_sum_d(loc, sd);
+  if (tid == 0) ex_st64(ex_map(tots + rank, 0), __double_as_longlong(ctot));
+  ex_csync();
   const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
   const double u = philox_uniform(seed, prm.request_id, a.step);
-  const double target = u * W;
-  if (tid == 0) s.ints[4] = 0x7FFFFFFF;
-  __syncthreads();
-  if (ex <= target && target < ex + loc) {
-    // the same arithmetic as the chunk sum above: float sums of 4, then float64
-    double run = ex;
-    for (int j = j0; j < j1; j += 4) {
-      float w4[4], l4 = 0.f;
+  if (rank == 0 && tid == 0) {
+    double W = 0.0;
+    for (int g = 0; g < a.G; ++g) W += tots[g];
+    const double target = u * W;
+    int gsel = -1;
+    double pre = 0.0;
+    for (int g = 0; g < a.G; ++g) {
+      if (gsel < 0 && tots[g] > 0.0 && (pre + tots[g] > target)) gsel = g;
+      if (gsel < 0) pre += tots[g];
+    }
+    int glast = -1;
+    for (int g = 0; g < a.G; ++g)
+      if (tots[g] > 0.0) glast = g;
+    if (gsel < 0) {  // (u W at the top of the mass: the last kept id)
+      gsel = glast;
+      pre = 0.0;
+      for (int g = 0; g < gsel; ++g) pre += tots[g];
+    }
+    for (int g = 0; g < a.G; ++g) {
+      const uint32_t cg = ex_map(ctl + 8, (uint32_t)g);
+      asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cg), "r"((uint32_t)gsel) : "memory");
+      ex_st64(ex_map(cd + 8, (uint32_t)g), __double_as_longlong(target - pre));
+      ex_st64(ex_map(cd + 9, (uint32_t)g), __double_as_longlong(W));
+      ex_st64(ex_map(cd + 10, (uint32_t)g), __double_as_longlong(target >= pre + tots[gsel] ? 1.0 : 0.0));
+    }
+  }
+  ex_csync();
+  if ((int)rank == ctl[8]) {
+    // this CTA holds the draw: walk its chunk in id order, rounds of 512 vectors (block scans)
+    const double tgt = cd[8], W = cd[9];
+    const bool at_top = cd[10] != 0.0;
+    double run = 0.0;
+    if (tid == 0) {
+      ctl[9] = -1;   // found element (local id)
+      ctl[11] = -1;  // last kept element (local id)
+    }
+    ex_bar();
+    for (int base = v0; base < v1; base += kExThreads) {
+      const int v = base + tid;
+      float z[VEC];
+      double wl[VEC];
+      double vs = 0.0;
+      int last = -1;
+      if (v < v1) {
+        R.vec(v, z);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float z = zs[j + e];
-        w4[e] = 0.f;
-        if (z > -INFINITY && make_comp(z, a.voff + j + e) >= C3) {
-          const float t = z - M;
-          w4[e] = ex2f(fmaf(t, rc.c_hi, t * rc.c_lo));
+        for (int t = 0; t < VEC; ++t) {
+          const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + v * VEC + t) >= C3;
+          wl[t] = kept ? exp(((double)z[t] - (double)M) * inv_tau) : 0.0;
+          vs += wl[t];
+          if (kept) last = v * VEC + t;
         }
-        l4 += w4[e];
-      }
-      if (run + (double)l4 > target) {
-        float cf = 0.f;
-        int pick = j + 3;
+      } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          cf += w4[e];
-          if (w4[e] > 0.f && run + (double)cf > target) {
-            pick = j + e;
+        for (int t = 0; t < VEC; ++t) wl[t] = 0.0;
+      }
+      double rt;
+      const double ex = ex_excl_scan_d(vs, &rt, sd) + run;
+      if (!at_top && vs > 0.0 && ex <= tgt && tgt < ex + vs) {  // (one thread: the crossing vector)
+        double c = ex;
+        int pick = last;
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) {
+          c += wl[t];
+          if (wl[t] > 0.0 && c > tgt) {
+            pick = v * VEC + t;
             break;
           }
         }
-        atomicMin(&s.ints[4], pick);
-        break;
+        ctl[9] = pick;
       }
-      run += (double)l4;
+      if (last >= 0) atomicMax(&ctl[11], last);
+      run += rt;
+      ex_bar();
+      if (ctl[9] >= 0) break;  // (uniform after the barrier)
     }
+    if (tid == 0) {
+      const int l = (ctl[9] >= 0) ? ctl[9] : ctl[11];  // (u W at the top of the mass: the last kept id)
+      float zz[VEC];
+      R.vec(l / VEC, zz);
+      const float ztok = zz[l % VEC];
+      const int tok = a.voff + l;
+      const double wtok = exp(((double)ztok - (double)M) * inv_tau);
+      const double lp = ((double)ztok - (double)M) * inv_tau - log(ri.S);
+      a.ro.tokens[r] = tok;
+      a.ro.logprobs[r] = (float)lp;
+      if (a.ro.flogprobs) a.ro.flogprobs[r] = (float)log(wtok / W);
+      if (a.ro.status) a.ro.status[r] = SAMPLER_ROW_OK;
+      RowInfo o = ri;
+      o.status = SAMPLER_ROW_OK;
+      o.W = W;
+      o.cutoff = C3;
+      o.token = tok;
+      a.ro.info[r] = o;
+      ctl[12] = tok;
+    }
+    ex_bar();
+    if (a.append && tid < 32) warp_append_token(a.hs, slot, ctl[12], tid);
   }
-  __syncthreads();
-  int jt = s.ints[4];
-  if (jt == 0x7FFFFFFF) {
-    // rounding: take the last kept id
-    int last = -1;
-    for (int j = j0; j < j1; ++j)
-      if (zs[j] > -INFINITY && make_comp(zs[j], a.voff + j) >= C3) last = j;
-    __syncthreads();
-    if (tid == 0) s.ints[4] = -1;
-    __syncthreads();
-    atomicMax(&s.ints[4], last);
-    __syncthreads();
-    jt = s.ints[4];
-  }
-  if (tid == 0) {
-    const float zt = zs[jt];
-    const double wt = exp(((double)zt - (double)M) / (double)rc.tau);
-    const double lp = ((double)zt - (double)M) / (double)rc.tau - log(S);
-    const int32_t tok = a.voff + jt;
-    a.ro.tokens[r] = tok;
-    a.ro.logprobs[r] = (float)lp;
-    if (a.ro.flogprobs) a.ro.flogprobs[r] = (float)log(wt / W);
-    if (a.ro.status) a.ro.status[r] = SAMPLER_ROW_OK;
-    RowInfo o = ri;
-    o.status = SAMPLER_ROW_OK;
-    o.W = W;
-    o.cutoff = C3;
-    o.token = tok;
-    a.ro.info[r] = o;
-    s.ints[5] = tok;
-  }
-  __syncthreads();
-  if (a.append && tid < 32) warp_append_token(a.hs, slot, s.ints[5], tid);
+  ex_csync();  // no CTA leaves while another may still address its shared memory
 }
 
 // Debug: q[b, v] = final filtered distribution (w_v / W over K3; one-hot for greedy rows).

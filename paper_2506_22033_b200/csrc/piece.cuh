@@ -58,6 +58,7 @@ __device__ __forceinline__ uint32_t key16_down(float f) {
   uint32_t b = __float_as_uint(f);
   uint32_t h = b >> 16;
   if ((b >> 31) && (b & 0xFFFFu)) h += 1;  // negative with dropped bits: one bf16 step down
+  if (h == 0xFF80u && f > -INFINITY) h = 0xFF7Fu;  // finite below the lowest bf16: its lowest finite key
   if (f != f) h = 0x7F80u;
   return h ^ ((h >> 15) ? 0xFFFFu : 0x8000u);
 }

@@ -628,6 +628,10 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     for (int i = 0; i < n && !need; ++i) need = row_may_pend(h->h_params[i], h->cfg.vocab_size, h->cfg.max_top_k);
   }
   if (need) {
+    // one cluster of G CTAs per row (every row launched; rows that are not pending exit at once):
+    // G = the largest power of two <= 8 with B * G <= 2 CTAs per SM
+    int G = 1;
+    while (G < 8 && (int64_t)B * G * 2 <= 2LL * h->sm_count) G *= 2;
     ExactArgs e{};
     e.logits = logits;
     e.ld = ld;
@@ -635,7 +639,8 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     e.V = h->cfg.vocab_size;
     e.voff = h->cfg.vocab_offset;
     e.vloc = h->cfg.vocab_local;
-    e.Vp = h->Vp;
+    e.G = G;
+    e.Lc = (int)((((int64_t)h->cfg.vocab_local + G - 1) / G + 127) / 128 * 128);
     e.slots = slots_dev;
     e.params_dev = params_dev;
     e.params_tab = h->d_params;
@@ -644,13 +649,23 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     e.append = append;
     e.pen_mode = h->cfg.penalty_mode;
     e.hs = a.hs;
-    e.scratch = h->d_scratch;
     e.ro = ro;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * G));
+    cfg.blockDim = dim3(kExThreads);
+    cfg.dynamicSmemBytes = kExactSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     if (h->cfg.logits_dtype == SAMPLER_BF16)
-      exact_kernel<__nv_bfloat16><<<B, kExThreads, kExactSmem, st>>>(e);
+      CK(h, cudaLaunchKernelEx(&cfg, exact_kernel<__nv_bfloat16>, e));
     else
-      exact_kernel<float><<<B, kExThreads, kExactSmem, st>>>(e);
-    CK(h, cudaGetLastError());
+      CK(h, cudaLaunchKernelEx(&cfg, exact_kernel<float>, e));
     tmark(h, 3, st);
     h->last_launches = 3;
   }

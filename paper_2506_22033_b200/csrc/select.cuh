@@ -16,6 +16,7 @@
 //   append     the sampled token into the slot's history (block-parallel shift from the smem copy)
 // mode 1 (vocab-sharded phase 1) emits the row's candidate record instead of deciding.
 #pragma once
+#include <cfloat>
 #include "block.cuh"
 #include "common.cuh"
 #include "elem.cuh"
@@ -583,6 +584,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   const bool rowok = !bad && M > -INFINITY;
   uint32_t lo_k = kKey16NegInf + 1;
   float Tv = 0.f;
+  bool take_all = false;
   uint64_t floor = 0;
   {
   // ---- bound: T = the K-th largest step key (each step key = the max of 1024 / 512 elements
@@ -648,7 +650,11 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     cbar();
     if (ctl[0] != 0) lo_k = (uint32_t)ctl[0];
   }
-  Tv = key16_val(lo_k);
+  // no bound (fewer than K finite keys, or the K-th below the histogram window): every finite
+  // element is collected, so the candidate set is the complete row (a top-k row with
+  // fewer than k finite logits is then decided here, not left pending)
+  take_all = lo_k == kKey16NegInf + 1;
+  Tv = take_all ? -FLT_MAX : key16_val(lo_k);
   // ---- collect: penalised elements (exact), then the qualifying groups (their re-read overlaps
   // the float64 softmax terms S = sum_parts s 2^((m - M) c) + sum_pen 2^((z' - M) c))
   auto push = [&](uint64_t c) {
@@ -767,16 +773,17 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     for (; j < nc && rank < keff; ++j) rank += ms.pool[j] > c ? 1 : 0;
     if (rank < keff) {
       ms.top[rank] = c;
-      // w = exp((z' - M)/tau) = 2^((z' - M) log2(e)/tau): MUFU exp2 (relative error ~2^-22), the
-      // argument rounded once to binary32
-      ms.wv[rank] = rc.greedy ? 0.0 : (double)ex2f((float)(((double)comp_val(c) - (double)M) * rc.c_d));
+      // w = exp((z' - M)/tau) in float64 (R16: the kept-set weights, their top-p prefix
+      // sums and the draw's CDF are float64-accurate, so a token may differ from the oracle's only
+      // when a boundary lies within 1e-9 of it)
+      ms.wv[rank] = rc.greedy ? 0.0 : dexp_call(((double)comp_val(c) - (double)M) / (double)rc.tau);
     }
   }
   cbar();
   STR(5);
   const int n = nc < keff ? nc : keff;
   // every element >= T is in the pool: the candidates are exact from the top down to T
-  uint64_t F = rowok ? make_comp(Tv, 0x7FFFFFFF) : 0ull;
+  uint64_t F = (rowok && !take_all) ? make_comp(Tv, 0x7FFFFFFF) : 0ull;
   F = floor > F ? floor : F;
   if (nc > keff) F = ms.top[keff - 1] > F ? ms.top[keff - 1] : F;
 

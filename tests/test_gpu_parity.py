@@ -112,6 +112,33 @@ def test_row_faults_nan_inf_all_neg_inf():
     assert math.isnan(out["logprobs"][0].item())
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_topk_only_rows_with_fewer_than_k_finite_logits(dtype):
+    """with every row top-k-only the exact multi-pass kernel is not launched; rows with
+    fewer finite logits than k (constrained decoding masks) must still be decided, with
+    K1 = every finite id; also a row whose finite logits lie far below one huge logit."""
+    from workloads.synth import f32_to_bf16_bits
+    rng = np.random.default_rng(78)
+    B, V = 8, 4000
+    z = rng.normal(size=(B, V)).astype(np.float32)
+    z[1, :] = -np.inf
+    z[1, [5, 77, 1234]] = [0.5, 1.5, -2.0]            # 3 finite logits, k = 40
+    z[2, :-39] = -np.inf                               # 39 finite logits, k = 40
+    z[3, :] = -np.inf
+    z[3, 100] = 3.0                                    # a single finite logit
+    z[4, 7] = 3.0e4                                    # one huge logit, the rest far below it
+    z[5, ::3] = -np.inf
+    raw = f32_to_bf16_bits(z) if dtype == "bf16" else z
+    params = [RowParams(temperature=0.9, top_k=40, top_p=0.95 if b % 2 else 1.0, seed=b, request_id=b)
+              for b in range(B)]
+    wl = Workload("fewfinite", B, V, dtype, raw, [[]] * B, [[]] * B, params)
+    orc = oracle_run(wl, step=2)
+    s, out = _run(wl, step=2)
+    assert s.last_launch_count() == 2  # stream + select only: nothing may stay pending
+    assert_parity(wl, out, orc)
+    assert out["tokens"][3].item() == 100
+
+
 def test_determinism_bit_identical():
     import torch
     wl = make_workload("c4", B=64)
