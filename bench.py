@@ -429,7 +429,8 @@ def main():
                      "peak_source": peak_src, "kernel": "stream_kernel",
                      "algorithmic_bytes_per_launch": algo,
                      "kernel_time_s": kern_s,
-                     "kernel_times_us": ({"stream_kernel": kt[0] * 1e3, "select_rows_kernel": kt[1] * 1e3}
+                     "kernel_times_us": ({n: kt[i] * 1e3 for i, n in
+                                          enumerate(["stream_kernel", "select_rows_kernel", "exact_kernel"][:len(kt)])}
                                          if kt else None),
                      "step_gbs": step_gbs, "step_frac": step_gbs / peak},
         "clocks": clocks,

@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   const bool topk = rc.topk_on && (uint64_t)rc.k < nfin;
   // locate the bucket where a running quantity (count or mass) first reaches target
   auto find_bucket = [&](bool mass, double target, uint64_t ctarget, int limit, int* bucket, double* before) {
-    if (tid == 0) ctl[0] = -1;
+    if (tid == 0) ctl[0] = 0x7FFFFFFF;
     ex_bar();
     double run = mbefore;
     uint32_t crun = cb;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
       crun += tc[j];
     }
     ex_bar();
-    const int bsel = ctl[0] < 0 ? -1 : ctl[0];
+    const int bsel = ctl[0] == 0x7FFFFFFF ? -1 : ctl[0];
     // its prefix: recompute in fixed order from the per-thread values (the owner publishes it)
     ex_bar();
     if (bsel >= 0 && tid == bsel / (kNB0 / kExThreads)) {
