@@ -60,7 +60,8 @@ constexpr int kExOffSideZ = kExOffSideId + kSide * 4;
 constexpr int kExOffCnt = kExOffSideZ + kSide * 4;     // u32 [kNB0] local counts
 constexpr int kExOffMass = kExOffCnt + kNB0 * 4;       // u64 [kNB0] local fixed masses
 constexpr int kExOffGat = kExOffMass + kNB0 * 8;       // u64 [kGat] (leader)
-constexpr int kExOffScr = kExOffGat + kGat * 8;        // scratch: doubles / ints / u64
+constexpr int kExOffWt = kExOffGat + kGat * 8;         // double [kNB0] 2^(-b/64)
+constexpr int kExOffScr = kExOffWt + kNB0 * 8;         // scratch: doubles / ints / u64
 constexpr int kExactSmem = kExOffScr + 2048;
 
 // ---- cluster helpers (a launch without clusters is a cluster of one CTA) ----------------
@@ -79,12 +80,12 @@ __device__ __forceinline__ uint32_t ex_map(const void* p, uint32_t rank) {
 }
 __device__ __forceinline__ uint32_t ex_ld32(uint32_t a) {
   uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a));  // (ordered by cluster barriers)
   return v;
 }
 __device__ __forceinline__ uint64_t ex_ld64(uint32_t a) {
   uint64_t v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void ex_st64(uint32_t a, uint64_t v) {
@@ -251,6 +252,8 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   double* cd = reinterpret_cast<double*>(smem + kExOffScr + 896);     // [16]
   uint64_t* cu = reinterpret_cast<uint64_t*>(smem + kExOffScr + 1024);  // [16]
   double* tots = reinterpret_cast<double*>(smem + kExOffScr + 1152);    // [16] per-CTA draw totals (leader)
+  double* wtab = reinterpret_cast<double*>(smem + kExOffWt);             // [kNB0] bucket top weights
+  for (int b = tid; b < kNB0; b += kExThreads) wtab[b] = exp2(-(double)b / 64.0);
 
   const int slot = a.slots ? a.slots[r] : r;
   const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
@@ -294,6 +297,14 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   }
   // weight coordinates of z: y = (M - z) log2(e)/tau; w = 2^-y; level-0 bucket floor(64 y)
   auto ycoord = [&](float z) -> double { return ((double)M - (double)z) * l2e_tau; };
+  // w = exp((z - M)/tau) = 2^-y = 2^(-b/64) * 2^-(y - b/64): the bucket top from the table, the
+  // rest by its short series (relative error < 3e-15); the far tail (y >= 32) directly
+  auto weight = [&](float z) -> double {
+    const double y = ycoord(z);
+    const int b = (int)(y * 64.0);
+    if (b >= kNB0 - 1) return exp2(-y);
+    return wtab[b] * exp2_neg_small((y - (double)b / 64.0) * kLn2);
+  };
   // one pass over the chunk's elements (coalesced: vector v of thread tid, stride 512)
   auto for_each = [&](auto&& fn) {
     for (int v = v0 + tid; v < v1; v += kExThreads) {
@@ -330,12 +341,22 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   };
   // the cluster's total of bucket b (leader; reads every CTA's histogram over DSMEM)
   auto tot_bucket = [&](int b, uint32_t* cnt, uint64_t* mass) {
+    uint32_t cv[8];
+    uint64_t mv[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)  // (all loads in flight, then the sums in CTA order)
+      if (g < a.G) {
+        cv[g] = ex_ld32(ex_map(hcnt + b, (uint32_t)g));
+        mv[g] = ex_ld64(ex_map(hmass + b, (uint32_t)g));
+      }
     uint32_t c = 0;
     uint64_t m = 0;
-    for (int g = 0; g < a.G; ++g) {
-      c += ex_ld32(ex_map(hcnt + b, (uint32_t)g));
-      m += ex_ld64(ex_map(hmass + b, (uint32_t)g));
-    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (g < a.G) {
+        c += cv[g];
+        m += mv[g];
+      }
     *cnt = c;
     *mass = m;
   };
@@ -529,25 +550,36 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     double pm = before;
     if (rank == 0) {
       ex_sort_desc(gat, n);
-      // walk: thread 0 over the sorted bucket (exact float64 weights, sequential like the oracle)
+      // walk the sorted bucket with exact float64 weights: rounds of 512 entries, block scans in
+      // sorted (= pi) order; the first entry whose cumulative count / mass reaches the target
       if (tid == 0) {
-        double run = before;
-        uint64_t sel = n > 0 ? gat[n - 1] : 0;
-        double selrun = run;
-        for (int i = 0; i < n; ++i) {
-          const double w = exp(((double)comp_val(gat[i]) - (double)M) * inv_tau);
-          run += w;
-          if (mode == 0 ? ((uint64_t)(i + 1) >= need) : (run >= target)) {
-            sel = gat[i];
-            selrun = run;
-            break;
-          }
-          selrun = run;
-        }
-        cu[0] = sel;
-        cd[3] = selrun;
+        ctl[13] = 0x7FFFFFFF;
+        cu[0] = n > 0 ? gat[n - 1] : 0;
+        cd[3] = before;
       }
       ex_bar();
+      double run = before;
+      for (int i0 = 0; i0 < n; i0 += kExThreads) {
+        const int i = i0 + tid;
+        const double w = (i < n) ? weight(comp_val(gat[i])) : 0.0;
+        double rt;
+        const double c = ex_excl_scan_d(w, &rt, sd) + run + w;  // inclusive cumulative of entry i
+        const bool hit = i < n && (mode == 0 ? ((uint64_t)(i + 1) >= need) : (c >= target));
+        if (hit) atomicMin(&ctl[13], i);
+        ex_bar();
+        const int first = ctl[13];
+        if (first != 0x7FFFFFFF) {
+          if (i == first) {
+            cu[0] = gat[i];
+            cd[3] = c;
+          }
+          ex_bar();
+          break;
+        }
+        run += rt;
+        if (tid == 0) cd[3] = run;  // (not reached: the whole bucket's mass)
+        ex_bar();
+      }
       pick = cu[0];
       pm = cd[3];
       // broadcast to every CTA
@@ -629,7 +661,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   //      thread holding u*W walk their elements in id order
   double loc = 0.0;
   for_each([&](float z, int l) {
-    if (make_comp(z, a.voff + l) >= C3) loc += exp(((double)z - (double)M) * inv_tau);
+    if (make_comp(z, a.voff + l) >= C3) loc += weight(z);
   });
   const double ctot = ex_sum_d(loc, sd);
   if (tid == 0) ex_st64(ex_map(tots + rank, 0), __double_as_longlong(ctot));
@@ -684,7 +716,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
 #pragma unroll
         for (int t = 0; t < VEC; ++t) {
           const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + v * VEC + t) >= C3;
-          wl[t] = kept ? exp(((double)z[t] - (double)M) * inv_tau) : 0.0;
+          wl[t] = kept ? weight(z[t]) : 0.0;
           vs += wl[t];
           if (kept) last = v * VEC + t;
         }

@@ -629,7 +629,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
   }
   if (need) {
     // one cluster of G CTAs per row (every row launched; rows that are not pending exit at once):
-    // G = the largest power of two <= 8 with B * G <= 2 CTAs per SM
+    // G = the largest power of two <= 8 with B * G <= 2 resident CTAs per SM (c2: G = 4)
     int G = 1;
     while (G < 8 && (int64_t)B * G * 2 <= 2LL * h->sm_count) G *= 2;
     ExactArgs e{};
