@@ -128,14 +128,16 @@ const char* sampler_last_error(const sampler* h);
 
 /* ---- per-slot state ----------------------------------------------------------------- */
 
-/* SYNC.  Copy n host params into the handle's table at host slot indices slots[0..n).
+/* SYNC.  Waits for all work on the handle's device (an in-flight sample may still read the table),
+ * then copies n host params into the handle's table at host slot indices slots[0..n).
  * Every entry is validated first (EINVAL: temperature < 0 or non-finite, top_p not in
  * (0,1], min_p not in [0,1], repetition_penalty <= 0 in OPENAI_CTRL mode, non-finite
  * penalties, reserved != 0; ERANGE: slot outside [0, B_max)); nothing is written on error. */
 int sampler_set_params(sampler* h, int32_t n, const int32_t* slots_host,
                        const sampling_params* params_host);
 
-/* SYNC.  Admit / evict (SPEC S:187 evict_and_admit): replace slot's history with the given
+/* SYNC.  Waits for all work on the handle's device (an in-flight sample with append may still write
+ * the slot), then admits / evicts (SPEC S:187 evict_and_admit): replaces slot's history with the given
  * host token lists and rebuild its unique-token penalty table from scratch.
  * prompt/output may be NULL when their count is 0.
  * Errors: ERANGE (slot out of range, n_prompt + n_output > L_max, any id outside [0, V)). */

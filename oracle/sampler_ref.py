@@ -43,11 +43,13 @@ ROW_ALL_NEG_INF = 2  # no token has positive weight
 
 GREEDY_EPS = 1e-5    # DESIGN.md R5: tau < 1e-5 (incl. 0) => greedy
 FLAG_EPS = 1e-6      # north star: "within 1e-6 of a CDF or tie boundary" (reported: RowResult.flagged6)
-FLAG_EPS_GPU = 1e-9  # DESIGN.md R16: the excuse band actually applied (RowResult.flagged).  Both sides
-                     # compute kept-set weights and prefix sums in float64 (error <= V * 2^-53 * W,
-                     # < 2e-11 * W for V <= 2e5), so a token may differ only when a boundary lies within
-                     # this band; the north star's 1e-6 is its upper limit, not its value (at 1e-6 a
-                     # 1e5-token nucleus is flagged in ~20% of draws, against the < 1e-4 bar)
+FLAG_EPS_GPU = 1e-10  # DESIGN.md R16: the excuse band actually applied (RowResult.flagged).  Both sides
+                      # compute kept-set weights and prefix sums in float64: this oracle's sequential
+                      # cumsum is within n * 2^-53 * W (< 2.3e-11 W for n <= 2e5 terms) of the exact sum,
+                      # the GPU's bucketed fixed-point masses within 5e-13 W, so a token may differ only
+                      # when a boundary lies within ~2.5e-11 W of it; the band is 4x that.  The north
+                      # star's 1e-6 is its upper limit, not its value (at 1e-6 a 1e5-token nucleus is
+                      # flagged in ~20% of draws, against the < 1e-4 bar; reported as flagged6)
 
 
 @dataclass

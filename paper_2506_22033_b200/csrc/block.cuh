@@ -1,5 +1,5 @@
-// block.cuh — block-wide (CTA) primitives for 256-thread blocks: deterministic reductions,
-// exact radix select of the K-th largest 64-bit composite, compaction and bitonic sort in smem.
+// block.cuh — block-wide (CTA) primitives for 256-thread blocks: deterministic reductions, exact
+// radix select of the K-th largest 64-bit composite and compaction in smem.
 #pragma once
 #include "common.cuh"
 
@@ -19,17 +19,6 @@ struct BlockScratch {
   int* i;        // [kBW + 8]
 };
 
-__device__ __forceinline__ float block_max_f(float v, const BlockScratch& s) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  v = warp_max(v);
-  cbar();
-  if (lane == 0) s.f[w] = v;
-  cbar();
-  float r = s.f[0];
-#pragma unroll
-  for (int j = 1; j < kBW; ++j) r = fmaxf(r, s.f[j]);
-  return r;
-}
 // fixed-order (deterministic) float64 sum
 __device__ __forceinline__ double block_sum_d(double v, const BlockScratch& s) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -51,29 +40,6 @@ __device__ __forceinline__ int block_sum_i(int v, const BlockScratch& s) {
   int r = 0;
 #pragma unroll
   for (int j = 0; j < kBW; ++j) r += s.i[j];
-  return r;
-}
-__device__ __forceinline__ int block_max_i(int v, const BlockScratch& s) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
-  cbar();
-  if (lane == 0) s.i[w] = v;
-  cbar();
-  int r = s.i[0];
-#pragma unroll
-  for (int j = 1; j < kBW; ++j) r = max(r, s.i[j]);
-  return r;
-}
-__device__ __forceinline__ int block_or_i(int v, const BlockScratch& s) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  v = __any_sync(kFull, v) ? 1 : 0;
-  cbar();
-  if (lane == 0) s.i[w] = v;
-  cbar();
-  int r = 0;
-#pragma unroll
-  for (int j = 0; j < kBW; ++j) r |= s.i[j];
   return r;
 }
 __device__ __forceinline__ void block_minmax_u64(uint64_t mn, uint64_t mx, const BlockScratch& s, uint64_t* omn,
@@ -188,88 +154,6 @@ __device__ __forceinline__ int block_compact_ge(uint64_t* buf, int n, uint64_t T
   block_minmax_u64(mn, 0, s, &a, &b);
   *kmin = a;
   return out;
-}
-
-// Sort buf[0..n) (n <= kBT, distinct nonzero values) descending into out[0..n) by rank counting:
-// thread t places buf[t] at the number of entries greater than it.  One pass, one barrier.
-__device__ __forceinline__ void block_rank_sort_desc(const uint64_t* buf, int n, uint64_t* out) {
-  if (threadIdx.x < n) {
-    const uint64_t c = buf[threadIdx.x];
-    int rank = 0;
-    for (int j = 0; j < n; ++j) rank += buf[j] > c;
-    out[rank] = c;
-  }
-  cbar();
-}
-
-// K-th largest (k >= 1) of one binary32 value per thread (-inf = absent; caller guarantees at
-// least k present).  Exact radix select on order-preserving keys, 8-bit digits, early exit.
-// Returns a value T with at least k present values >= T and no present value in [T, kth) .
-__device__ __noinline__ float block_kth_largest_f(float v, int k, uint32_t* hist, const BlockScratch& s) {
-  const bool present = v > -INFINITY;
-  const uint32_t key = present ? f2key(v) : 0u;
-  uint32_t prefix = 0;
-  int need = k;
-  for (int d = 24; d >= 0; d -= 8) {
-    for (int i = threadIdx.x; i < 256; i += kBT) hist[i] = 0;
-    cbar();
-    if (present && (d == 24 || (key >> (d + 8)) == prefix)) atomicAdd(&hist[(key >> d) & 255u], 1u);
-    cbar();
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      uint32_t c8[8];
-      int ls = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c8[j] = hist[255 - 8 * lane - j];
-        ls += (int)c8[j];
-      }
-      const int incl = warp_incl_scan_i(ls, lane);
-      const int excl = incl - ls;
-      if (excl < need && need <= incl) {
-        int acc = excl;
-        for (int j = 0; j < 8; ++j) {
-          if (acc + (int)c8[j] >= need) {
-            s.i[kBW + 0] = 255 - 8 * lane - j;
-            s.i[kBW + 1] = acc;
-            s.i[kBW + 2] = (int)c8[j];
-            break;
-          }
-          acc += (int)c8[j];
-        }
-      }
-    }
-    cbar();
-    const int digit = s.i[kBW + 0], above = s.i[kBW + 1], bincnt = s.i[kBW + 2];
-    cbar();
-    prefix = (prefix << 8) | (uint32_t)digit;
-    need -= above;
-    if (bincnt == need) return key2f(prefix << d);
-  }
-  return key2f(prefix);
-}
-
-// Bitonic sort of buf[0..n) descending (zeros sort last); n <= N (power of two) entries of buf.
-__device__ __forceinline__ void block_sort_desc(uint64_t* buf, int n) {
-  int N = 1;
-  while (N < n) N <<= 1;
-  for (int i = n + threadIdx.x; i < N; i += kBT) buf[i] = 0;
-  cbar();
-  for (int k = 2; k <= N; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < N; i += kBT) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = buf[i], b = buf[ixj];
-          const bool desc = (i & k) == 0;
-          if (desc ? (a < b) : (a > b)) {
-            buf[i] = b;
-            buf[ixj] = a;
-          }
-        }
-      }
-      cbar();
-    }
 }
 
 }  // namespace smp

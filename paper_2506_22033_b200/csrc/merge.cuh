@@ -122,8 +122,7 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
 // kept candidate is accumulated by broadcasting every kept (id, w) once — no sort, no barrier.
 __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, double S, uint64_t F, bool bad,
                                         const RowCfg& rc, const sampling_params& p, uint64_t seed, uint64_t step,
-                                        int row, const RowOut& ro, bool pending_ok, uint64_t* tr,
-                                        bool pre = false, double logS_pre = 0.0, double u_pre = 0.0) {
+                                        int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {
   constexpr int Q = SAMPLER_KCAND_MAX / 32;
   constexpr int UNK = 0x7FFFFFFF;
   const int lane = threadIdx.x & 31;
@@ -140,7 +139,7 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
   for (int q = 0; q < Q; ++q) {
     const int i = lane + 32 * q;
     c[q] = (i < n) ? top[i] : 0ull;
-    w[q] = (i < n && !rc.greedy) ? (pre ? ms.wv[i] : exp(((double)comp_val(c[q]) - (double)M) * inv_tau)) : 0.0;
+    w[q] = (i < n && !rc.greedy) ? exp(((double)comp_val(c[q]) - (double)M) * inv_tau) : 0.0;
   }
   DTR(9);
   int status = SAMPLER_ROW_OK;
@@ -230,7 +229,7 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
         const uint64_t c0 = __shfl_sync(kFull, c[0], 0);
         tok = comp_id(c0);
         W = 1.0;
-        lp = ((double)comp_val(c0) - (double)M) - (pre ? logS_pre : log(S));
+        lp = ((double)comp_val(c0) - (double)M) - log(S);
         flp = 0.0;
       } else {
         // kept set K3 = first n3 of pi; the draw walks it in ascending id order (R10): every
@@ -246,7 +245,7 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
           if (kept) a += w[q];
         }
         W = warp_sum_d(a);
-        const double u = pre ? u_pre : philox_uniform(seed, p.request_id, step);
+        const double u = philox_uniform(seed, p.request_id, step);
         const double target = u * W;
         DTR(12);
         if (n3 <= 32) {
@@ -283,7 +282,7 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
           if (lane + 32 * q < n3 && rk[q] == pick) {
             own = 1;
             tl = id[q];
-            lpl = ((double)comp_val(c[q]) - (double)M) * inv_tau - (pre ? logS_pre : log(S));
+            lpl = ((double)comp_val(c[q]) - (double)M) * inv_tau - log(S);
             flpl = log(w[q] / W);
           }
         const int src = __ffs(__ballot_sync(kFull, own)) - 1;
@@ -405,24 +404,6 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
   uint64_t F = ms.bs.u[0];
   if (U > keff && n > 0) F = ms.top[n - 1] > F ? ms.top[n - 1] : F;
   const bool bad = (ms.bs.i[0] & kRecBad) != 0;
-
-  if (mode == 1) {  // ---- local merge: emit one record
-    uint64_t* oe = reinterpret_cast<uint64_t*>(out_rec + kRecHdrBytes);
-    for (int i = tid; i < n; i += kBT) oe[i] = ms.top[i];
-    if (tid == 0) {
-      RecHdr h;
-      h.m = M;
-      h.flags = bad ? kRecBad : 0u;
-      h.s = S;
-      h.R = (double)M * rc.c_d;
-      h.n = (uint32_t)n;
-      h.rsv = 0;
-      h.frontier = F;
-      *reinterpret_cast<RecHdr*>(out_rec) = h;
-    }
-    cbar();
-    return;
-  }
 
   // ---- final decision (warp 0)
   if (tid < 32) {

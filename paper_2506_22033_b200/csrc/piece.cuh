@@ -148,36 +148,4 @@ __device__ __forceinline__ uint32_t listed_mask(const UniqEntry* e, int n, int g
   return m;
 }
 
-// Bitonic sort of one value per lane, descending across the warp (lane 0 = largest).
-__device__ __forceinline__ uint32_t warp_sort_desc_u32(uint32_t x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t y = __shfl_xor_sync(kFull, x, j);
-      const bool desc = (lane & k) == 0;  // k == 32: the whole warp descending
-      const bool lower = (lane & j) == 0;
-      x = (lower == desc) ? max(x, y) : min(x, y);
-    }
-  return x;
-}
-
-// |{i < n : L[i] >= x}| for a descending list L (binary lifting, n <= 2*top)
-template <int TOP>
-__device__ __forceinline__ int count_ge_desc(const uint32_t* L, int n, uint32_t x) {
-  int pos = 0;
-#pragma unroll
-  for (int st = TOP; st; st >>= 1)
-    if (pos + st <= n && L[pos + st - 1] >= x) pos += st;
-  return pos;
-}
-template <int TOP>
-__device__ __forceinline__ int count_gt_desc(const uint32_t* L, int n, uint32_t x) {
-  int pos = 0;
-#pragma unroll
-  for (int st = TOP; st; st >>= 1)
-    if (pos + st <= n && L[pos + st - 1] > x) pos += st;
-  return pos;
-}
-
 }  // namespace smp

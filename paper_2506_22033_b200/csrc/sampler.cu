@@ -36,17 +36,13 @@ struct sampler {
   SlotMeta* d_meta = nullptr;
   UniqEntry* d_uniq = nullptr;
   int32_t* d_hist = nullptr;
-  uint8_t* d_records = nullptr;
-  int32_t* d_tickets = nullptr;
   RowInfo* d_info = nullptr;
-  float* d_scratch = nullptr;
   uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
   PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
   RowHand* d_hand = nullptr;    // [max_batch] phase A -> B hand-off
   PenEnt* d_pent = nullptr;     // [max_batch][max_history] penalised entries (hand-off)
   uint16_t* d_gkeys = nullptr;  // [max_batch][Vq/4] group keys (phase A -> phase B)
   uint64_t* d_trace = nullptr;
-  int dbg = 0;                  // SAMPLER_DBG development switches (stream.cuh)  // SAMPLER_TRACE=1: per-CTA phase timestamps of the last launch
   // host mirror
   std::vector<sampling_params> h_params;
   std::string err;
@@ -192,14 +188,10 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   h->Vq = vq_of(c.vocab_local, h->vec);
   h->rec_stride = (rec_stride_bytes(c.max_top_k) + 127) / 128 * 128;
   const int64_t B = c.max_batch, L = c.max_history;
-  // records: candidate records (sharded exchange) and one warp record per (warp, row) sub-piece
-  const int64_t nrec = B + 1;
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
             al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
-            al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_records, h->rec_stride * nrec) &&
-            al((void**)&h->d_tickets, sizeof(int32_t) * B) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
-            al((void**)&h->d_scratch, sizeof(float) * B * (int64_t)h->Vp) &&
+            al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
             al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
             al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&
             al((void**)&h->d_hand, sizeof(RowHand) * B) &&  al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
@@ -228,7 +220,6 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
           cudaSuccess ||
       cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
       cudaMemset(h->d_pmask, 0, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) != cudaSuccess ||
-      cudaMemset(h->d_tickets, 0, sizeof(int32_t) * B) != cudaSuccess ||
       cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
       cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kStreamSmem) != cudaSuccess ||
@@ -256,7 +247,6 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
   cudaFuncSetAttribute(exact_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, SMP_CARVEOUT);
 #endif
-  if (getenv("SAMPLER_DBG")) h->dbg = atoi(getenv("SAMPLER_DBG"));
   if (getenv("SAMPLER_TRACE")) {
     if (cudaMalloc((void**)&h->d_trace, sizeof(uint64_t) * (trace_a_len(h) + 32 * (int64_t)B)) != cudaSuccess) h->d_trace = nullptr;
   }
@@ -271,10 +261,7 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_meta);
   cudaFree(h->d_uniq);
   cudaFree(h->d_hist);
-  cudaFree(h->d_records);
-  cudaFree(h->d_tickets);
   cudaFree(h->d_info);
-  cudaFree(h->d_scratch);
   cudaFree(h->d_trace);
   cudaFree(h->d_gkeys);
   cudaFree(h->d_pmask);
@@ -296,6 +283,7 @@ int sampler_set_params(sampler* h, int32_t n, const int32_t* slots, const sampli
     if (e) return fail(h, SAMPLER_EINVAL, "params[%d]: %s", i, e);
   }
   CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaDeviceSynchronize());  // no in-flight sample may still read the table (sampler.h)
   for (int32_t i = 0; i < n; ++i) {
     h->h_params[slots[i]] = params[i];
     CK(h, cudaMemcpy(h->d_params + slots[i], &params[i], sizeof(sampling_params), cudaMemcpyHostToDevice));
@@ -319,6 +307,8 @@ static int upload_slot(sampler* h, int slot, const std::vector<int32_t>& prompt,
   }
   std::vector<int32_t> toks(prompt);
   toks.insert(toks.end(), output.begin(), output.end());
+  CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaDeviceSynchronize());  // no in-flight sample may still append to this slot (sampler.h)
   SlotMeta sm;
   sm.n_prompt = (int32_t)prompt.size();
   sm.n_out = (int32_t)output.size();
@@ -497,7 +487,6 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.pent = h->d_pent;
   a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
-  a.dbg = h->dbg;
   return a;
 }
 
@@ -550,7 +539,6 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.hs = hist_state(h);
   s.parts = h->d_parts;
   s.hand = h->d_hand;
-  s.dbg = h->dbg;
   s.pent = h->d_pent;
   s.gkeys = h->d_gkeys;
   s.ro = ro;

@@ -49,7 +49,6 @@ struct SelectArgs {
   HistState hs;
   const PartRec* parts;    // phase A partial records [B][rpr][kCW]
   const RowHand* hand;     // phase A hand-off [B]
-  int dbg;
   const PenEnt* pent;      // [B][L]
   const uint16_t* gkeys;
   RowOut ro;
@@ -202,9 +201,9 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
 
 // Final decision for one row by the whole block, candidate-parallel (R6-R11; the same
 // rules as merge.cuh warp_decide): candidate i = top[i] (pi order, weight wv[i] = exp((z'-M)/tau)
-// in float64) is owned by thread i.  Every prefix sum is a plain loop in a fixed order (pi order
+// in float64) is owned by thread i.  Every prefix sum is a fixed-order warp scan plus the warp totals (pi order
 // for top-k/top-p, ascending id for the draw), so the arithmetic is the oracle's sequential sums
-// and no warp scan or shuffle sits on the critical path.  Returns the token (-1: not OK).
+// (deterministic).  Returns the token (-1: not OK).
 __device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
                                          uint64_t F, bool bad, const RowCfg& rc, const sampling_params& p,
                                          double u, int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {

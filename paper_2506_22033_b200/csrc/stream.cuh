@@ -93,7 +93,6 @@ struct StreamArgs {
   PenEnt* pent;        // [B][L]
   uint16_t* gkeys;     // [B][gk_stride(Vq)]: group keys | step keys
   uint64_t* trace;     // debug: per-CTA start / end timestamps (globaltimer ns, 64 per CTA), nullable
-  int dbg;             // development switches (SAMPLER_DBG): bit0 no exp-sum, bit1 no keys, bit2 no mask
 };
 
 // ---- packed binary32 pairs (sm_100a FADD2 / FMUL2) ----------------------------------
@@ -281,7 +280,6 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   __syncthreads();
 
   if (w == kCW + 1) {
-    if (a.dbg & 512) return;  // (development: no hand-off)
     // ================= penalty warp: the hand-off of the rows that start in this span =================
     const int64_t rfirst = (s0 + a.spr - 1) / a.spr;
     for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
@@ -351,7 +349,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
             if (++kk == a.spr) { kk = 0; ++rr; }
           }
         }
-        const bool bmcopy = !(a.dbg & 256);
+        constexpr bool bmcopy = true;
         mbar_arrive_expect_tx(full + sl, bytes + (bmcopy ? (uint32_t)n * 128u : 0u));
         uint8_t* dst = ring + sl * (kTileSteps * kStepBytes);
         uint8_t* bdst = reinterpret_cast<uint8_t*>(bm) + sl * (kTileSteps * 128);
@@ -364,10 +362,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
             ++j;
             ++k;
           } while (j < n && k < a.spr);
-          if (a.dbg & 1024)
-            bulk_g2s_nohint(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl);
-          else
-            bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
+          bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
           // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
           if (bmcopy) {
             const int slot = a.slots ? a.slots[r] : r;
@@ -485,7 +480,10 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
         for (;;) {
           float tmax;
           es = GroupMath<T>::esum_tmax(cur4, ls.nm, c2, tmax);
-          gm = (VEC == 8) ? tmax + ls.mref : GroupMath<T>::gmax(cur4);  // bf16: exact
+          // bf16: t = z - m_ref is exact (and so is t + m_ref = z) when |m_ref| < 2^16 |z|; otherwise
+          // (a group far below the reference) the max is taken on the raw values
+          gm = (VEC == 8) ? tmax + ls.mref : GroupMath<T>::gmax(cur4);
+          if (VEC == 8 && !(fabsf(ls.mref) <= 16384.0f * fabsf(gm))) gm = GroupMath<T>::gmax(cur4);
           if (!(gm > ls.thr)) break;
           ls.rebase(gm, c, inv8);
         }

@@ -2,7 +2,7 @@
 compare them with the north-star parity rule:
   * greedy / argmax ids bit-exact
   * stochastic rows: exp(logprob) and q within 1e-5 relative or 1e-6 absolute
-  * token ids identical except in rows the oracle flags (a cutoff or u within FLAG_EPS_GPU = 1e-9 of a
+  * token ids identical except in rows the oracle flags (a cutoff or u within FLAG_EPS_GPU = 1e-10 of a
     boundary, R16; rows within the north star's 1e-6 are counted as flagged6)
 """
 from __future__ import annotations

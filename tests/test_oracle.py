@@ -349,15 +349,15 @@ def _p(**kw):
 
 
 def test_flags_top_p_boundary_both_bands():
-    """SURVEY §8c-10 top-p flag: |c_j - p*W1| <= eps*W1 (or the same for c_{j-1}).  1024 equal
-    logits give w = 1 exactly, so W1 = 1024 and c_j = j + 1 exactly; p = 2^-10 + m*2^-33 is exact in
+    """SURVEY §8c-10 top-p flag: |c_j - p*W1| <= eps*W1 (or the same for c_{j-1}).  2048 equal
+    logits give w = 1 exactly, so W1 = 2048 and c_j = j + 1 exactly; p = 2^-11 + m*2^-34 is exact in
     binary32 and puts p*W1 exactly m*2^-23 above c_0 = 1: the gap is known to the last bit."""
     from oracle.sampler_ref import FLAG_EPS, FLAG_EPS_GPU
-    z = np.zeros(1024, np.float32)
-    for m, f6, fg in ((4, True, True), (4000, True, False), (20000, False, False)):
-        p = 2.0 ** -10 + m * 2.0 ** -33
+    z = np.zeros(2048, np.float32)
+    for m, f6, fg in ((1, True, True), (4000, True, False), (20000, False, False)):
+        p = 2.0 ** -11 + m * 2.0 ** -34
         assert float(np.float32(p)) == p
-        gap = m * 2.0 ** -23 / 1024.0                   # |c_0 - p*W1| / W1
+        gap = m * 2.0 ** -23 / 2048.0                   # |c_0 - p*W1| / W1
         assert (gap <= FLAG_EPS) == f6 and (gap <= FLAG_EPS_GPU) == fg
         r = run(z, _p(temperature=1.0, top_p=p, seed=3), u=0.7)
         assert list(r.kept) == [0, 1]                    # c_0 = 1 < p*W1 <= c_1 = 2
@@ -372,10 +372,10 @@ def test_flags_min_p_boundary_both_bands():
     from oracle.sampler_ref import FLAG_EPS, FLAG_EPS_GPU
     w1 = math.exp(-14.0)
     z = np.array([0.0, -14.0, -30.0], np.float32)
-    for dist, f6, fg in ((4e-10, True, True), (-4e-10, True, True), (5e-7, True, False), (2e-6, False, False)):
+    for dist, f6, fg in ((4e-11, True, True), (-4e-11, True, True), (5e-7, True, False), (2e-6, False, False)):
         mp = float(np.float32(w1 + dist))
         d = abs(w1 - mp)
-        assert abs(d - abs(dist)) < 1e-12
+        assert abs(d - abs(dist)) < 1e-13
         r = run(z, _p(temperature=1.0, min_p=mp, seed=1), u=0.3)
         assert r.flags6["min_p"] == f6 and r.flags["min_p"] == fg, (dist, r.flags6, r.flags)
         assert (1 in r.kept.tolist()) == (w1 >= mp)
@@ -385,7 +385,7 @@ def test_flags_min_p_boundary_both_bands():
 def test_flags_draw_boundary_both_bands():
     """draw flag: |C_tok - u*W| or |C_prev - u*W| <= eps*W, with u passed in explicitly."""
     z = np.array([0.0, 0.0, 0.0, 0.0], np.float32)     # w = 1 each, W = 4, C = 1, 2, 3, 4
-    for du, f6, fg in ((2e-7, True, False), (2e-10, True, True), (-2e-10, True, True), (1e-3, False, False)):
+    for du, f6, fg in ((2e-7, True, False), (2e-11, True, True), (-2e-11, True, True), (1e-3, False, False)):
         u = 0.5 + du                                   # u*W = 2 + 4*du: next to C = 2
         r = run(z, _p(temperature=1.0, seed=1), u=u)
         assert r.flags6["draw"] == f6 and r.flags["draw"] == fg, (du, r.flags6, r.flags)
