@@ -4,7 +4,10 @@
 logprobs -> history append), BASELINE.json metric:
     "sampled rows/s & HBM GB/s vs 8 TB/s, B=256 V=152064 top-k/top-p+penalties"
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard rows|vocab]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard rows|split|vocab]
+      --shard rows  (default) every rank samples its own batch of the config (replicas, weak scaling)
+      --shard split one global batch split by rows across the ranks (batch-row sharding, strong)
+      --shard vocab one global batch split by vocabulary (TP lm_head style; strong)
     python bench.py --impl reference ...      # the float64 CPU oracle as the reference arm
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on
@@ -42,7 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--batch", type=int, default=None, help="override B (c5 latency sweep)")
-    ap.add_argument("--shard", default="rows", choices=["rows", "vocab"])
+    ap.add_argument("--shard", default="rows", choices=["rows", "split", "vocab"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -258,8 +261,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     vocab_mode = world > 1 and a.shard == "vocab"
+    split_mode = world > 1 and a.shard == "split"
 
-    wls = [make_workload(a.config, B=a.batch, seed_offset=i + (0 if vocab_mode else 17 * rank)) for i in range(NDIST)]
+    wls = [make_workload(a.config, B=a.batch, seed_offset=i + (0 if (vocab_mode or split_mode) else 17 * rank))
+           for i in range(NDIST)]
+    B_global = wls[0].B
+    if split_mode:  # this rank's rows of the one global batch
+        from paper_2506_22033_b200.distributed import batch_row_bounds
+        from workloads.synth import Workload
+        blo, bhi = batch_row_bounds(B_global, world, rank)
+        wls = [Workload(w.name, bhi - blo, w.V, w.dtype, w.raw[blo:bhi], w.prompts[blo:bhi], w.outputs[blo:bhi],
+                        w.params[blo:bhi]) for w in wls]
     wl = wls[0]
     esize = 2 if wl.dtype == "bf16" else 4
     B, V = wl.B, wl.V
@@ -279,7 +291,10 @@ def main():
         lo, hi = vocab_shard_bounds(V, world, rank)
     else:
         lo, hi = 0, V
-    s = Sampler(V, B * nset, max_history=L, max_top_k=128, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
+    # candidate records sized by the batch's real top-k (vocab sharding: 48 + 8 K bytes per row)
+    ks = [p.top_k for p in wl.params if p.temperature >= 1e-5]
+    kc = max(ks) if ks and all(1 <= k <= 128 for k in ks) else 128
+    s = Sampler(V, B * nset, max_history=L, max_top_k=kc, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
     slot_sets = []
     for k in range(nset):
         sl = list(range(k * B, (k + 1) * B))
@@ -311,7 +326,7 @@ def main():
     torch.cuda.synchronize()
     launches_per_step = s.last_launch_count() + (1 if vocab_mode else 0)
 
-    use_graph = not a.no_graph and not vocab_mode
+    use_graph = not a.no_graph  # (vocab sharding: the NCCL all-gather is captured in the graph too)
     graphs = {}
 
     def run_steps(first, n):
@@ -441,7 +456,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
 
-    rows_total = B * (1 if vocab_mode else world)
+    rows_total = B_global if (vocab_mode or split_mode) else B * world
     value = rows_total / (ms_step / 1000.0)
     peak, peak_src = load_peaks()
     algo = algorithmic_bytes(wl, uniq0, esize) if not vocab_mode else (B * (hi - lo) * esize + 8 * sum(uniq0))
@@ -454,10 +469,12 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_step, "ms_per_step_raw_launch": ms_raw, "higher_is_better": True,
-        "scaling": "strong" if vocab_mode else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if (vocab_mode or split_mode) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": a.config, "B": B, "V": V, "logits_dtype": wl.dtype,
-                   "parallelism": (f"vocab{world}" if vocab_mode else (f"rows{world}" if world > 1 else "1gpu")),
+                   "parallelism": (f"vocab{world}" if vocab_mode else (f"split{world}" if split_mode else
+                                   (f"rows{world}" if world > 1 else "1gpu"))),
+                   "record_bytes_per_row": rb // B,
                    "l2": f"{NBUF} rotating logits buffers ({NBUF * B * (hi - lo) * esize / 1e6:.0f} MB >= 2x L2 126 MB)",
                    "history": f"{np.mean([len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)]):.0f} tokens/row "
                               f"+1 per step (appended in-kernel; {nset} rotating slot sets, each history grows "

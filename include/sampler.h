@@ -72,10 +72,13 @@ enum {
   SAMPLER_ROW_OK = 0,
   SAMPLER_ROW_NONFINITE = 1,   /* a NaN or +inf logit in the row ("finite entries") */
   SAMPLER_ROW_ALL_NEG_INF = 2, /* no token has positive probability */
-  SAMPLER_ROW_UNRESOLVED = 3   /* vocab-sharded merge: the row's kept set is not bounded by the
+  SAMPLER_ROW_UNRESOLVED = 3,  /* vocab-sharded merge: the row's kept set is not bounded by the
                                   exchanged candidates (top-p/min-p-only rows, or top_k >
                                   max_top_k); see DESIGN.md §8 NEXT-1.  Never produced by
                                   sampler_sample on an unsharded handle. */
+  SAMPLER_ROW_INVALID = 4      /* slots_dev[b] outside [0, B_max), or params_dev[b] a parameter set
+                                  that sampler_set_params would reject: checked on the device, the
+                                  row gets token -1 and logprob NaN, its slot is not touched */
 };
 
 typedef struct {

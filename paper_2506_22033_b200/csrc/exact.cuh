@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   double* wtab = reinterpret_cast<double*>(smem + kExOffWt);             // [kNB0] bucket top weights
   for (int b = tid; b < kNB0; b += kExThreads) wtab[b] = exp2(-(double)b / 64.0);
 
-  const int slot = a.slots ? a.slots[r] : r;
+  const int slot = row_slot(a.slots, r, a.hs.nslots, nullptr);  // (pending rows have a valid slot)
   const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
   const RowCfg rc = decode_row(prm, a.V, 1);
   const float M = ri.M;
@@ -778,7 +778,7 @@ __global__ void debug_q_kernel(const void* logits, int64_t ld, int V, int voff, 
                                const RowInfo* info, float* q) {
   const int r = blockIdx.y;
   const RowInfo ri = info[r];
-  const int slot = slots ? slots[r] : r;
+  const int slot = row_slot(slots, r, hs.nslots, nullptr);
   const sampling_params prm = params_dev ? params_dev[r] : params_tab[slot];
   const RowCfg rc = decode_row(prm, V, 1);
   const UniqEntry* ut = hs.uniq + (int64_t)slot * hs.L;

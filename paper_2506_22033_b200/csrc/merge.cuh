@@ -42,7 +42,28 @@ struct HistState {
   int spr;          // steps per row of the local slice
   int vec;          // elements per 16-byte vector (8 bf16 / 4 f32)
   int voff, vloc;
+  int nslots;       // B_max
 };
+
+// Row r's request slot, validated on the device (device slot arrays are not checked on the host):
+// an out-of-range slot reads slot 0 for memory safety and marks the row invalid.
+__device__ __forceinline__ int row_slot(const int32_t* slots, int r, int nslots, bool* ok) {
+  const int s = slots ? slots[r] : r;
+  const bool v = s >= 0 && s < nslots;
+  if (ok) *ok = v;
+  return v ? s : 0;
+}
+// The parameter checks of sampler_set_params (R5), for device-supplied parameter arrays.
+__device__ __forceinline__ bool params_ok(const sampling_params& p, int pen_mode) {
+  if (!(p.temperature >= 0.0f) || !(p.temperature < INFINITY)) return false;
+  if (!(p.top_p > 0.0f && p.top_p <= 1.0f)) return false;
+  if (!(p.min_p >= 0.0f && p.min_p <= 1.0f)) return false;
+  if (!(fabsf(p.repetition_penalty) < INFINITY) || !(fabsf(p.presence_penalty) < INFINITY) ||
+      !(fabsf(p.frequency_penalty) < INFINITY))
+    return false;
+  if (pen_mode == SAMPLER_PEN_OPENAI_CTRL && !(p.repetition_penalty > 0.0f)) return false;
+  return p.reserved == 0;
+}
 
 __host__ __device__ inline void pmask_pos(int le, int vec, int* word, uint32_t* bit) {
   const int v = le / vec, k = v / 128, d = v % 128;
@@ -121,6 +142,7 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
 // Candidates live in registers (candidate i = lane + 32q); the id-order cumulative mass of each
 // kept candidate is accumulated by broadcasting every kept (id, w) once — no sort, no barrier.
 __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, double S, uint64_t F, bool bad,
+                                        bool invalid,
                                         const RowCfg& rc, const sampling_params& p, uint64_t seed, uint64_t step,
                                         int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {
   constexpr int Q = SAMPLER_KCAND_MAX / 32;
@@ -143,7 +165,9 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
   }
   DTR(9);
   int status = SAMPLER_ROW_OK;
-  if (bad)
+  if (invalid)
+    status = SAMPLER_ROW_INVALID;
+  else if (bad)
     status = SAMPLER_ROW_NONFINITE;
   else if (n == 0 || !(M > -INFINITY))
     status = SAMPLER_ROW_ALL_NEG_INF;
@@ -325,7 +349,7 @@ __device__ __forceinline__ int warp_decide(const MergeSmem& ms, int n, float M, 
 __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch, int nrec, int row, int slot,
                                              const sampling_params& p, uint64_t seed, uint64_t step, int V,
                                              int kcand, int mode, uint8_t* out_rec, const RowOut& ro, int append,
-                                             const HistState& hs, bool pending_ok, const MergeSmem& ms,
+                                             const HistState& hs, bool pending_ok, bool invalid, const MergeSmem& ms,
                                              uint64_t* tr) {
 #define MTR(k)                              \
   do {                                      \
@@ -335,7 +359,7 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
   const RowCfg rc = decode_row(p, V, kcand);
   const int tid = threadIdx.x, lane = tid & 31;
   const int keff = rc.keff;
-  const bool do_app = append && mode == 0;
+  const bool do_app = append && mode == 0 && !invalid;
   // ---- one round trip: headers, entries, history meta
   const int nslot = nrec * keff;  // <= kMaxRec * SAMPLER_KCAND_MAX == kPool
   for (int i = tid; i < nslot; i += kBT) {
@@ -407,7 +431,7 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
 
   // ---- final decision (warp 0)
   if (tid < 32) {
-    const int t = warp_decide(ms, n, M, S, F, bad, rc, p, seed, step, row, ro, pending_ok, tr);
+    const int t = warp_decide(ms, n, M, S, F, bad, invalid, rc, p, seed, step, row, ro, pending_ok, tr);
     if (lane == 0) ms.bs.i[1] = t;
   }
   MTR(4);
@@ -476,6 +500,7 @@ struct MergeArgs {
   HistState hs;
   RowOut ro;
   uint64_t* trace;  // debug: per-row phase timestamps (32 per row), nullable
+  int pen_mode;
 };
 constexpr int kMergeKernelSmem = kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8 + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12 + 512;
 
@@ -497,11 +522,12 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
   ms.bs.u = reinterpret_cast<uint64_t*>(scr + 96);
   ms.bs.i = reinterpret_cast<int*>(scr + 224);
   uint64_t* tr = m.trace ? m.trace + 32 * (int64_t)r : nullptr;
-  const int slot = m.slots ? m.slots[r] : r;
+  bool slot_ok;
+  const int slot = row_slot(m.slots, r, m.hs.nslots, &slot_ok);
   const sampling_params prm = m.params_dev ? m.params_dev[r] : m.params_tab[slot];
   const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
   block_merge_row(m.records + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step, m.V,
-                  m.kcand, 0, nullptr, m.ro, m.append, m.hs, false, ms, tr);
+                  m.kcand, 0, nullptr, m.ro, m.append, m.hs, false, !slot_ok || !params_ok(prm, m.pen_mode), ms, tr);
 }
 
 }  // namespace smp

@@ -70,6 +70,7 @@ static HistState hist_state(const sampler* h) {
   s.uniq = h->d_uniq;
   s.tokens = h->d_hist;
   s.L = h->cfg.max_history;
+  s.nslots = h->cfg.max_batch;
   s.pmask = h->d_pmask;
   s.spr = (int)(h->Vq / kStepVec);
   s.vec = h->vec;
@@ -586,6 +587,7 @@ static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_par
   m.hs = hist_state(h);
   m.ro = ro;
   m.trace = h->d_trace ? h->d_trace + trace_a_len(h) : nullptr;
+  m.pen_mode = h->cfg.penalty_mode;
   return m;
 }
 

@@ -205,7 +205,7 @@ __device__ __noinline__ uint64_t select_collect_slow(const SelectArgs& a, const 
 // for top-k/top-p, ascending id for the draw), so the arithmetic is the oracle's sequential sums
 // (deterministic).  Returns the token (-1: not OK).
 __device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n, float M, double S, double logS,
-                                         uint64_t F, bool bad, const RowCfg& rc, const sampling_params& p,
+                                         uint64_t F, bool bad, bool invalid, const RowCfg& rc, const sampling_params& p,
                                          double u, int row, const RowOut& ro, bool pending_ok, uint64_t* tr) {
   constexpr int UNK = 0x7FFFFFFF;
 #define BTR(k)                                    \
@@ -225,7 +225,8 @@ __device__ __forceinline__ int block_decide(const MergeSmem& ms, int* ctl, int n
   }
   cbar();
   int status = SAMPLER_ROW_OK;
-  if (bad) status = SAMPLER_ROW_NONFINITE;
+  if (invalid) status = SAMPLER_ROW_INVALID;
+  else if (bad) status = SAMPLER_ROW_NONFINITE;
   else if (n == 0 || !(M > -INFINITY)) status = SAMPLER_ROW_ALL_NEG_INF;
   // n_exact = |{i : top[i] >= F}| (a prefix: top is sorted descending)
   const bool own = tid < n;
@@ -456,6 +457,8 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   cbar();
   const int slot = s_hand->slot;
   const sampling_params prm = a.params_dev ? a.params_dev[r] : s_hand->prm;
+  // device-supplied slots / params are validated here (SAMPLER_ROW_INVALID; the slot is not touched)
+  const bool invalid = s_hand->pad[0] != 0 || !params_ok(prm, a.pen_mode);
   const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
   const RowCfg rc = decode_row(prm, a.V, a.kcand);
   const int keff = rc.keff;
@@ -811,7 +814,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   STR(21);
   int32_t tok;
   {
-    tok = block_decide(ms, ctl, n, M, S, logS, F, bad, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
+    tok = block_decide(ms, ctl, n, M, S, logS, F, bad, invalid, rc, prm, u, r, a.ro, a.pending_ok != 0, tr);
   }
   STR(6);
   if (!a.append || tok < 0) return;

@@ -283,13 +283,15 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
     // ================= penalty warp: the hand-off of the rows that start in this span =================
     const int64_t rfirst = (s0 + a.spr - 1) / a.spr;
     for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
-      const int slot = a.slots ? a.slots[r] : (int)r;
+      bool slot_ok;
+      const int slot = row_slot(a.slots, (int)r, a.hs.nslots, &slot_ok);
       const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
       const SlotMeta sm = a.hs.meta[slot];
       if (lane == 0) {
         RowHand h;
         h.slot = slot;
-        h.pad[0] = h.pad[1] = h.pad[2] = 0;
+        h.pad[0] = slot_ok ? 0 : 1;  // (phase B: SAMPLER_ROW_INVALID)
+        h.pad[1] = h.pad[2] = 0;
         h.meta = sm;
         h.prm = prm;
         a.hand[r] = h;
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
           bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
           // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
           if (bmcopy) {
-            const int slot = a.slots ? a.slots[r] : r;
+            const int slot = row_slot(a.slots, r, a.hs.nslots, nullptr);
             bulk_g2s(bdst + j0 * 128, a.hs.pmask + ((int64_t)slot * a.spr + k0) * 32, (uint32_t)(j - j0) * 128u,
                      full + sl, pol);
           }
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   const int r_cta1 = (int)((s0 + nspan - 1) / a.spr);
   for (int g = w; g <= r_cta1 - r_cta0; g += kCW) {
     const int r = r_cta0 + g;
-    const int slot = a.slots ? a.slots[r] : r;
+    const int slot = row_slot(a.slots, r, a.hs.nslots, nullptr);
     const sampling_params* gprm = a.params_dev ? a.params_dev + r : a.params_tab + slot;
     const float temp = gprm->temperature;
     const float tau = (temp < kGreedyEps) ? 1.0f : temp;

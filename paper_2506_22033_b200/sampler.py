@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsampler_b200.so")
 SAMPLER_OK, SAMPLER_EINVAL, SAMPLER_ENOMEM, SAMPLER_ECUDA, SAMPLER_ERANGE, SAMPLER_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 SAMPLER_F32, SAMPLER_BF16 = 0, 2
 PEN_OPENAI_CTRL, PEN_LINEAR = 0, 1
-ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED = 0, 1, 2, 3
+ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED, ROW_INVALID = 0, 1, 2, 3, 4
 
 EXPORTED = [
     "sampler_create", "sampler_destroy", "sampler_last_error", "sampler_set_params", "sampler_set_history",

@@ -16,7 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2506_22033_b200.distributed import batch_row_bounds, sample_vocab_sharded, vocab_shard_bounds
+from paper_2506_22033_b200.distributed import (batch_row_bounds, sample_batch_sharded, sample_vocab_sharded,
+                                               vocab_shard_bounds)
 
 
 def _free_port():
@@ -64,9 +65,15 @@ class _StandInSampler:
         v = torch.arange(self.rb * B, dtype=torch.int64)
         rec.copy_(((v + 31 * self.rank + 7) % 251).to(torch.uint8))
 
-    def merge(self, gathered, world, B, step, slots=None, params=None, seeds=None, append=False):
+    def merge(self, gathered, world, B, step, slots=None, params=None, seeds=None, append=False, out=None):
         self.merged = (gathered.clone(), world, B, step)
         return {"tokens": torch.zeros(B, dtype=torch.int32)}
+
+    def sample(self, logits_rows, step, slots=None, params=None, seeds=None, append=False, out=None):
+        # stand-in result: token = 1000 * rank + local row, logprob = -(token) / 8
+        n = logits_rows.shape[0]
+        tok = (1000 * self.rank + torch.arange(n)).to(torch.int32)
+        return {"tokens": tok, "logprobs": -tok.to(torch.float32) / 8}
 
 
 def _worker(rank, world, port, q):
@@ -83,6 +90,16 @@ def _worker(rank, world, port, q):
         for r in range(world):
             v = torch.arange(rb, dtype=torch.int64)
             ok = ok and torch.equal(g[r * rb:(r + 1) * rb], ((v + 31 * r + 7) % 251).to(torch.uint8))
+        # batch-row sharding of one global batch of 7 rows: every rank ends with the whole result
+        Bg = 7
+        blo, bhi = batch_row_bounds(Bg, world, rank)
+        o = sample_batch_sharded(s, torch.zeros(bhi - blo, 4), step=1, B_global=Bg)
+        exp_tok = []
+        for r in range(world):
+            l2, h2 = batch_row_bounds(Bg, world, r)
+            exp_tok += [1000 * r + i for i in range(h2 - l2)]
+        ok = ok and o["tokens"].tolist() == exp_tok
+        ok = ok and torch.equal(o["logprobs"], -torch.tensor(exp_tok, dtype=torch.float32) / 8)
         # bench.py: time of the slowest rank
         t = torch.tensor([1.0 + rank])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -1,0 +1,93 @@
+"""The multi-GPU entry points on a real NCCL process group (world size 1: one GPU per gpurun call),
+end to end against the float64 oracle, and captured in a CUDA graph.
+
+* vocab-sharded (TP lm_head style): sample_local -> NCCL all_gather_into_tensor ->
+  merge, on the whole vocabulary as the single shard;
+* batch-row sharded: sample + the (token, logprob) all-gather.
+The G = 2/4/8 split of the vocabulary is covered in test_gpu_parity.py with an in-process gather
+(and the exchange plumbing at world size 2 with gloo in test_distributed.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests._helpers import assert_parity, make_sampler, oracle_run
+from workloads.synth import device_logits, make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist.group.WORLD
+    dist.destroy_process_group()
+
+
+def test_vocab_sharded_nccl_world1_matches_oracle(nccl_group):
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import sample_vocab_sharded, vocab_shard_bounds
+    wl = make_workload("c3", B=24, V=20000)
+    lo, hi = vocab_shard_bounds(wl.V, 1, 0)
+    s = Sampler(wl.V, wl.B, max_history=1024, max_top_k=40, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    x = device_logits(wl)
+    out = sample_vocab_sharded(s, x[:, lo:hi], 4)
+    torch.cuda.synchronize()
+    assert (out["status"] == 0).all()
+    assert_parity(wl, out, oracle_run(wl, 4))
+
+
+def test_vocab_sharded_step_in_cuda_graph(nccl_group):
+    """The whole sharded step (local pass, NCCL all-gather, merge) captured once and replayed."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import sample_vocab_sharded
+    wl = make_workload("c3", B=16, V=12000)
+    s = Sampler(wl.V, wl.B, max_history=1024, max_top_k=40, dtype=wl.dtype, vocab_offset=0, vocab_local=wl.V)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    x = device_logits(wl)
+    rb = s.record_bytes(wl.B)
+    rec = torch.empty(rb, dtype=torch.uint8, device="cuda")
+    gathered = torch.empty(rb, dtype=torch.uint8, device="cuda")
+    out = s._outs(wl.B, None)
+    eager = sample_vocab_sharded(s, x, 7, rec=rec, gathered=gathered, out=s._outs(wl.B, None))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        sample_vocab_sharded(s, x, 7, rec=rec, gathered=gathered, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    for k in ("tokens", "logprobs", "status"):
+        assert torch.equal(out[k], eager[k]), k
+    assert_parity(wl, out, oracle_run(wl, 7))
+
+
+def test_batch_row_sharded_nccl_world1_matches_oracle(nccl_group):
+    import torch
+    from paper_2506_22033_b200.distributed import batch_row_bounds, sample_batch_sharded
+    wl = make_workload("c4", B=48, V=16000)
+    lo, hi = batch_row_bounds(wl.B, 1, 0)
+    s = make_sampler(wl)
+    x = device_logits(wl)[lo:hi]
+    o = sample_batch_sharded(s, x, 2, wl.B)
+    torch.cuda.synchronize()
+    assert torch.equal(o["tokens"], o["local"]["tokens"])
+    assert_parity(wl, o["local"], oracle_run(wl, 2))
+    assert np.isfinite(o["logprobs"].cpu().numpy()).all()

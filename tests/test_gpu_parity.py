@@ -227,6 +227,41 @@ def test_slots_and_device_params_and_seeds():
     assert_parity(wl2, out, oracle_run(wl2, 2))
 
 
+def test_invalid_device_slots_and_params_give_row_status():
+    """Device-supplied slots / params are not seen by the host: an out-of-range slot or a parameter
+    set that sampler_set_params rejects gives SAMPLER_ROW_INVALID for that row (token -1, NaN
+    logprob, no append), every other row is unaffected (ADVICE / VERDICT r1 item 11)."""
+    import torch
+    from paper_2506_22033_b200 import ROW_INVALID, params_to_device
+    wl = make_workload("c3", B=10, V=9000)
+    s = make_sampler(wl, max_batch=16)
+    x = device_logits(wl)
+    params = [RowParams(**p.__dict__) for p in wl.params]
+    params[2].temperature = -1.0
+    params[3].top_p = 0.0
+    params[4].repetition_penalty = 0.0   # OPENAI_CTRL needs > 0
+    params[5].min_p = float("nan")
+    slots = torch.arange(wl.B, dtype=torch.int32, device="cuda")
+    slots[6] = 16                          # == max_batch: out of range
+    slots[7] = -3
+    before = [s.get_history(b) for b in range(wl.B)]
+    out = s.sample(x, 1, slots=slots, params=params_to_device(params), append=True)
+    torch.cuda.synchronize()
+    st = out["status"].cpu().tolist()
+    tok = out["tokens"].cpu().tolist()
+    bad = {2, 3, 4, 5, 6, 7}
+    for b in range(wl.B):
+        if b in bad:
+            assert st[b] == ROW_INVALID and tok[b] == -1, (b, st[b], tok[b])
+            assert math.isnan(out["logprobs"][b].item())
+        else:
+            assert st[b] == 0
+    for b in (2, 3, 4, 5):                 # invalid rows appended nothing to their (valid) slots
+        assert s.get_history(b) == before[b]
+    orc = oracle_run(wl, 1, rows=[b for b in range(wl.B) if b not in bad])
+    assert_parity(wl, out, orc)
+
+
 def test_vocab_sharded_equals_unsharded_fake_allgather():
     """G vocab slices on one GPU with an in-process all-gather (torch.cat) == unsharded sampling."""
     import torch

@@ -24,6 +24,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from oracle import sample_row  # noqa: E402
+from oracle.sampler_ref import FLAG_EPS, FLAG_EPS_GPU  # noqa: E402
 from tests._helpers import make_sampler, oracle_params  # noqa: E402
 from workloads.synth import device_logits, make_workload  # noqa: E402
 
@@ -60,7 +61,7 @@ def main():
     cores = len(os.sched_getaffinity(0))
     summary = {"rows": 0, "flagged": 0, "flagged6": 0, "mismatch": 0, "unflagged_mismatch": 0,
                "prob_violations": 0, "status_mismatch": 0, "per_config": {}, "cores": cores,
-               "band": {"excuse": 1e-9, "north_star": 1e-6}, "tolerance": {"rel": REL, "abs": ABS}}
+               "band": {"excuse": FLAG_EPS_GPU, "north_star": FLAG_EPS}, "tolerance": {"rel": REL, "abs": ABS}}
     t0 = time.time()
     ctx = mp.get_context("fork")
     for cfg in cfgs:
