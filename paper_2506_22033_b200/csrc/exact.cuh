@@ -60,9 +60,43 @@ constexpr int kExOffSideZ = kExOffSideId + kSide * 4;
 constexpr int kExOffCnt = kExOffSideZ + kSide * 4;     // u32 [kNB0] local counts
 constexpr int kExOffMass = kExOffCnt + kNB0 * 4;       // u64 [kNB0] local fixed masses
 constexpr int kExOffGat = kExOffMass + kNB0 * 8;       // u64 [kGat] (leader)
-constexpr int kExOffWt = kExOffGat + kGat * 8;         // double [kNB0] 2^(-b/64)
-constexpr int kExOffScr = kExOffWt + kNB0 * 8;         // scratch: doubles / ints / u64
-constexpr int kExactSmem = kExOffScr + 2048;
+constexpr int kExOffWt = kExOffGat + kGat * 8;         // double [64] 2^(-j/64)
+constexpr int kPmBlocks = 132;                         // presence-bitmap blocks (128 vectors) staged
+constexpr int kExOffPm = kExOffWt + 64 * 8;            // u32 [kPmBlocks * 32] the chunk's bitmap
+constexpr int kExOffScr = kExOffPm + kPmBlocks * 128;  // scratch: doubles / ints / u64
+constexpr int kExOffKh = kExOffScr + 2048;             // bf16 rows: u16 counts per 16-bit value key [65536]
+constexpr int kExactSmem = kExOffKh;                   // f32 rows
+constexpr int kExactSmemBf16 = kExOffKh + 65536 * 2;   // bf16 rows
+constexpr int kKhMaxChunk = 65535;                     // (u16 counts: chunks of at most this many elements)
+
+#ifdef EXACT_PROF  // development timing marks (separate build: tools/exact_marks.sh)
+__device__ uint64_t g_exprof[3][8][24];
+#define EXPROF(i)                                                           \
+  do {                                                                      \
+    if (tid == 0 && r < 3) {                                                \
+      uint64_t t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      g_exprof[r][rank][i] = t_;                                            \
+      if (i == 15)                                                          \
+        for (int j_ = 1; j_ < 24; ++j_)                                     \
+          printf("EXPROF r%d c%d m%d %llu\n", r, (int)rank, j_,             \
+                 (unsigned long long)g_exprof[r][rank][j_]);                \
+    }                                                                       \
+  } while (0)
+#else
+#define EXPROF(i) \
+  do {            \
+  } while (0)
+#endif
+
+#ifdef EXACT_STOP  // development: leave after stage i (timing of the stages; results invalid)
+#define EXSTOP(i) \
+  if (EXACT_STOP == i) return
+#define EXACT_STOP_ON(i) (EXACT_STOP == i)
+#else
+#define EXSTOP(i)
+#define EXACT_STOP_ON(i) false
+#endif
 
 // ---- cluster helpers (a launch without clusters is a cluster of one CTA) ----------------
 __device__ __forceinline__ uint32_t ex_rank() {
@@ -107,9 +141,21 @@ __device__ __forceinline__ void smem_add_u64(uint64_t* p, uint64_t v) {
   if (up) atomicAdd(p32 + 1, up);
 }
 
+// 2^x by the library (out of line: the rare far-tail / table paths; keeps the kernel's code small)
+__device__ __noinline__ double ex_exp2(double x) { return exp2(x); }
+
 // 2^-s for s in [0, ln2/64) via its series in s*ln2 (relative error < 3e-15)
 __device__ __forceinline__ double exp2_neg_small(double d) {  // d = s * ln2 in [0, 0.0109)
   return 1.0 - d * (1.0 - d * (0.5 - d * (1.0 / 6.0 - d * (1.0 / 24.0 - d * (1.0 / 120.0)))));
+}
+
+// w = 2^-y = 2^(-b/64) * 2^-(y - b/64), b = floor(64 y): the bucket top from the 64-entry table
+// 2^(-j/64) and an exact power of two, the rest by its short series; the far tail (y >= 32) by the
+// library.  Out of line: called per element only off the hot loops (those use per-value tables).
+__device__ __noinline__ double ex_weight(double y, const double* wtab) {
+  const int b = (int)(y * 64.0);
+  if (b >= kNB0 - 1) return exp2(-y);
+  return wtab[b & 63] * __hiloint2double((1023 - (b >> 6)) << 20, 0) * exp2_neg_small((y - (double)b / 64.0) * kLn2);
 }
 
 // block-wide fixed-order sums / scans (512 threads)
@@ -178,12 +224,20 @@ __device__ void ex_sort_desc(uint64_t* buf, int n) {
     }
 }
 
+// order-preserving 16-bit key of a bf16 value (its bits) and back
+__device__ __forceinline__ uint32_t okey_of_bits(uint32_t h) { return h ^ ((h & 0x8000u) ? 0xFFFFu : 0x8000u); }
+__device__ __forceinline__ float val_of_okey(uint32_t k) {
+  const uint32_t h = k ^ ((k & 0x8000u) ? 0x8000u : 0xFFFFu);
+  return __uint_as_float(h << 16);
+}
+
 // the row as seen by one CTA: z' of local id l (penalties applied), element iteration by vectors
 template <typename T>
 struct ExRow {
   static constexpr int VEC = Dec<T>::N;
   const uint8_t* rowp;      // local slice of the row
-  const uint32_t* pm;       // the slot's presence bitmap (phase A step-lane layout)
+  const uint32_t* pm;       // the slot's presence bitmap (phase A step-lane layout) from block kb
+  int kb;
   const int* side_id;       // sorted local ids of the chunk's penalised elements
   const float* side_z;
   int nside;                // entries in smem (if ovf: the chunk's penalised ids come from the table)
@@ -195,10 +249,10 @@ struct ExRow {
   int pen_mode;
   // penalised bits of vector v (VEC elements at local id v*VEC)
   __device__ __forceinline__ uint32_t pbits(int v) const {
-    const int k = v >> 7, d = v & 127;
+    const int k = (v >> 7) - kb, d = v & 127;
     return (pm[k * 32 + (d & 31)] >> ((d >> 5) * VEC)) & ((1u << VEC) - 1u);
   }
-  __device__ __forceinline__ float pen_value(int l) const {
+  __device__ __noinline__ float pen_value(int l) const {  // (rare: penalised elements only)
     if (!ovf) {
       int lo = 0, hi = nside;
       while (lo < hi) {
@@ -218,8 +272,8 @@ struct ExRow {
     return apply_penalty(Dec<T>::load1(rowp, l), ut[lo].meta, prm, pen_mode);
   }
   // the VEC values z' of vector v (-inf past the slice end)
-  __device__ __forceinline__ void vec(int v, float (&z)[Dec<T>::N]) const {
-    const uint4 u = *reinterpret_cast<const uint4*>(rowp + (int64_t)v * 16);
+  __device__ __forceinline__ uint4 ld(int v) const { return *reinterpret_cast<const uint4*>(rowp + (int64_t)v * 16); }
+  __device__ __forceinline__ void vec(int v, const uint4 u, float (&z)[Dec<T>::N]) const {
     const uint32_t pb = pbits(v);
 #pragma unroll
     for (int t = 0; t < VEC; ++t) {
@@ -252,8 +306,8 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   double* cd = reinterpret_cast<double*>(smem + kExOffScr + 896);     // [16]
   uint64_t* cu = reinterpret_cast<uint64_t*>(smem + kExOffScr + 1024);  // [16]
   double* tots = reinterpret_cast<double*>(smem + kExOffScr + 1152);    // [16] per-CTA draw totals (leader)
-  double* wtab = reinterpret_cast<double*>(smem + kExOffWt);             // [kNB0] bucket top weights
-  for (int b = tid; b < kNB0; b += kExThreads) wtab[b] = exp2(-(double)b / 64.0);
+  double* wtab = reinterpret_cast<double*>(smem + kExOffWt);             // [64] 2^(-j/64)
+  if (tid < 64) wtab[tid] = exp2(-(double)tid / 64.0);
 
   const int slot = row_slot(a.slots, r, a.hs.nslots, nullptr);  // (pending rows have a valid slot)
   const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
@@ -265,6 +319,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   ExRow<T> R;
   R.rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * sizeof(T);
   R.pm = a.hs.pmask + (int64_t)slot * a.hs.spr * 32;
+  R.kb = 0;
   R.side_id = side_id;
   R.side_z = side_z;
   R.ut = a.hs.uniq + (int64_t)slot * a.hs.L;
@@ -276,7 +331,17 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   R.prm = prm;
   R.pen_mode = a.pen_mode;
   const int v0 = R.c0 / VEC, v1 = (R.c1 + VEC - 1) / VEC;  // vectors of the chunk
+  {  // the chunk's presence bitmap into smem (one coalesced copy; every pass reads it per vector)
+    const int kb = v0 >> 7, nb = v1 > v0 ? ((v1 - 1) >> 7) - kb + 1 : 0;
+    if (nb <= kPmBlocks) {
+      uint32_t* pms = reinterpret_cast<uint32_t*>(smem + kExOffPm);
+      for (int i = tid; i < nb * 32; i += kExThreads) pms[i] = R.pm[(int64_t)kb * 32 + i];
+      R.pm = pms;
+      R.kb = kb;
+    }
+  }
 
+  EXPROF(1);
   // ---- the chunk's penalised elements: their table entries are contiguous (sorted by id)
   {
     int below = 0, inside = 0;
@@ -299,22 +364,58 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   auto ycoord = [&](float z) -> double { return ((double)M - (double)z) * l2e_tau; };
   // w = exp((z - M)/tau) = 2^-y = 2^(-b/64) * 2^-(y - b/64): the bucket top from the table, the
   // rest by its short series (relative error < 3e-15); the far tail (y >= 32) directly
-  auto weight = [&](float z) -> double {
-    const double y = ycoord(z);
-    const int b = (int)(y * 64.0);
-    if (b >= kNB0 - 1) return exp2(-y);
-    return wtab[b] * exp2_neg_small((y - (double)b / 64.0) * kLn2);
+  auto weight = [&](float z) -> double { return ex_weight(ycoord(z), wtab); };
+  // one pass over the chunk's vectors (coalesced: vector v of thread tid, stride 512), the loads
+  // of 4 vectors issued together (the passes are latency-bound otherwise)
+  auto for_vecs = [&](auto&& fn) {
+    constexpr int U = 4;
+    for (int v = v0 + tid; v < v1; v += U * kExThreads) {
+      uint4 u[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (v + j * kExThreads < v1) u[j] = R.ld(v + j * kExThreads);
+      // (one copy of the body: the vectors picked by selects, not an unrolled loop - code size)
+#pragma unroll 1
+      for (int j = 0; j < U; ++j) {
+        if (v + j * kExThreads >= v1) break;
+        const uint4 uj = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
+        fn(v + j * kExThreads, uj);
+      }
+    }
   };
-  // one pass over the chunk's elements (coalesced: vector v of thread tid, stride 512)
   auto for_each = [&](auto&& fn) {
-    for (int v = v0 + tid; v < v1; v += kExThreads) {
+    for_vecs([&](int v, const uint4 u) {
       float z[VEC];
-      R.vec(v, z);
+      R.vec(v, u, z);
 #pragma unroll
       for (int t = 0; t < VEC; ++t)
         if (z[t] > -INFINITY) fn(z[t], v * VEC + t);
-    }
+    });
   };
+  // bf16 rows (and the chunk's penalised ids in smem): pass 1 is an integer count histogram over the
+  // 65 536 value keys; every float64 quantity is then computed once per distinct value (count x
+  // weight), not per element.  (f32 rows, or more penalised ids than fit in smem: per element.)
+  const bool keyed = (VEC == 8) && !R.ovf && (R.c1 - R.c0) <= kKhMaxChunk;
+  uint32_t* kh = reinterpret_cast<uint32_t*>(smem + kExOffKh);  // [32768] pairs of u16 counts
+  auto kcount = [&](uint32_t k) -> uint32_t { return (kh[k >> 1] >> ((k & 1u) * 16)) & 0xFFFFu; };
+  // y and the level-0 bucket of a value (the same float64 arithmetic everywhere: consistent)
+  auto bucket0 = [&](float z, double* yout) -> int {
+    const double y = ycoord(z);
+    *yout = y;
+    if (!(y >= 0.0)) return -1;
+    const double q = y * 64.0;
+    return q >= (double)(kNB0 - 1) ? kNB0 - 1 : (int)q;
+  };
+  auto add_bucket = [&](float z, uint32_t c) {
+    if (c == 0 || !(z > -INFINITY)) return;  // (-inf, NaN)
+    double y;
+    const int b = bucket0(z, &y);
+    if (b < 0) return;
+    const double rel = (b == kNB0 - 1) ? ex_exp2(-(y - (double)b / 64.0)) : exp2_neg_small((y - (double)b / 64.0) * kLn2);
+    atomicAdd(&hcnt[b], c);
+    smem_add_u64(&hmass[b], (uint64_t)c * (uint64_t)(rel * kFix40 + 0.5));
+  };
+
   // histogram of a level: bucket(y) in [0, nb) for y in [ybase, ybase + nb / scale), masses
   // relative to the bucket top 2^-(ybase + b/scale)
   auto histogram = [&](double ybase, double scale, int nb) {
@@ -333,7 +434,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
         else return;
       }
       const double d = (y - ybase - (double)b / scale) * kLn2;  // >= 0
-      const double rel = (b == nb - 1 && nb == kNB0) ? exp2(-(y - ybase - (double)b / scale)) : exp2_neg_small(d);
+      const double rel = (b == nb - 1 && nb == kNB0) ? ex_exp2(-(y - ybase - (double)b / scale)) : exp2_neg_small(d);
       atomicAdd(&hcnt[b], 1u);
       smem_add_u64(&hmass[b], (uint64_t)(rel * kFix40 + 0.5));
     });
@@ -363,6 +464,62 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   // gather the composites of every element of bucket b (level given) into the leader's buffer
   auto gather = [&](double ybase, double scale, int nb, int b) {
     const uint32_t cnt_addr = ex_map(ctl + 20, 0);
+    if (keyed && nb == kNB0) {
+      // the bucket is a contiguous range of value keys (the bucket is monotone in the value):
+      // its ends by bisection with the same float64 arithmetic, then an integer test per element
+      // P(k) = bucket(k) > b and Q(k) = bucket(k) >= b are true-then-false over the keys from -max
+      // (0x80) up: klo = first key with !P, khi = first key with !Q.  Two rounds of a 512-way search.
+      {
+        double y;
+        const uint32_t ks = 0x80u + (uint32_t)tid * 128u;  // samples 0x80 + 128 t
+        const int bs = bucket0(val_of_okey(ks), &y);
+        const int np = __syncthreads_count(bs >= 0 && bs > b);   // samples with P (a prefix)
+        const int nq = __syncthreads_count(bs >= 0 && bs >= b);  // samples with Q
+        // the first !P key lies in (sample np-1, sample np]: threads 0..127 test its 128 keys
+        const uint32_t pb0 = np > 0 ? 0x80u + (uint32_t)(np - 1) * 128u + 1u : 0x80u;
+        const uint32_t qb0 = nq > 0 ? 0x80u + (uint32_t)(nq - 1) * 128u + 1u : 0x80u;
+        const uint32_t kk = (tid < 128 ? pb0 : qb0) + (uint32_t)(tid & 127);
+        const int bk2 = (tid < 256 && kk < 65536u) ? bucket0(val_of_okey(kk), &y) : -1;
+        const bool pt = tid < 128 && kk < 65536u && bk2 >= 0 && bk2 > b;
+        const bool qt = tid >= 128 && tid < 256 && kk < 65536u && bk2 >= 0 && bk2 >= b;
+        const int cp = __syncthreads_count(pt), cq = __syncthreads_count(qt);
+        if (tid == 0) {
+          ctl[24] = (int)min(65536u, np > 0 ? pb0 + (uint32_t)cp : 0x80u);
+          ctl[25] = (int)min(65536u, nq > 0 ? qb0 + (uint32_t)cq : 0x80u);
+        }
+        ex_bar();
+      }
+      const uint32_t klo = (uint32_t)ctl[24], khi = (uint32_t)ctl[25];  // keys [klo, khi)
+      for_vecs([&](int v, const uint4 u) {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        uint32_t hit = 0;  // elements of the vector in [klo, khi)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const uint32_t h = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+          hit |= (okey_of_bits(h) - klo < khi - klo ? 1u : 0u) << t;  // (unsigned range test)
+        }
+        if (!hit) return;
+        hit &= ~R.pbits(v);  // (penalised: from the side list)
+        while (hit) {
+          const int t = __ffs(hit) - 1;
+          hit &= hit - 1;
+          const int l = v * 8 + t;
+          if (l >= R.c1) break;
+          const uint32_t h = (w[t >> 1] >> ((t & 1) * 16)) & 0xFFFFu;
+          const uint32_t at = ex_atom_add(cnt_addr, 1u);
+          if (at < (uint32_t)kGat) ex_st64(ex_map(gat + at, 0), make_comp(__uint_as_float(h << 16), a.voff + l));
+        }
+      });
+      for (int e = tid; e < R.nside; e += kExThreads) {
+        double y;
+        const float z = side_z[e];
+        if (z > -INFINITY && bucket0(z, &y) == b) {
+          const uint32_t at = ex_atom_add(cnt_addr, 1u);
+          if (at < (uint32_t)kGat) ex_st64(ex_map(gat + at, 0), make_comp(z, a.voff + side_id[e]));
+        }
+      }
+      return;
+    }
     for_each([&](float z, int l) {
       const double q = (ycoord(z) - ybase) * scale;
       if (!(q >= 0.0)) return;
@@ -378,9 +535,62 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   };
 
   ex_csync();  // every CTA's side list is built; the cluster is resident
+  EXPROF(2);
+  EXSTOP(2);
   // ---- pass 1: level-0 histograms; the leader sums the cluster's and finds the cutoffs
-  histogram(0.0, 64.0, kNB0);
+  if (keyed) {
+    for (int i = tid; i < 32768; i += kExThreads) kh[i] = 0;
+    for (int i = tid; i < kNB0; i += kExThreads) {
+      hcnt[i] = 0;
+      hmass[i] = 0;
+    }
+    ex_bar();
+    EXPROF(19);
+    // every element of the chunk's whole vectors counted by its raw value key (one shared atomic
+    // each, no per-element tests); then the penalised ones moved to their z' (side list) and the
+    // ragged tail of the last chunk counted; -inf / NaN keys are skipped when the keys are read
+    const int vfull = R.c1 / 8;
+    for (int v = v0 + tid; v < vfull; v += 4 * kExThreads) {
+      uint4 u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (v + j * kExThreads < vfull) u[j] = R.ld(v + j * kExThreads);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (v + j * kExThreads < vfull) {
+          const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t k = okey_of_bits((t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu));
+            atomicAdd(&kh[k >> 1], 1u << ((k & 1u) * 16));
+          }
+        }
+    }
+    if (tid < 8 && vfull * 8 + tid < R.c1) {  // the ragged tail (past the last whole vector)
+      const uint32_t k = okey_of_bits(__float_as_uint(Dec<T>::load1(R.rowp, vfull * 8 + tid)) >> 16);
+      atomicAdd(&kh[k >> 1], 1u << ((k & 1u) * 16));
+    }
+    ex_bar();
+    for (int e = tid; e < R.nside; e += kExThreads) {  // penalised: out of the raw keys
+      const uint32_t k = okey_of_bits(__float_as_uint(Dec<T>::load1(R.rowp, side_id[e])) >> 16);
+      atomicSub(&kh[k >> 1], 1u << ((k & 1u) * 16));
+    }
+    ex_bar();
+    EXPROF(20);
+    for (int i = tid; i < 32768; i += kExThreads) {
+      const uint32_t w = kh[i];
+      if (!w) continue;
+      add_bucket(val_of_okey(2u * i), w & 0xFFFFu);
+      add_bucket(val_of_okey(2u * i + 1u), w >> 16);
+    }
+    for (int e = tid; e < R.nside; e += kExThreads) add_bucket(side_z[e], 1u);
+    ex_bar();
+  } else {
+    histogram(0.0, 64.0, kNB0);
+  }
   ex_csync();
+  EXPROF(3);
+  EXSTOP(3);
   // level-0 totals per bucket, in the leader; every CTA reads them (fixed order, deterministic)
   uint32_t tc[kNB0 / kExThreads];
   double tm[kNB0 / kExThreads];
@@ -388,9 +598,11 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     const int b = tid * (kNB0 / kExThreads) + j;  // thread owns 4 consecutive buckets
     uint64_t m;
     tot_bucket(b, &tc[j], &m);
-    tm[j] = (double)m * (1.0 / kFix40) * exp2(-(double)b / 64.0);
+    tm[j] = (double)m * (1.0 / kFix40) * ex_exp2(-(double)b / 64.0);
   }
   ex_csync();  // (every CTA has read every histogram; they may be reused)
+  EXPROF(4);
+  EXSTOP(4);
 
   // cutoffs as composites: K = { composite >= C }
   uint64_t Ck = 0, Cp = 0, Cm = 0;
@@ -467,11 +679,13 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     ex_csync();
     gather(0.0, 64.0, kNB0, b0);
     ex_csync();
+  EXPROF(5);
     if (ctl[20] == 0 || rank != 0) {
       // (non-leaders only help gather)
     }
     int n = (int)ex_ld32(ex_map(ctl + 20, 0));
     ex_csync();
+  EXPROF(6);
     if (n > kGat) {  // too large: one more level inside bucket b0
       level = 1;
       histogram(ybase, scale, kNB1);
@@ -483,9 +697,10 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
         const int b = tid * (kNB1 / kExThreads) + j;
         uint64_t m;
         tot_bucket(b, &sc[j], &m);
-        sm[j] = (double)m * (1.0 / kFix40) * exp2(-(ybase + (double)b / scale));
+        sm[j] = (double)m * (1.0 / kFix40) * ex_exp2(-(ybase + (double)b / scale));
       }
       ex_csync();
+  EXPROF(7);
       double l_m = 0.0;
       uint32_t l_c = 0;
       for (int j = 0; j < kNB1 / kExThreads; ++j) {
@@ -544,6 +759,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
       ex_csync();
       n = (int)ex_ld32(ex_map(ctl + 20, 0));
       ex_csync();
+  EXPROF(8);
     }
     n = min(n, kGat);  // (beyond: a pathological tie mass; the first kGat are kept)
     uint64_t pick = 0;
@@ -591,6 +807,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     }
     (void)level;
     ex_csync();
+  EXPROF(9);
     pick = cu[0];
     pm = cd[3];
     *prefix_mass = pm;
@@ -598,6 +815,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   };
 
   // ---- top-k (count) cutoff, then W1 = mass of K1
+  EXPROF(10);
   int bk = kNB0;
   if (topk) {
     double bf;
@@ -629,6 +847,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     W1 = mtot;
   }
   // ---- top-p cutoff over K1 (renormalised, R7; >= p W1, R8)
+  EXPROF(11);
   if (rc.top_p < 1.0f) {
     const double target = (double)rc.top_p * W1;
     int bp;
@@ -658,14 +877,63 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   C3 = Cm > C3 ? Cm : C3;
 
   // ---- the draw: W = mass of K3 in id order; per-CTA totals -> cluster prefix -> the CTA and the
+  EXPROF(12);
+  EXSTOP(12);
   //      thread holding u*W walk their elements in id order
   double loc = 0.0;
-  for_each([&](float z, int l) {
-    if (make_comp(z, a.voff + l) >= C3) loc += weight(z);
-  });
+  if (keyed) {
+    // per distinct value: count x weight for values above the cutoff value; the ties AT the cutoff
+    // value are kept by id (ids up to the cutoff's), counted by one integer pass when present
+    // (in the 32-bit key order of the composites: C3 may sit below every value, e.g. 0)
+    const uint32_t key3 = (uint32_t)(C3 >> 32);
+    const float v3 = comp_val(C3);
+    const uint32_t id3 = (uint32_t)comp_id(C3);
+    for (int k = tid; k < 65536; k += kExThreads) {
+      const uint32_t c = kcount((uint32_t)k);
+      if (!c) continue;
+      const float z = val_of_okey((uint32_t)k);
+      if (z > -INFINITY && f2key(z) > key3) loc += (double)c * weight(z);  // (not NaN)
+    }
+    for (int e = tid; e < R.nside; e += kExThreads)
+      if (side_z[e] > -INFINITY && make_comp(side_z[e], a.voff + side_id[e]) >= C3) loc += weight(side_z[e]);
+    const uint32_t bits3 = __float_as_uint(v3);
+    // (ties at value 0 include -0: the composites order +0 and -0 as equal, like the oracle)
+    const bool zero3 = v3 == 0.0f;
+    const uint32_t ntie = (bits3 & 0xFFFFu) == 0u && v3 > -INFINITY && (bits3 >> 16) != 0xFF80u
+                              ? kcount(okey_of_bits(bits3 >> 16)) + (zero3 ? kcount(0x7FFFu) : 0u)
+                              : 0u;
+    const bool tie_key = ntie > 0;
+    // (ids are contiguous per CTA: a chunk wholly at or below id3 keeps all its ties, one wholly
+    // above none; only the CTA holding id3 counts by id)
+    const int64_t l3 = (int64_t)id3 - a.voff;
+    if (tie_key && l3 >= (int64_t)R.c1 - 1) {
+      if (tid == 0) loc += (double)ntie * weight(v3);
+    } else if (tie_key && l3 >= (int64_t)R.c0) {
+      const uint32_t h3 = bits3 >> 16;
+      uint32_t nt = 0;
+      for_vecs([&](int v, const uint4 u) {
+        const uint32_t pb = R.pbits(v);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int l = v * 8 + t;
+          const uint32_t h = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+          const bool eq = zero3 ? (h & 0x7FFFu) == 0u : h == h3;
+          if (l < R.c1 && !((pb >> t) & 1u) && eq && (uint32_t)(a.voff + l) <= id3) ++nt;
+        }
+      });
+      loc += (double)nt * weight(v3);
+    }
+  } else {
+    for_each([&](float z, int l) {
+      if (make_comp(z, a.voff + l) >= C3) loc += weight(z);
+    });
+  }
   const double ctot = ex_sum_d(loc, sd);
   if (tid == 0) ex_st64(ex_map(tots + rank, 0), __double_as_longlong(ctot));
   ex_csync();
+  EXPROF(13);
+  EXSTOP(13);
   const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
   const double u = philox_uniform(seed, prm.request_id, a.step);
   if (rank == 0 && tid == 0) {
@@ -695,59 +963,258 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     }
   }
   ex_csync();
+  EXPROF(14);
+  EXSTOP(14);
   if ((int)rank == ctl[8]) {
     // this CTA holds the draw: walk its chunk in id order, rounds of 512 vectors (block scans)
     const double tgt = cd[8], W = cd[9];
     const bool at_top = cd[10] != 0.0;
-    double run = 0.0;
     if (tid == 0) {
       ctl[9] = -1;   // found element (local id)
       ctl[11] = -1;  // last kept element (local id)
     }
     ex_bar();
-    for (int base = v0; base < v1; base += kExThreads) {
-      const int v = base + tid;
-      float z[VEC];
-      double wl[VEC];
-      double vs = 0.0;
-      int last = -1;
-      if (v < v1) {
-        R.vec(v, z);
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) {
-          const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + v * VEC + t) >= C3;
-          wl[t] = kept ? weight(z[t]) : 0.0;
-          vs += wl[t];
-          if (kept) last = v * VEC + t;
+    // bf16 rows: the weights of the values with exponent in [2^-16, 2^8) from a table (one entry per
+    // value, the same float64 arithmetic as weight(); built over the key histogram, no longer needed)
+    constexpr int kE0 = 127 - 16, kNE = 24;
+    double* wk = reinterpret_cast<double*>(smem + kExOffKh);  // [2][kNE][128]
+    double* side_w = wk + 2 * kNE * 128;  // [kSide] weights of the side list's z'
+    // the side-list index of each vector's first penalised element (prefix of the bitmap counts)
+    uint16_t* prank = reinterpret_cast<uint16_t*>(side_w + kSide);  // [chunk vectors <= 8192]
+    static_assert((2 * kNE * 128 + kSide) * 8 + 8192 * 2 <= 65536 * 2, "tables overlay the key histogram");
+    if (keyed) {
+      for (int e = tid; e < R.nside; e += kExThreads) side_w[e] = side_z[e] > -INFINITY ? weight(side_z[e]) : 0.0;
+      {
+        const int S2 = (v1 - v0 + kExThreads - 1) / kExThreads;
+        const int a0 = min(v1, v0 + tid * S2), a1 = min(v1, a0 + S2);
+        int cnt = 0;
+        for (int v = a0; v < a1; ++v) cnt += __popc(R.pbits(v));
+        const int lane = tid & 31, w = tid >> 5;
+        const int incl = warp_incl_scan_i(cnt, lane);
+        if (lane == 31) si[w] = incl;
+        ex_bar();
+        int run = incl - cnt;
+        for (int i = 0; i < w; ++i) run += si[i];
+        for (int v = a0; v < a1; ++v) {
+          prank[v - v0] = (uint16_t)run;
+          run += __popc(R.pbits(v));
         }
-      } else {
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) wl[t] = 0.0;
       }
-      double rt;
-      const double ex = ex_excl_scan_d(vs, &rt, sd) + run;
-      if (!at_top && vs > 0.0 && ex <= tgt && tgt < ex + vs) {  // (one thread: the crossing vector)
-        double c = ex;
-        int pick = last;
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) {
-          c += wl[t];
-          if (wl[t] > 0.0 && c > tgt) {
-            pick = v * VEC + t;
-            break;
-          }
-        }
-        ctl[9] = pick;
+      for (int i = tid; i < 2 * kNE * 128; i += kExThreads) {
+        const uint32_t h = ((uint32_t)(i / (kNE * 128)) << 15) | ((uint32_t)(kE0 + (i / 128) % kNE) << 7) | (uint32_t)(i & 127);
+        const float z = __uint_as_float(h << 16);
+        wk[i] = (z <= M) ? weight(z) : 0.0;
       }
-      if (last >= 0) atomicMax(&ctl[11], last);
-      run += rt;
       ex_bar();
-      if (ctl[9] >= 0) break;  // (uniform after the barrier)
     }
+    EXPROF(21);
+    if (EXACT_STOP_ON(21)) return;
+    const uint32_t key3c = (uint32_t)(C3 >> 32), id3c = (uint32_t)comp_id(C3);
+    // bf16 kept test in the 16-bit value-key order: kept <=> kb3 + [local id > l3] <= okey <= okey(+max)
+    // (ties at the cutoff value kept up to its id; a cutoff value that is no bf16 value has no ties)
+    int kb3 = 0x80;                 // (no cutoff: every finite value, from okey(-max))
+    int64_t l3 = INT64_MAX;
+    if (keyed && C3 != 0) {
+      const float v3 = comp_val(C3);
+      const uint32_t b3 = __float_as_uint(v3);
+      if ((b3 & 0xFFFFu) == 0u) {  // a bf16 value: +0 stands for both zeros (composite order)
+        kb3 = (int)okey_of_bits(b3 >> 16);
+        l3 = (int64_t)id3c - a.voff;
+      } else {                     // the first value key above v3 (bisection, one thread)
+        if (tid == 0) {
+          uint32_t lo = 0x80u, hi = 0xFF80u;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (val_of_okey(mid) > v3) hi = mid;
+            else lo = mid + 1;
+          }
+          ctl[16] = (int)lo;
+        }
+        ex_bar();
+        kb3 = ctl[16];
+      }
+    }
+    // the kept weights w[0..VEC) of vector v (0 if not kept); *lastk = its last kept local id
+    auto vec_w = [&](int v, const uint4 u, double* w, int* lastk) {
+      const int lb = v * VEC;
+      const uint32_t pb = R.pbits(v);
+      if (VEC == 8 && keyed) {
+        // unpenalised elements: the kept test on the value key, the weight from the per-value table
+        // (values outside it after, rarely); penalised ones from the side list (weights precomputed)
+        const uint32_t ok = ~pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
+        uint32_t kept_m = 0, slow = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
+          uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+          h = h == 0x8000u ? 0u : h;  // (-0 is +0)
+          const uint32_t k = okey_of_bits(h);
+          const uint32_t kt = (uint32_t)kb3 + ((int64_t)(lb + t) > l3 ? 1u : 0u);
+          const bool kept = ((ok >> t) & 1u) && k >= kt && k <= 0xFF7Fu;  // (finite, at or above the cutoff)
+          const uint32_t wi = (h & 0x7FFFu) - (uint32_t)(kE0 << 7);  // index within the sign's table
+          const bool inw = wi < (uint32_t)(kNE * 128);
+          const double wt = wk[inw ? wi + (h >> 15) * (kNE * 128) : 0u];
+          w[t] = (kept && inw) ? wt : 0.0;
+          kept_m |= (kept ? 1u : 0u) << t;
+          slow |= (kept && !inw ? 1u : 0u) << t;
+        }
+        if (slow) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if ((slow >> t) & 1u) {
+              const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
+              const uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+              w[t] = weight(__uint_as_float(h << 16));
+            }
+        }
+        const uint32_t pq = pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
+        if (pq) {
+          int e = prank[v - v0];  // its first penalised element's side entry (then consecutive)
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if ((pq >> t) & 1u) {
+              const float z = side_z[e];
+              const bool kept = z > -INFINITY && make_comp(z, a.voff + lb + t) >= C3;
+              w[t] = kept ? side_w[e] : 0.0;
+              kept_m |= (kept ? 1u : 0u) << t;
+              ++e;
+            }
+        }
+        if (kept_m) *lastk = lb + 31 - __clz(kept_m);
+        return;
+      }
+      float z[VEC];
+      R.vec(v, u, z);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) {
+        const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + lb + t) >= C3;
+        w[t] = kept ? weight(z[t]) : 0.0;
+        *lastk = kept ? lb + t : *lastk;
+      }
+    };
+    // rounds of 512 vectors in id order (vector v0 + 512 i + tid: coalesced, loads of 4 rounds in
+    // flight): per round the warps' kept masses (fixed-order warp sums) into smem; then the round,
+    // the warp and the lane holding the target, each from those sums (no per-round block barrier)
+    const int nr = (v1 - v0 + kExThreads - 1) / kExThreads;  // rounds (<= kGat / kExW)
+    double* rs = reinterpret_cast<double*>(gat);              // [nr][kExW] (the gather list is done)
+    const int lane = tid & 31, wp = tid >> 5;
+    int last = -1;
+    uint4 un[4];  // (the next 4 rounds' vectors in flight while 4 are processed)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v = v0 + j * kExThreads + tid;
+      if (j < nr && v < v1) un[j] = R.ld(v);
+    }
+    for (int i0 = 0; i0 < nr; i0 += 4) {
+      uint4 u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        u[j] = un[j];
+        const int v = v0 + (i0 + 4 + j) * kExThreads + tid;
+        if (i0 + 4 + j < nr && v < v1) un[j] = R.ld(v);
+      }
+#pragma unroll 1
+      for (int j = 0; j < 4 && i0 + j < nr; ++j) {
+        const int v = v0 + (i0 + j) * kExThreads + tid;
+        const uint4 uj = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
+        double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#if defined(EXACT_EXP) && EXACT_EXP == 3
+        w[0] = (double)uj.x;
+#else
+        if (v < v1) vec_w(v, uj, w, &last);
+#endif
+        double ls = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) ls += w[q];
+#if !(defined(EXACT_EXP) && EXACT_EXP == 2)
+        ls = warp_sum_d(ls);
+#endif
+        if (lane == 0) rs[(i0 + j) * kExW + wp] = ls;
+      }
+    }
+    EXPROF(16);
+    if (EXACT_STOP_ON(16)) return;
+    ex_bar();
+    EXPROF(17);
+    // warp 0: round totals (warps in order), their prefix; the round rr holding the target and the
+    // mass before it, then the warp ww inside it
+    if (tid < 32) {
+      double run = 0.0;
+      int rr = -1, ww = -1;
+      double before = 0.0;
+      for (int i0 = 0; i0 < nr && rr < 0; i0 += 32) {
+        const int i = i0 + lane;
+        double tot = 0.0;
+        if (i < nr)
+          for (int k = 0; k < kExW; ++k) tot += rs[i * kExW + k];
+        const double incl = warp_incl_scan_d(tot, lane);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, i < nr && tot > 0.0 && run + incl > tgt);
+        if (bal) {
+          const int src = __ffs(bal) - 1;
+          rr = i0 + src;
+          before = __shfl_sync(0xFFFFFFFFu, run + incl - tot, src);
+        }
+        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      }
+      if (rr >= 0 && !at_top) {
+        const double wv = lane < kExW ? rs[rr * kExW + lane] : 0.0;
+        const double incl = warp_incl_scan_d(wv, lane);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, lane < kExW && wv > 0.0 && before + incl > tgt);
+        const int src = bal ? __ffs(bal) - 1 : -1;
+        ww = src;
+        if (src >= 0) before = __shfl_sync(0xFFFFFFFFu, before + incl - wv, src);
+      }
+      if (lane == 0) {
+        ctl[14] = rr;
+        ctl[15] = ww;
+        cd[11] = before;
+      }
+    }
+    ex_bar();
+    {
+      const int rr = ctl[14], ww = ctl[15];
+      if (rr >= 0 && ww >= 0 && wp == ww) {
+        // the warp holding the target: its lanes' vectors again, a warp scan, the crossing lane
+        // walks its elements in order
+        const int v = v0 + rr * kExThreads + tid;
+        double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int lk = -1;
+        if (v < v1) vec_w(v, R.ld(v), w, &lk);
+        double ls = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) ls += w[q];
+        const double incl = warp_incl_scan_d(ls, lane);
+        const double before = cd[11];
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ls > 0.0 && before + incl > tgt);
+        int lmax = lk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xFFFFFFFFu, lmax, o));
+        if (bal) {
+          if (lane == __ffs(bal) - 1) {
+            double c = before + incl - ls;
+            int p = lk;  // (rounding inside the lane: its last kept)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+              c += w[q];
+              if (w[q] > 0.0 && c > tgt) {
+                p = v * VEC + q;
+                break;
+              }
+            }
+            ctl[9] = p;
+          }
+        } else if (lane == 0) {
+          ctl[9] = lmax;  // (rounding: the target at the warp's very top - its last kept id)
+        }
+      }
+    }
+    if (last >= 0) atomicMax(&ctl[11], last);
+    ex_bar();
+    EXPROF(18);
     if (tid == 0) {
       const int l = (ctl[9] >= 0) ? ctl[9] : ctl[11];  // (u W at the top of the mass: the last kept id)
       float zz[VEC];
-      R.vec(l / VEC, zz);
+      R.vec(l / VEC, R.ld(l / VEC), zz);
       const float ztok = zz[l % VEC];
       const int tok = a.voff + l;
       const double wtok = exp(((double)ztok - (double)M) * inv_tau);
@@ -768,6 +1235,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     if (a.append && tid < 32) warp_append_token(a.hs, slot, ctl[12], tid);
   }
   ex_csync();  // no CTA leaves while another may still address its shared memory
+  EXPROF(15);
 }
 
 // Debug: q[b, v] = final filtered distribution (w_v / W over K3; one-hot for greedy rows).

@@ -227,7 +227,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
       cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem) !=
           cudaSuccess ||
       cudaFuncSetAttribute(exact_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kExactSmem) != cudaSuccess ||
+                           kExactSmemBf16) != cudaSuccess ||
       cudaFuncSetAttribute(select_rows_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kSelectSmem) != cudaSuccess ||
       cudaFuncSetAttribute(select_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelectSmem) !=
@@ -620,8 +620,12 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
   if (need) {
     // one cluster of G CTAs per row (every row launched; rows that are not pending exit at once):
     // G = the largest power of two <= 8 with B * G <= 2 resident CTAs per SM (c2: G = 4)
+    // bf16: one CTA per SM (the value-key histogram), chunks of <= 65535 elements
+    const bool bf = h->cfg.logits_dtype == SAMPLER_BF16;
+    const int per_sm = bf ? 1 : 2;
     int G = 1;
-    while (G < 8 && (int64_t)B * G * 2 <= 2LL * h->sm_count) G *= 2;
+    while (G < 8 && (int64_t)B * G * 2 <= (int64_t)per_sm * h->sm_count) G *= 2;
+    while (bf && G < 8 && ((int64_t)h->cfg.vocab_local + G - 1) / G > kKhMaxChunk - 127) G *= 2;
     ExactArgs e{};
     e.logits = logits;
     e.ld = ld;
@@ -643,7 +647,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(B * G));
     cfg.blockDim = dim3(kExThreads);
-    cfg.dynamicSmemBytes = kExactSmem;
+    cfg.dynamicSmemBytes = bf ? kExactSmemBf16 : kExactSmem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
