@@ -879,58 +879,182 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   // ---- the draw: W = mass of K3 in id order; per-CTA totals -> cluster prefix -> the CTA and the
   EXPROF(12);
   EXSTOP(12);
-  //      thread holding u*W walk their elements in id order
-  double loc = 0.0;
+  //      thread holding u*W walk their elements in id order.  Every CTA: the kept mass of its chunk in
+  //      rounds of 512 vectors (id order), per (round, warp) into smem; the CTA totals from those.
+  // bf16 rows: the weights of the values with exponent in [2^-16, 2^8) from a table (one entry per
+  // value, the same float64 arithmetic as weight(); built over the key histogram, no longer needed)
+  constexpr int kE0 = 127 - 16, kNE = 24;
+  double* wk = reinterpret_cast<double*>(smem + kExOffKh);  // [2][kNE][128]
+  double* side_w = wk + 2 * kNE * 128;  // [kSide] weights of the side list's z'
+  // the side-list index of each vector's first penalised element (prefix of the bitmap counts)
+  uint16_t* prank = reinterpret_cast<uint16_t*>(side_w + kSide);  // [chunk vectors <= 8192]
+  static_assert((2 * kNE * 128 + kSide) * 8 + 8192 * 2 <= 65536 * 2, "tables overlay the key histogram");
   if (keyed) {
-    // per distinct value: count x weight for values above the cutoff value; the ties AT the cutoff
-    // value are kept by id (ids up to the cutoff's), counted by one integer pass when present
-    // (in the 32-bit key order of the composites: C3 may sit below every value, e.g. 0)
-    const uint32_t key3 = (uint32_t)(C3 >> 32);
-    const float v3 = comp_val(C3);
-    const uint32_t id3 = (uint32_t)comp_id(C3);
-    for (int k = tid; k < 65536; k += kExThreads) {
-      const uint32_t c = kcount((uint32_t)k);
-      if (!c) continue;
-      const float z = val_of_okey((uint32_t)k);
-      if (z > -INFINITY && f2key(z) > key3) loc += (double)c * weight(z);  // (not NaN)
+    for (int e = tid; e < R.nside; e += kExThreads) side_w[e] = side_z[e] > -INFINITY ? weight(side_z[e]) : 0.0;
+    {
+      const int S2 = (v1 - v0 + kExThreads - 1) / kExThreads;
+      const int a0 = min(v1, v0 + tid * S2), a1 = min(v1, a0 + S2);
+      int cnt = 0;
+      for (int v = a0; v < a1; ++v) cnt += __popc(R.pbits(v));
+      const int lane = tid & 31, w = tid >> 5;
+      const int incl = warp_incl_scan_i(cnt, lane);
+      if (lane == 31) si[w] = incl;
+      ex_bar();
+      int run = incl - cnt;
+      for (int i = 0; i < w; ++i) run += si[i];
+      for (int v = a0; v < a1; ++v) {
+        prank[v - v0] = (uint16_t)run;
+        run += __popc(R.pbits(v));
+      }
     }
-    for (int e = tid; e < R.nside; e += kExThreads)
-      if (side_z[e] > -INFINITY && make_comp(side_z[e], a.voff + side_id[e]) >= C3) loc += weight(side_z[e]);
-    const uint32_t bits3 = __float_as_uint(v3);
-    // (ties at value 0 include -0: the composites order +0 and -0 as equal, like the oracle)
-    const bool zero3 = v3 == 0.0f;
-    const uint32_t ntie = (bits3 & 0xFFFFu) == 0u && v3 > -INFINITY && (bits3 >> 16) != 0xFF80u
-                              ? kcount(okey_of_bits(bits3 >> 16)) + (zero3 ? kcount(0x7FFFu) : 0u)
-                              : 0u;
-    const bool tie_key = ntie > 0;
-    // (ids are contiguous per CTA: a chunk wholly at or below id3 keeps all its ties, one wholly
-    // above none; only the CTA holding id3 counts by id)
-    const int64_t l3 = (int64_t)id3 - a.voff;
-    if (tie_key && l3 >= (int64_t)R.c1 - 1) {
-      if (tid == 0) loc += (double)ntie * weight(v3);
-    } else if (tie_key && l3 >= (int64_t)R.c0) {
-      const uint32_t h3 = bits3 >> 16;
-      uint32_t nt = 0;
-      for_vecs([&](int v, const uint4 u) {
-        const uint32_t pb = R.pbits(v);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int l = v * 8 + t;
-          const uint32_t h = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
-          const bool eq = zero3 ? (h & 0x7FFFu) == 0u : h == h3;
-          if (l < R.c1 && !((pb >> t) & 1u) && eq && (uint32_t)(a.voff + l) <= id3) ++nt;
-        }
-      });
-      loc += (double)nt * weight(v3);
+    for (int i = tid; i < 2 * kNE * 128; i += kExThreads) {
+      const uint32_t h = ((uint32_t)(i / (kNE * 128)) << 15) | ((uint32_t)(kE0 + (i / 128) % kNE) << 7) | (uint32_t)(i & 127);
+      const float z = __uint_as_float(h << 16);
+      wk[i] = (z <= M) ? weight(z) : 0.0;
     }
-  } else {
-    for_each([&](float z, int l) {
-      if (make_comp(z, a.voff + l) >= C3) loc += weight(z);
-    });
+    ex_bar();
   }
-  const double ctot = ex_sum_d(loc, sd);
-  if (tid == 0) ex_st64(ex_map(tots + rank, 0), __double_as_longlong(ctot));
+  EXPROF(21);
+  if (EXACT_STOP_ON(21)) return;
+  const uint32_t key3c = (uint32_t)(C3 >> 32), id3c = (uint32_t)comp_id(C3);
+  // bf16 kept test in the 16-bit value-key order: kept <=> kb3 + [local id > l3] <= okey <= okey(+max)
+  // (ties at the cutoff value kept up to its id; a cutoff value that is no bf16 value has no ties)
+  int kb3 = 0x80;                 // (no cutoff: every finite value, from okey(-max))
+  int64_t l3 = INT64_MAX;
+  if (keyed && C3 != 0) {
+    const float v3 = comp_val(C3);
+    const uint32_t b3 = __float_as_uint(v3);
+    if ((b3 & 0xFFFFu) == 0u) {  // a bf16 value: +0 stands for both zeros (composite order)
+      kb3 = (int)okey_of_bits(b3 >> 16);
+      l3 = (int64_t)id3c - a.voff;
+    } else {                     // the first value key above v3 (bisection, one thread)
+      if (tid == 0) {
+        uint32_t lo = 0x80u, hi = 0xFF80u;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (val_of_okey(mid) > v3) hi = mid;
+          else lo = mid + 1;
+        }
+        ctl[16] = (int)lo;
+      }
+      ex_bar();
+      kb3 = ctl[16];
+    }
+  }
+  // the kept weights w[0..VEC) of vector v (0 if not kept); *lastk = its last kept local id
+  auto vec_w = [&](int v, const uint4 u, double* w, int* lastk) {
+    const int lb = v * VEC;
+    const uint32_t pb = R.pbits(v);
+    if (VEC == 8 && keyed) {
+      // unpenalised elements: the kept test on the value key, the weight from the per-value table
+      // (values outside it after, rarely); penalised ones from the side list (weights precomputed)
+      const uint32_t ok = ~pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
+      uint32_t kept_m = 0, slow = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
+        uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+        h = h == 0x8000u ? 0u : h;  // (-0 is +0)
+        const uint32_t k = okey_of_bits(h);
+        const uint32_t kt = (uint32_t)kb3 + ((int64_t)(lb + t) > l3 ? 1u : 0u);
+        const bool kept = ((ok >> t) & 1u) && k >= kt && k <= 0xFF7Fu;  // (finite, at or above the cutoff)
+        const uint32_t wi = (h & 0x7FFFu) - (uint32_t)(kE0 << 7);  // index within the sign's table
+        const bool inw = wi < (uint32_t)(kNE * 128);
+        const double wt = wk[inw ? wi + (h >> 15) * (kNE * 128) : 0u];
+        w[t] = (kept && inw) ? wt : 0.0;
+        kept_m |= (kept ? 1u : 0u) << t;
+        slow |= (kept && !inw ? 1u : 0u) << t;
+      }
+      if (slow) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if ((slow >> t) & 1u) {
+            const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
+            const uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+            w[t] = weight(__uint_as_float(h << 16));
+          }
+      }
+      const uint32_t pq = pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
+      if (pq) {
+        int e = prank[v - v0];  // its first penalised element's side entry (then consecutive)
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if ((pq >> t) & 1u) {
+            const float z = side_z[e];
+            const bool kept = z > -INFINITY && make_comp(z, a.voff + lb + t) >= C3;
+            w[t] = kept ? side_w[e] : 0.0;
+            kept_m |= (kept ? 1u : 0u) << t;
+            ++e;
+          }
+      }
+      if (kept_m) *lastk = lb + 31 - __clz(kept_m);
+      return;
+    }
+    float z[VEC];
+    R.vec(v, u, z);
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) {
+      const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + lb + t) >= C3;
+      w[t] = kept ? weight(z[t]) : 0.0;
+      *lastk = kept ? lb + t : *lastk;
+    }
+  };
+  // rounds of 512 vectors in id order (vector v0 + 512 i + tid: coalesced, loads of 4 rounds in
+  // flight): per round the warps' kept masses (fixed-order warp sums) into smem; then the round,
+  // the warp and the lane holding the target, each from those sums (no per-round block barrier)
+  const int nr = (v1 - v0 + kExThreads - 1) / kExThreads;  // rounds (<= kGat / kExW)
+  double* rs = reinterpret_cast<double*>(gat);              // [nr][kExW] (the gather list is done)
+  const int lane = tid & 31, wp = tid >> 5;
+  int last = -1;
+  uint4 un[4];  // (the next 4 rounds' vectors in flight while 4 are processed)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int v = v0 + j * kExThreads + tid;
+    if (j < nr && v < v1) un[j] = R.ld(v);
+  }
+  for (int i0 = 0; i0 < nr; i0 += 4) {
+    uint4 u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u[j] = un[j];
+      const int v = v0 + (i0 + 4 + j) * kExThreads + tid;
+      if (i0 + 4 + j < nr && v < v1) un[j] = R.ld(v);
+    }
+#pragma unroll 1
+    for (int j = 0; j < 4 && i0 + j < nr; ++j) {
+      const int v = v0 + (i0 + j) * kExThreads + tid;
+      const uint4 uj = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
+      double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#if defined(EXACT_EXP) && EXACT_EXP == 3
+      w[0] = (double)uj.x;
+#else
+      if (v < v1) vec_w(v, uj, w, &last);
+#endif
+      double ls = 0.0;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) ls += w[q];
+#if !(defined(EXACT_EXP) && EXACT_EXP == 2)
+      ls = warp_sum_d(ls);
+#endif
+      if (lane == 0) rs[(i0 + j) * kExW + wp] = ls;
+    }
+  }
+  if (tid == 0) ctl[11] = -1;  // last kept element (local id)
+  ex_bar();
+  if (last >= 0) atomicMax(&ctl[11], last);
+  // the CTA total: round totals (warps in order), scanned 32 rounds at a time (the same arithmetic
+  // as the search below, so that the two agree to the bit)
+  if (tid < 32) {
+    double run = 0.0;
+    for (int i0 = 0; i0 < nr; i0 += 32) {
+      const int i = i0 + lane;
+      double tot = 0.0;
+      if (i < nr)
+        for (int k = 0; k < kExW; ++k) tot += rs[i * kExW + k];
+      run += __shfl_sync(0xFFFFFFFFu, warp_incl_scan_d(tot, lane), 31);
+    }
+    if (lane == 0) ex_st64(ex_map(tots + rank, 0), __double_as_longlong(run));
+  }
   ex_csync();
   EXPROF(13);
   EXSTOP(13);
@@ -966,172 +1090,10 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   EXPROF(14);
   EXSTOP(14);
   if ((int)rank == ctl[8]) {
-    // this CTA holds the draw: walk its chunk in id order, rounds of 512 vectors (block scans)
+    // this CTA holds the draw: the round, the warp and the lane holding the target from its sums
     const double tgt = cd[8], W = cd[9];
     const bool at_top = cd[10] != 0.0;
-    if (tid == 0) {
-      ctl[9] = -1;   // found element (local id)
-      ctl[11] = -1;  // last kept element (local id)
-    }
-    ex_bar();
-    // bf16 rows: the weights of the values with exponent in [2^-16, 2^8) from a table (one entry per
-    // value, the same float64 arithmetic as weight(); built over the key histogram, no longer needed)
-    constexpr int kE0 = 127 - 16, kNE = 24;
-    double* wk = reinterpret_cast<double*>(smem + kExOffKh);  // [2][kNE][128]
-    double* side_w = wk + 2 * kNE * 128;  // [kSide] weights of the side list's z'
-    // the side-list index of each vector's first penalised element (prefix of the bitmap counts)
-    uint16_t* prank = reinterpret_cast<uint16_t*>(side_w + kSide);  // [chunk vectors <= 8192]
-    static_assert((2 * kNE * 128 + kSide) * 8 + 8192 * 2 <= 65536 * 2, "tables overlay the key histogram");
-    if (keyed) {
-      for (int e = tid; e < R.nside; e += kExThreads) side_w[e] = side_z[e] > -INFINITY ? weight(side_z[e]) : 0.0;
-      {
-        const int S2 = (v1 - v0 + kExThreads - 1) / kExThreads;
-        const int a0 = min(v1, v0 + tid * S2), a1 = min(v1, a0 + S2);
-        int cnt = 0;
-        for (int v = a0; v < a1; ++v) cnt += __popc(R.pbits(v));
-        const int lane = tid & 31, w = tid >> 5;
-        const int incl = warp_incl_scan_i(cnt, lane);
-        if (lane == 31) si[w] = incl;
-        ex_bar();
-        int run = incl - cnt;
-        for (int i = 0; i < w; ++i) run += si[i];
-        for (int v = a0; v < a1; ++v) {
-          prank[v - v0] = (uint16_t)run;
-          run += __popc(R.pbits(v));
-        }
-      }
-      for (int i = tid; i < 2 * kNE * 128; i += kExThreads) {
-        const uint32_t h = ((uint32_t)(i / (kNE * 128)) << 15) | ((uint32_t)(kE0 + (i / 128) % kNE) << 7) | (uint32_t)(i & 127);
-        const float z = __uint_as_float(h << 16);
-        wk[i] = (z <= M) ? weight(z) : 0.0;
-      }
-      ex_bar();
-    }
-    EXPROF(21);
-    if (EXACT_STOP_ON(21)) return;
-    const uint32_t key3c = (uint32_t)(C3 >> 32), id3c = (uint32_t)comp_id(C3);
-    // bf16 kept test in the 16-bit value-key order: kept <=> kb3 + [local id > l3] <= okey <= okey(+max)
-    // (ties at the cutoff value kept up to its id; a cutoff value that is no bf16 value has no ties)
-    int kb3 = 0x80;                 // (no cutoff: every finite value, from okey(-max))
-    int64_t l3 = INT64_MAX;
-    if (keyed && C3 != 0) {
-      const float v3 = comp_val(C3);
-      const uint32_t b3 = __float_as_uint(v3);
-      if ((b3 & 0xFFFFu) == 0u) {  // a bf16 value: +0 stands for both zeros (composite order)
-        kb3 = (int)okey_of_bits(b3 >> 16);
-        l3 = (int64_t)id3c - a.voff;
-      } else {                     // the first value key above v3 (bisection, one thread)
-        if (tid == 0) {
-          uint32_t lo = 0x80u, hi = 0xFF80u;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (val_of_okey(mid) > v3) hi = mid;
-            else lo = mid + 1;
-          }
-          ctl[16] = (int)lo;
-        }
-        ex_bar();
-        kb3 = ctl[16];
-      }
-    }
-    // the kept weights w[0..VEC) of vector v (0 if not kept); *lastk = its last kept local id
-    auto vec_w = [&](int v, const uint4 u, double* w, int* lastk) {
-      const int lb = v * VEC;
-      const uint32_t pb = R.pbits(v);
-      if (VEC == 8 && keyed) {
-        // unpenalised elements: the kept test on the value key, the weight from the per-value table
-        // (values outside it after, rarely); penalised ones from the side list (weights precomputed)
-        const uint32_t ok = ~pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
-        uint32_t kept_m = 0, slow = 0;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
-          uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
-          h = h == 0x8000u ? 0u : h;  // (-0 is +0)
-          const uint32_t k = okey_of_bits(h);
-          const uint32_t kt = (uint32_t)kb3 + ((int64_t)(lb + t) > l3 ? 1u : 0u);
-          const bool kept = ((ok >> t) & 1u) && k >= kt && k <= 0xFF7Fu;  // (finite, at or above the cutoff)
-          const uint32_t wi = (h & 0x7FFFu) - (uint32_t)(kE0 << 7);  // index within the sign's table
-          const bool inw = wi < (uint32_t)(kNE * 128);
-          const double wt = wk[inw ? wi + (h >> 15) * (kNE * 128) : 0u];
-          w[t] = (kept && inw) ? wt : 0.0;
-          kept_m |= (kept ? 1u : 0u) << t;
-          slow |= (kept && !inw ? 1u : 0u) << t;
-        }
-        if (slow) {
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if ((slow >> t) & 1u) {
-              const uint32_t wd = t < 2 ? u.x : t < 4 ? u.y : t < 6 ? u.z : u.w;
-              const uint32_t h = (t & 1) ? (wd >> 16) : (wd & 0xFFFFu);
-              w[t] = weight(__uint_as_float(h << 16));
-            }
-        }
-        const uint32_t pq = pb & (lb + 8 <= R.c1 ? 0xFFu : (1u << max(0, R.c1 - lb)) - 1u);
-        if (pq) {
-          int e = prank[v - v0];  // its first penalised element's side entry (then consecutive)
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if ((pq >> t) & 1u) {
-              const float z = side_z[e];
-              const bool kept = z > -INFINITY && make_comp(z, a.voff + lb + t) >= C3;
-              w[t] = kept ? side_w[e] : 0.0;
-              kept_m |= (kept ? 1u : 0u) << t;
-              ++e;
-            }
-        }
-        if (kept_m) *lastk = lb + 31 - __clz(kept_m);
-        return;
-      }
-      float z[VEC];
-      R.vec(v, u, z);
-#pragma unroll
-      for (int t = 0; t < VEC; ++t) {
-        const bool kept = z[t] > -INFINITY && make_comp(z[t], a.voff + lb + t) >= C3;
-        w[t] = kept ? weight(z[t]) : 0.0;
-        *lastk = kept ? lb + t : *lastk;
-      }
-    };
-    // rounds of 512 vectors in id order (vector v0 + 512 i + tid: coalesced, loads of 4 rounds in
-    // flight): per round the warps' kept masses (fixed-order warp sums) into smem; then the round,
-    // the warp and the lane holding the target, each from those sums (no per-round block barrier)
-    const int nr = (v1 - v0 + kExThreads - 1) / kExThreads;  // rounds (<= kGat / kExW)
-    double* rs = reinterpret_cast<double*>(gat);              // [nr][kExW] (the gather list is done)
-    const int lane = tid & 31, wp = tid >> 5;
-    int last = -1;
-    uint4 un[4];  // (the next 4 rounds' vectors in flight while 4 are processed)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int v = v0 + j * kExThreads + tid;
-      if (j < nr && v < v1) un[j] = R.ld(v);
-    }
-    for (int i0 = 0; i0 < nr; i0 += 4) {
-      uint4 u[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        u[j] = un[j];
-        const int v = v0 + (i0 + 4 + j) * kExThreads + tid;
-        if (i0 + 4 + j < nr && v < v1) un[j] = R.ld(v);
-      }
-#pragma unroll 1
-      for (int j = 0; j < 4 && i0 + j < nr; ++j) {
-        const int v = v0 + (i0 + j) * kExThreads + tid;
-        const uint4 uj = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
-        double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#if defined(EXACT_EXP) && EXACT_EXP == 3
-        w[0] = (double)uj.x;
-#else
-        if (v < v1) vec_w(v, uj, w, &last);
-#endif
-        double ls = 0.0;
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) ls += w[q];
-#if !(defined(EXACT_EXP) && EXACT_EXP == 2)
-        ls = warp_sum_d(ls);
-#endif
-        if (lane == 0) rs[(i0 + j) * kExW + wp] = ls;
-      }
-    }
+    if (tid == 0) ctl[9] = -1;  // found element (local id)
     EXPROF(16);
     if (EXACT_STOP_ON(16)) return;
     ex_bar();
@@ -1208,7 +1170,6 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
         }
       }
     }
-    if (last >= 0) atomicMax(&ctl[11], last);
     ex_bar();
     EXPROF(18);
     if (tid == 0) {
