@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hist", type=int, default=None,
+                    help="history tokens per row (NEXT-4 curve; default: the config's own)")
     return ap.parse_args()
 
 
@@ -265,6 +267,14 @@ def main():
 
     wls = [make_workload(a.config, B=a.batch, seed_offset=i + (0 if (vocab_mode or split_mode) else 17 * rank))
            for i in range(NDIST)]
+    if a.hist:  # long histories: the config's history recipe at a.hist tokens per row
+        from workloads.synth import bf16_bits_to_f32, gen_history
+        hrng = np.random.default_rng(1234 + rank)
+        for w in wls:
+            f = bf16_bits_to_f32(w.raw) if w.dtype == "bf16" else w.raw
+            hs = [gen_history(hrng, f[b], a.hist - min(128, a.hist // 2), min(128, a.hist // 2)) for b in range(w.B)]
+            w.prompts[:] = [p for p, _ in hs]
+            w.outputs[:] = [o for _, o in hs]
     B_global = wls[0].B
     if split_mode:  # this rank's rows of the one global batch
         from paper_2506_22033_b200.distributed import batch_row_bounds

@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   }
   EXPROF(21);
   if (EXACT_STOP_ON(21)) return;
-  const uint32_t key3c = (uint32_t)(C3 >> 32), id3c = (uint32_t)comp_id(C3);
+  const uint32_t id3c = (uint32_t)comp_id(C3);
   // bf16 kept test in the 16-bit value-key order: kept <=> kb3 + [local id > l3] <= okey <= okey(+max)
   // (ties at the cutoff value kept up to its id; a cutoff value that is no bf16 value has no ties)
   int kb3 = 0x80;                 // (no cutoff: every finite value, from okey(-max))

@@ -135,6 +135,64 @@ __device__ __forceinline__ void warp_append_token(const HistState& hs, int slot,
   __syncwarp();
 }
 
+// Append `tok` to a long history (more unique entries than phase B stages in smem) by the whole
+// block (P:371 incremental update): the insertion point by a two-round 256-way search of the sorted
+// table, then the entries above it moved up one slot in chunks of 4 per thread from the top down
+// (every chunk read before any of it is written), the new entry, the token.
+__device__ __noinline__ void block_append_global(const HistState& hs, int slot, int32_t tok) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  SlotMeta* sm = hs.meta + slot;
+  const int np = sm->n_prompt, no = sm->n_out, nu = sm->n_uniq;
+  if (np + no + 1 > hs.L) {
+    if (tid == 0) sm->flags |= 1;
+    return;
+  }
+  UniqEntry* u = hs.uniq + (int64_t)slot * hs.L;
+  // round 1: samples at i = t * step; the count below tok is a prefix
+  const int step = (nu + nt - 1) / nt;
+  const int i1 = tid * step;
+  const int c1 = __syncthreads_count(i1 < nu && u[i1].id < tok);
+  const int base = c1 > 0 ? (c1 - 1) * step + 1 : 0;  // (entries below base are < tok)
+  int c2 = 0;  // round 2: the step - 1 entries after the last sample below tok
+  for (int o = 0; o < step; o += nt) {
+    const int i2 = base + o + tid;
+    c2 += __syncthreads_count(o + tid < step && i2 < nu && u[i2].id < tok);
+  }
+  const int less = c1 > 0 ? base + c2 : 0;
+  const bool found = less < nu && u[less].id == tok;
+  if (found) {
+    if (tid == 0) u[less].meta += 2u;
+  } else {
+    for (int top = nu; top > less; top -= 4 * nt) {
+      UniqEntry e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = top - 1 - tid - q * nt;
+        if (i >= less) e[q] = u[i];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = top - 1 - tid - q * nt;
+        if (i >= less) u[i + 1] = e[q];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      UniqEntry e;
+      e.id = tok;
+      e.meta = 2u;
+      u[less] = e;
+      pmask_set(hs, slot, tok);
+    }
+  }
+  if (tid == 0) {
+    hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
+    sm->n_out = no + 1;
+    if (!found) sm->n_uniq = nu + 1;
+  }
+}
+
 // Final decision for one row by one warp (R6-R11): top-k -> top-p (renormalised over
 // the top-k survivors) -> min-p over the candidates top[0..n) (sorted by pi), exact down to the
 // frontier F; inverse-CDF draw over the kept set in ascending id order with the Philox uniform;

@@ -479,6 +479,24 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   }
   const UniqEntry* utab = a.hs.uniq + (int64_t)slot * a.hs.L;
   const uint8_t* rowp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
+  // very long tables (nu > kSelPen): the entries past the smem copy straight from phase A's hand-off
+  // (id, meta, exact z'), 4 per thread in flight; fn(id, local id, z') for those inside the slice
+  const uint4* pent_r = reinterpret_cast<const uint4*>(a.pent + (int64_t)r * a.hs.L);
+  auto for_long = [&](auto&& fn) {
+#pragma unroll 1
+    for (int e0 = kSelPen + tid; e0 < nu; e0 += 4 * kBT) {
+      uint4 x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e0 + q * kBT < nu) x[q] = pent_r[e0 + q * kBT];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (e0 + q * kBT >= nu) break;
+        const int l = (int)x[q].x - a.voff;
+        if (l >= 0 && l < a.vloc) fn((int)x[q].x, l, __uint_as_float(x[q].z));
+      }
+    }
+  };
   // the penalised entries: smem copy of the table (id order) for masking and the append, and the
   // exact penalised values s_zp (entries outside this vocabulary slice are skipped by id)
   STR(1);
@@ -499,14 +517,10 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     if (!(zp < INFINITY)) fl |= kRecBad;  // NaN / +inf logit (or penalised value)
     else mloc = fmaxf(mloc, zp);
   }
-  for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
-    const UniqEntry ue = utab[e];
-    const int l = ue.id - a.voff;
-    if (l < 0 || l >= a.vloc) continue;
-    const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+  for_long([&](int, int, float zp) {
     if (!(zp < INFINITY)) fl |= kRecBad;
     else mloc = fmaxf(mloc, zp);
-  }
+  });
   // one barrier for max and flags together; meanwhile the last warp finds the bound T = the K-th
   // largest step key (each step key = the max of 1024 / 512 elements rounded down, so K distinct
   // elements are >= val(T); every element >= val(T) lies in a group with key >= T or is
@@ -573,14 +587,9 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       // (binary32 MUFU exp2, like the stream's own terms: relative error ~2^-22 per term)
       if (l >= 0 && l < a.vloc && zp > -INFINITY) t += (double)ex2f((float)(((double)zp - (double)M) * rc.c_d));
     }
-#pragma unroll 1
-    for (int e = kSelPen + tid; e < nu; e += kBT) {
-      const UniqEntry ue = utab[e];
-      const int l = ue.id - a.voff;
-      if (l < 0 || l >= a.vloc) continue;
-      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
-      if (zp > -INFINITY) t += dexp2_call(((double)zp - (double)M) * rc.c_d);
-    }
+    for_long([&](int, int, float zp) {
+      if (zp > -INFINITY) t += (double)ex2f((float)(((double)zp - (double)M) * rc.c_d));
+    });
     return t;
   };
   const bool rowok = !bad && M > -INFINITY;
@@ -615,13 +624,9 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       const float zp = s_zp[e];
       if (l >= 0 && l < a.vloc && zp > -INFINITY && zp < INFINITY) add_key(key16_down(zp));
     }
-    for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
-      const UniqEntry ue = utab[e];
-      const int l = ue.id - a.voff;
-      if (l < 0 || l >= a.vloc) continue;
-      const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
+    for_long([&](int, int, float zp) {
       if (zp > -INFINITY && zp < INFINITY) add_key(key16_down(zp));
-    }
+    });
     for (int w = tid; w < gwords; w += kBT) {
       const uint4 g = (w < kSelGR * kBT) ? s_gk[w] : gk4[w];
       const uint32_t x[4] = {g.x, g.y, g.z, g.w};
@@ -670,13 +675,9 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     const float zp = s_zp[e];
     if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, s_ue[e].id));
   }
-  for (int e = kSelPen + tid; e < nu; e += kBT) {  // very long tables: straight from global
-    const UniqEntry ue = utab[e];
-    const int l = ue.id - a.voff;
-    if (l < 0 || l >= a.vloc) continue;
-    const float zp = apply_penalty(Dec<T>::load1(rowp, l), ue.meta, prm, a.pen_mode);
-    if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, ue.id));
-  }
+  for_long([&](int id, int, float zp) {
+    if (zp >= Tv && zp > -INFINITY && zp < INFINITY) push(make_comp(zp, id));
+  });
   STR(19);
   const uint32_t lo2 = lo_k | (lo_k << 16);
   for (int base = 0; base < gwords; base += kSelGR * kBT) {
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   STR(6);
   if (!a.append || tok < 0) return;
   if (nu > kSelPen) {
-    if (tid < 32) warp_append_token(a.hs, slot, tok, lane);
+    block_append_global(a.hs, slot, tok);
     return;
   }
   block_append_smem(a.hs, slot, tok, smeta, s_ue, ms.bs);

@@ -393,3 +393,44 @@ def test_long_histories_penalties(n_hist):
     orc = oracle_run(wl, step=3)
     s, out = _run(wl, step=3)
     assert_parity(wl, out, orc)
+
+
+@pytest.mark.parametrize("n_hist", [32768, 131072])
+def test_very_long_histories_full_vocab(n_hist):
+    """NEXT-4 (L_max <= 128K): 32K / 128K-token histories at the c3 vocabulary, every
+    penalty, top-k / top-p / min-p / unfiltered rows, three steps with in-kernel appends against the
+    oracle's recount."""
+    import torch
+    rng = np.random.default_rng(n_hist)
+    B, V = 4, 152064
+    z = gen_logits(rng, B, V, "bf16")
+    prompts, outputs = [], []
+    for b in range(B):
+        # a Zipf-like stream over the vocabulary (repeats) plus a pool of likely tokens
+        h = np.concatenate([rng.zipf(1.1, size=n_hist // 2) % V, rng.integers(0, V, size=n_hist - n_hist // 2)])
+        rng.shuffle(h)
+        h = h.astype(np.int64).tolist()
+        prompts.append(h[: n_hist - 64])
+        outputs.append(h[n_hist - 64:])
+    params = [RowParams(temperature=0.8, top_k=40, top_p=0.9, min_p=0.05, repetition_penalty=1.2,
+                        presence_penalty=0.4, frequency_penalty=0.1, seed=1, request_id=0),
+              RowParams(temperature=1.0, top_p=0.95, repetition_penalty=1.1, presence_penalty=0.3,
+                        frequency_penalty=0.2, seed=2, request_id=1),
+              RowParams(temperature=0.7, min_p=0.1, repetition_penalty=1.3, seed=3, request_id=2),
+              RowParams(temperature=1.0, frequency_penalty=0.05, seed=4, request_id=3)]
+    wl = Workload("hist", B, V, "bf16", z, prompts, outputs, params)
+    s = make_sampler(wl, max_history=n_hist + 16)
+    x = device_logits(wl)
+    for step in range(3):
+        out = s.sample(x, step, append=True)
+        torch.cuda.synchronize()
+        assert_parity(wl, out, oracle_run(wl, step))
+        tok = out["tokens"].cpu().numpy()
+        for b in range(B):  # the oracle's history follows the sampled tokens (S:248)
+            wl.outputs[b] = wl.outputs[b] + [int(tok[b])]
+    for b in range(B):
+        h = s.get_history(b)
+        assert h["output"] == wl.outputs[b]
+        ids = sorted(set(wl.prompts[b]) | set(wl.outputs[b]))
+        assert h["uniq_ids"] == ids
+
