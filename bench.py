@@ -180,6 +180,27 @@ def _oracle_rows(args):
     return len(rows)
 
 
+def time_paper_cpu(wl, seconds=3.0):
+    """NEXT-3: the paper's column-wise CPU sampler (baselines/paper_cpu: transposed logits,
+    incremental dense penalty buffers, AVX-512, one worker thread per host core)
+    on the same workload, logits in host memory (the device-to-host copy is not included), tokens
+    appended every step.  Returns (rows/s, threads, steps, wall)."""
+    from baselines.paper_cpu import PaperCpuSampler
+    s = PaperCpuSampler(wl.V, wl.B, max_output=max(len(o) for o in wl.outputs) + 4096)
+    for b in range(wl.B):
+        s.set_params(b, wl.params[b])
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    s.step(wl.raw, 0)  # warm-up (page-in)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        s.step(wl.raw, n + 1, append=True)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 4000:
+            break
+    return wl.B * n / el, s.threads, n, el
+
+
 def time_oracle(wl, seconds, max_rows=None):
     """Run the oracle (as it stands) over whole rows of `wl` on all host cores (one process per
     core, BLAS threads = 1) for about `seconds`; returns (rows/s, cores, rows done, wall)."""
@@ -512,6 +533,15 @@ def main():
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                                 "sample": f"whole batches of {a.config} (B={B}) rows, float64 oracle, one process "
                                           f"per core: {done} rows in {el:.1f}s"}
+        try:
+            v2, th, n2, el2 = time_paper_cpu(wl)
+            line["paper_cpu"] = {"value": v2, "unit": UNIT, "cores": th, "kind": "paper column-wise CPU sampler",
+                                 "cpu": cpu_model(),
+                                 "sample": f"{n2} steps of {a.config} (B={B}) in {el2:.1f}s, logits in host memory "
+                                           f"(D2H copy not included), AVX-512, one thread per core "
+                                           f"(baselines/paper_cpu, NEXT-3)"}
+        except Exception as e:  # (a comparator only: its absence never fails the GPU bench)
+            line["paper_cpu"] = {"unavailable": str(e)[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
