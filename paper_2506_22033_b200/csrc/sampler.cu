@@ -191,7 +191,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   const int64_t B = c.max_batch, L = c.max_history;
   auto al = [&](void** p, size_t n) -> bool { return cudaMalloc(p, n) == cudaSuccess; };
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
-            al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * B * L) &&
+            al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * (B * L + 4))  /* (+4: phase A's 16-byte bulk copies) */ &&
             al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
             al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
             al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&

@@ -46,7 +46,10 @@ constexpr int kSOffRing = 0;
 constexpr int kSOffBm = kSOffRing + kNS * kTileSteps * kStepBytes;  // [kNS][kTileSteps][32] u32
 constexpr int kSOffBar = kSOffBm + kNS * kTileSteps * 128;
 constexpr int kSOffSeg = kSOffBar + 2 * kNS * 8;
-constexpr int kStreamSmem = kSOffSeg + kMaxSeg * 8;
+constexpr int kPenB = 1024;                 // penalty hand-off: table entries per batch (32 per lane)
+constexpr int kSOffPen = kSOffSeg + kMaxSeg * 8;                     // [2][kPenB + 2] UniqEntry (TMA-staged)
+constexpr int kSOffPenBar = kSOffPen + 2 * (kPenB + 2) * 8;          // 2 mbarriers
+constexpr int kStreamSmem = kSOffPenBar + 2 * 8;
 
 // Phase A -> phase B hand-off of one batch row, written by the CTA that holds the row's first step
 // (its penalty warp), so that phase B starts with one round trip and no slot indirection:
@@ -275,6 +278,8 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       mbar_init(full + s, 1);
       mbar_init(empty + s, kCW);
     }
+    mbar_init(reinterpret_cast<uint64_t*>(smem + kSOffPenBar), 1);
+    mbar_init(reinterpret_cast<uint64_t*>(smem + kSOffPenBar) + 1, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -282,6 +287,9 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   if (w == kCW + 1) {
     // ================= penalty warp: the hand-off of the rows that start in this span =================
     const int64_t rfirst = (s0 + a.spr - 1) / a.spr;
+    UniqEntry* pbuf = reinterpret_cast<UniqEntry*>(smem + kSOffPen);
+    uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + kSOffPenBar);
+    uint32_t pphase[2] = {0u, 0u};
     for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
       bool slot_ok;
       const int slot = row_slot(a.slots, (int)r, a.hs.nslots, &slot_ok);
@@ -298,34 +306,47 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
       }
       const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
       const uint8_t* rowp = lg + r * ldb;
-      // batches of 16 entries per lane: every table load, then every logit gather, in flight at once
-      constexpr int PB = 16;
-      for (int e0 = 0; e0 < sm.n_uniq; e0 += 32 * PB) {
-        UniqEntry ue[PB];
-        float raw[PB];
+      // batches of kPenB table entries: the table slice bulk-copied into smem (double-buffered: the
+      // next batch's copy is in flight while this one's logits are gathered, 32 per lane at once)
+      const int nb = (sm.n_uniq + kPenB - 1) / kPenB;
+      auto issue = [&](int j) {  // lane 0: batch j into buffer j & 1; returns the 8-byte skew
+        const int e0 = j * kPenB, n = min(kPenB, sm.n_uniq - e0);
+        const uintptr_t src = reinterpret_cast<uintptr_t>(ut + e0);
+        const uintptr_t s16 = src & ~(uintptr_t)15;
+        const uint32_t bytes = (uint32_t)(((src - s16) + (uintptr_t)n * 8 + 15) & ~(uintptr_t)15);
+        uint64_t* bar = pbar + (j & 1);
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_g2s_nohint(pbuf + (j & 1) * (kPenB + 2), reinterpret_cast<const void*>(s16), bytes, bar);
+      };
+      if (nb > 0 && lane == 0) issue(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb && lane == 0) issue(j + 1);  // (its buffer's previous batch is consumed)
+        mbar_wait(pbar + (j & 1), pphase[j & 1]);
+        pphase[j & 1] ^= 1u;
+        const int e0 = j * kPenB, n = min(kPenB, sm.n_uniq - e0);
+        const UniqEntry* bu = pbuf + (j & 1) * (kPenB + 2) +
+                              ((reinterpret_cast<uintptr_t>(ut + e0) & 15) ? 1 : 0);  // (the skew)
+        float raw[kPenB / 32];
 #pragma unroll
-        for (int q = 0; q < PB; ++q) {
-          const int e = e0 + lane + 32 * q;
-          if (e < sm.n_uniq) ue[q] = ut[e];
-          else ue[q].id = -1;
+        for (int q = 0; q < kPenB / 32; ++q) {
+          const int e = lane + 32 * q;
+          const int le = e < n ? bu[e].id - a.voff : -1;
+          raw[q] = (le >= 0 && le < a.vloc) ? Dec<T>::load1(rowp, le) : 0.f;
         }
 #pragma unroll
-        for (int q = 0; q < PB; ++q) {
-          const int le = ue[q].id - a.voff;
-          raw[q] = (ue[q].id >= 0 && le >= 0 && le < a.vloc) ? Dec<T>::load1(rowp, le) : 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < PB; ++q) {
-          const int e = e0 + lane + 32 * q;
-          if (e >= sm.n_uniq) continue;
-          const int le = ue[q].id - a.voff;
+        for (int q = 0; q < kPenB / 32; ++q) {
+          const int e = lane + 32 * q;
+          if (e >= n) continue;
+          const UniqEntry ue = bu[e];
+          const int le = ue.id - a.voff;
           PenEnt pe;
-          pe.id = ue[q].id;
-          pe.meta = ue[q].meta;
-          pe.zp = (le >= 0 && le < a.vloc) ? apply_penalty(raw[q], ue[q].meta, prm, a.pen_mode) : 0.f;
+          pe.id = ue.id;
+          pe.meta = ue.meta;
+          pe.zp = (le >= 0 && le < a.vloc) ? apply_penalty(raw[q], ue.meta, prm, a.pen_mode) : 0.f;
           pe.pad = 0;
-            a.pent[r * a.hs.L + e] = pe;
+          a.pent[r * a.hs.L + e0 + e] = pe;
         }
+        __syncwarp();  // every lane is done with buffer j & 1 before it is refilled
       }
     }
     if (a.trace && lane == 0) a.trace[blockIdx.x * 64 + 8] = gtimer();
