@@ -131,11 +131,13 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg):
+def load_traffic(cfg, kernel="stream_kernel"):
+    """DRAM bytes read + written per launch of `kernel` at `cfg`, from the committed ncu --set full
+    summary (tools/ncu_summary.py), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(cfg)
+        return d.get(f"{cfg}_{kernel}", d.get(cfg) if kernel == "stream_kernel" else None)
     return None
 
 
@@ -513,7 +515,8 @@ def main():
                    "graph": use_graph},
         "gbs": step_gbs,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": load_traffic(a.config),
+                     "frac": achieved / peak, "traffic": load_traffic(a.config, ["stream_kernel", "select_rows_kernel", "exact_kernel"][kdom] if kt
+                                                       else "stream_kernel"),
                      "peak_source": peak_src,
                      "kernel": ["stream_kernel", "select_rows_kernel", "exact_kernel"][kdom] if kt else "step",
                      "algorithmic_bytes_per_launch": algo,

@@ -1,7 +1,7 @@
 """Summarise an ncu --set full report (read here, no GPU) into profiles/:
    python tools/ncu_summary.py gpurun_out/<tag>/full.ncu-rep <config> <round-tag>
 writes profiles/ncu_<round-tag>_<config>.txt (key metrics per kernel) and updates
-profiles/ncu_traffic.json {config: dram bytes read+write per launch of stream_kernel}."""
+profiles/ncu_traffic.json {config_kernel: dram bytes read+write per launch} (and {config: stream_kernel's})."""
 import csv
 import io
 import json
@@ -46,8 +46,10 @@ def main():
     open(path, "w").write(f"# ncu --set full --clock-control none, {rep}\n" + "\n".join(out) + "\n")
     tj = os.path.join(root, "profiles", "ncu_traffic.json")
     d = json.load(open(tj)) if os.path.exists(tj) else {}
-    d[cfg] = traffic.get("stream_kernel")
-    d[cfg + "_select_rows_kernel"] = traffic.get("select_rows_kernel")
+    for k, v in traffic.items():  # per (config, kernel); bench.py reports the dominant kernel's
+        d[f"{cfg}_{k}"] = v
+    if "stream_kernel" in traffic:
+        d[cfg] = traffic["stream_kernel"]
     json.dump(d, open(tj, "w"), indent=1)
     print(open(path).read())
 
