@@ -74,8 +74,9 @@ enum {
   SAMPLER_ROW_ALL_NEG_INF = 2, /* no token has positive probability */
   SAMPLER_ROW_UNRESOLVED = 3,  /* vocab-sharded merge: the row's kept set is not bounded by the
                                   exchanged candidates (top-p/min-p-only rows, or top_k >
-                                  max_top_k); see DESIGN.md §8 NEXT-1.  Never produced by
-                                  sampler_sample on an unsharded handle. */
+                                  max_top_k); the sampler_resolve_round rounds below finish it
+                                  (DESIGN.md §8 NEXT-1).  Never produced by sampler_sample on an
+                                  unsharded handle. */
   SAMPLER_ROW_INVALID = 4      /* slots_dev[b] outside [0, B_max), or params_dev[b] a parameter set
                                   that sampler_set_params would reject: checked on the device, the
                                   row gets token -1 and logprob NaN, its slot is not touched */
@@ -212,12 +213,57 @@ int sampler_sample_local(sampler* h, const void* logits_slice, int64_t ld, int32
  * blocks of sampler_record_bytes(h,B) bytes, rank order) into the final tokens.  Every rank
  * computes identical outputs (deterministic, rank-ordered reductions).  History append (if
  * requested) is applied on every rank (replicated per-rank tables).  Rows whose kept set is not
- * bounded by the candidates get SAMPLER_ROW_UNRESOLVED. */
+ * bounded by the candidates get SAMPLER_ROW_UNRESOLVED (token -1, no append) and are finished by
+ * the resolve rounds below. */
 int sampler_merge(sampler* h, const void* gathered_records_dev, int32_t world, int32_t B,
                   const int32_t* slots_dev, const sampling_params* params_dev,
                   const uint64_t* seeds_dev, uint64_t step, int32_t append_to_history,
                   int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
                   int32_t* row_status_dev, void* cuda_stream);
+
+/* ---- vocab-sharded rows not bounded by the candidates (NEXT-1) ------------------------
+ * The filter is over the whole renormalised distribution (§2.1 eq.), so a top-p-only,
+ * min-p-only or unfiltered row (or top_k > max_top_k) needs more than the candidate records.  Such
+ * a row is finished, without gathering logits (§5.1 (3)), by a distributed mass-weighted
+ * radix select over the pi-order keys (z' desc, id asc): per round every rank histograms its slice
+ * (256 bins of the next 8 key bits: counts and 128-bit fixed-point masses w*2^80) or, once the
+ * target bin holds <= 638 elements, sends those elements; every rank ingests the same gathered
+ * bytes with integer arithmetic and narrows the same per-row state (top-k cutoff, then top-p
+ * cutoff, then the kept mass per rank, then the owner rank's id-order draw; min-p is an
+ * element-wise test).  DESIGN.md §8 (NEXT-1) has the protocol.
+ *
+ * Usage, after sampler_merge on every rank (same B / slots / params / seeds / step):
+ *   round 0: sampler_resolve_round(..., round=0, gathered=NULL, ...) -> payload
+ *   round r = 1, 2, ...: all-gather the payloads (rank order, world x sampler_resolve_bytes(h,B)
+ *            bytes) and call sampler_resolve_round(..., round=r, gathered, ...) -> next payload;
+ *   stop when *active_dev == 0 after a round (or after sampler_resolve_max_rounds() exchanges,
+ *   which always suffices: capturable in a CUDA graph with a fixed round count).
+ * Resolved rows get their token / logprobs / status SAMPLER_ROW_OK written into the same output
+ * arrays as sampler_merge (and the history append, on every rank, when append_to_history); rows
+ * the merge already decided are not touched.  Rows still unresolved (too few rounds) keep
+ * SAMPLER_ROW_UNRESOLVED.  The handle keeps one state per row between rounds: one resolve sequence
+ * per handle at a time, stream-ordered (ASYNC).
+ * Errors: EINVAL (NULL / misaligned buffers, world not in [1,16], rank not in [0,world), round < 0,
+ * gathered NULL for round > 0), ECUDA. */
+
+/* Bytes of one rank's resolve payload for B rows (16 + 5120 per row). */
+int64_t sampler_resolve_bytes(const sampler* h, int32_t B);
+
+/* ASYNC.  One resolve round on this rank (see above).  logits_slice / ld as for
+ * sampler_sample_local; gathered_dev: the previous round's all-gathered payloads (dev, world x
+ * resolve_bytes, rank order; NULL at round 0); payload_dev (dev, resolve_bytes(h,B), 16-byte
+ * aligned): this round's payload; outputs as for sampler_merge; active_dev (dev int32, nullable):
+ * set to the number of rows still unresolved after this round. */
+int sampler_resolve_round(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
+                          const int32_t* slots_dev, const sampling_params* params_dev,
+                          const uint64_t* seeds_dev, uint64_t step, int32_t round,
+                          const void* gathered_dev, int32_t world, int32_t rank, void* payload_dev,
+                          int32_t append_to_history, int32_t* tokens_dev, float* logprobs_dev,
+                          float* filtered_logprobs_dev, int32_t* row_status_dev,
+                          int32_t* active_dev, void* cuda_stream);
+
+/* Exchanges after which every row is resolved (2 x (8 histogram + 1 gather) + kept mass + draw). */
+int32_t sampler_resolve_max_rounds(void);
 
 /* ---- introspection ------------------------------------------------------------------ */
 

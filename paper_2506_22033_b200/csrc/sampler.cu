@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "exact.cuh"
 #include "merge.cuh"
+#include "resolve.cuh"
 #include "select.cuh"
 #include "stream.cuh"
 
@@ -37,6 +38,7 @@ struct sampler {
   UniqEntry* d_uniq = nullptr;
   int32_t* d_hist = nullptr;
   RowInfo* d_info = nullptr;
+  ResState* d_rs = nullptr;     // [max_batch] NEXT-1 resolve rounds (resolve.cuh)
   uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
   PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
   RowHand* d_hand = nullptr;    // [max_batch] phase A -> B hand-off
@@ -193,6 +195,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
   bool ok = al((void**)&h->d_params, sizeof(sampling_params) * B) &&
             al((void**)&h->d_meta, sizeof(SlotMeta) * B) && al((void**)&h->d_uniq, sizeof(UniqEntry) * (B * L + 4))  /* (+4: phase A's 16-byte bulk copies) */ &&
             al((void**)&h->d_hist, sizeof(int32_t) * B * L) && al((void**)&h->d_info, sizeof(RowInfo) * B) &&
+            al((void**)&h->d_rs, sizeof(ResState) * B) &&
             al((void**)&h->d_gkeys, sizeof(uint16_t) * B * gk_stride(h->Vq)) &&
             al((void**)&h->d_pmask, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) &&
             al((void**)&h->d_hand, sizeof(RowHand) * B) &&  al((void**)&h->d_pent, sizeof(PenEnt) * B * L) &&
@@ -222,6 +225,7 @@ int sampler_create(const sampler_config* cfg, sampler** out) {
       cudaMemset(h->d_meta, 0, sizeof(SlotMeta) * B) != cudaSuccess ||
       cudaMemset(h->d_pmask, 0, sizeof(uint32_t) * B * (h->Vq / kStepVec) * 32) != cudaSuccess ||
       cudaMemset(h->d_info, 0, sizeof(RowInfo) * B) != cudaSuccess ||
+      cudaMemset(h->d_rs, 0, sizeof(ResState) * B) != cudaSuccess ||
       cudaFuncSetAttribute(stream_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kStreamSmem) != cudaSuccess ||
       cudaFuncSetAttribute(stream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem) !=
@@ -263,6 +267,7 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_uniq);
   cudaFree(h->d_hist);
   cudaFree(h->d_info);
+  cudaFree(h->d_rs);
   cudaFree(h->d_trace);
   cudaFree(h->d_gkeys);
   cudaFree(h->d_pmask);
@@ -769,5 +774,66 @@ int sampler_merge(sampler* h, const void* gathered, int32_t world, int32_t B, co
   h->last_launches = 1;
   return SAMPLER_OK;
 }
+
+int64_t sampler_resolve_bytes(const sampler* h, int32_t B) {
+  if (!h || B < 0) return -1;
+  return kResRowBytes * (int64_t)B;
+}
+
+int sampler_resolve_round(sampler* h, const void* logits_slice, int64_t ld, int32_t B, const int32_t* slots_dev,
+                          const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step, int32_t round,
+                          const void* gathered_dev, int32_t world, int32_t rank, void* payload_dev,
+                          int32_t append_to_history, int32_t* tokens_dev, float* logprobs_dev,
+                          float* filtered_logprobs_dev, int32_t* row_status_dev, int32_t* active_dev,
+                          void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  int rc = check_logits(h, logits_slice, ld, B);
+  if (rc) return rc;
+  if (!payload_dev || !tokens_dev || !logprobs_dev) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (((uintptr_t)payload_dev) % 16 || (gathered_dev && ((uintptr_t)gathered_dev) % 16))
+    return fail(h, SAMPLER_EINVAL, "payload / gathered buffers must be 16-byte aligned");
+  if (world < 1 || world > kMaxRec) return fail(h, SAMPLER_EINVAL, "world must be in [1, %d]", kMaxRec);
+  if (rank < 0 || rank >= world) return fail(h, SAMPLER_EINVAL, "rank out of [0, world)");
+  if (round < 0) return fail(h, SAMPLER_EINVAL, "round must be >= 0");
+  if (round > 0 && !gathered_dev) return fail(h, SAMPLER_EINVAL, "gathered_dev is NULL for round > 0");
+  CK(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  ResolveArgs a{};
+  a.logits = (const uint8_t*)logits_slice;
+  a.ld = ld;
+  a.esize = (h->cfg.logits_dtype == SAMPLER_BF16) ? 2 : 4;
+  a.B = B;
+  a.V = h->cfg.vocab_size;
+  a.kcand = h->cfg.max_top_k;
+  a.world = world;
+  a.rank = rank;
+  a.round = round;
+  a.gathered = (const uint8_t*)gathered_dev;
+  a.payload = (uint8_t*)payload_dev;
+  a.slots = slots_dev;
+  a.params_dev = params_dev;
+  a.params_tab = h->d_params;
+  a.seeds = seeds_dev;
+  a.step = step;
+  a.append = append_to_history;
+  a.hs = hist_state(h);
+  a.ro = RowOut{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
+  a.info = h->d_info;
+  a.rs = h->d_rs;
+  a.active = active_dev;
+  a.pen_mode = h->cfg.penalty_mode;
+  if (active_dev) CK(h, cudaMemsetAsync(active_dev, 0, sizeof(int32_t), st));
+  tmark(h, 0, st);
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    resolve_kernel<__nv_bfloat16><<<B, kResThreads, 0, st>>>(a);
+  else
+    resolve_kernel<float><<<B, kResThreads, 0, st>>>(a);
+  CK(h, cudaGetLastError());
+  tmark(h, 1, st);
+  h->last_launches = 1;
+  return SAMPLER_OK;
+}
+
+int32_t sampler_resolve_max_rounds(void) { return kResMaxRounds; }
 
 }  // extern "C"

@@ -27,10 +27,15 @@ def vocab_shard_bounds(V: int, world: int, rank: int, align: int = 8):
 
 
 def sample_vocab_sharded(sampler: Sampler, logits_slice: torch.Tensor, step: int, group=None,
-                         slots=None, params=None, seeds=None, append=False, rec=None, gathered=None, out=None):
+                         slots=None, params=None, seeds=None, append=False, rec=None, gathered=None, out=None,
+                         resolve=True, resolve_rounds=None, resolve_bufs=None):
     """Two-phase vocab-sharded sampling over a torch.distributed process group (NCCL): local candidate
     records -> ONE all_gather_into_tensor (rank order) -> the same deterministic merge on every rank.
-    With rec / gathered / out preallocated the call allocates nothing (CUDA-graph capturable)."""
+    Rows the candidates do not bound (top-p-only / min-p-only / unfiltered, top_k > max_top_k) are then
+    finished by the resolve rounds (NEXT-1, `resolve_unbounded`) unless resolve=False.
+    With rec / gathered / out / resolve_bufs preallocated the call allocates nothing; under CUDA-graph
+    capture the resolve round count defaults to its bound (resolve_max_rounds), so it never synchronises.
+    A caller whose rows are all bounded by top_k <= max_top_k (or greedy) passes resolve=False."""
     B = logits_slice.shape[0]
     rb = sampler.record_bytes(B)
     world = dist.get_world_size(group)
@@ -40,7 +45,40 @@ def sample_vocab_sharded(sampler: Sampler, logits_slice: torch.Tensor, step: int
         gathered = torch.empty(world * rb, dtype=torch.uint8, device=logits_slice.device)
     sampler.sample_local(logits_slice, rec, slots=slots, params=params)
     dist.all_gather_into_tensor(gathered, rec, group=group)
-    return sampler.merge(gathered, world, B, step, slots=slots, params=params, seeds=seeds, append=append, out=out)
+    out = sampler.merge(gathered, world, B, step, slots=slots, params=params, seeds=seeds, append=append, out=out)
+    if resolve:
+        if resolve_rounds is None and logits_slice.is_cuda and torch.cuda.is_current_stream_capturing():
+            resolve_rounds = sampler.resolve_max_rounds()  # no host read inside a graph: the bound
+        resolve_unbounded(sampler, logits_slice, step, out, lambda g, p: dist.all_gather_into_tensor(g, p, group=group),
+                          world, dist.get_rank(group), slots=slots, params=params, seeds=seeds, append=append,
+                          rounds=resolve_rounds, bufs=resolve_bufs)
+    return out
+
+
+def resolve_buffers(sampler: Sampler, B: int, world: int, device):
+    """(payload, gathered, active) buffers for resolve_unbounded."""
+    nb = sampler.resolve_bytes(B)
+    return (torch.empty(nb, dtype=torch.uint8, device=device), torch.empty(world * nb, dtype=torch.uint8, device=device),
+            torch.zeros(1, dtype=torch.int32, device=device))
+
+
+def resolve_unbounded(sampler: Sampler, logits_slice: torch.Tensor, step: int, out: dict, exchange, world: int,
+                      rank: int, slots=None, params=None, seeds=None, append=False, rounds=None, bufs=None):
+    """NEXT-1: finish the rows sampler_merge left SAMPLER_ROW_UNRESOLVED (include/sampler.h, resolve rounds).
+    exchange(gathered, payload) must all-gather the ranks' payloads in rank order (NCCL all_gather_into_tensor).
+    rounds=None: stop as soon as no row is active (one 4-byte device->host read per round); an int: exactly
+    that many exchanges (sampler.resolve_max_rounds() always suffices; CUDA-graph capturable).
+    Returns the number of exchanges issued."""
+    B = logits_slice.shape[0]
+    payload, gathered, active = bufs if bufs is not None else resolve_buffers(sampler, B, world, logits_slice.device)
+    kw = dict(slots=slots, params=params, seeds=seeds, append=append, active=active)
+    sampler.resolve_round(logits_slice, step, 0, None, world, rank, payload, out, **kw)
+    n = 0
+    while (rounds is None and int(active.item()) > 0) or (rounds is not None and n < rounds):
+        exchange(gathered, payload)
+        n += 1
+        sampler.resolve_round(logits_slice, step, n, gathered, world, rank, payload, out, **kw)
+    return n
 
 
 def batch_row_bounds(B: int, world: int, rank: int):

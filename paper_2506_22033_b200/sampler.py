@@ -25,6 +25,7 @@ EXPORTED = [
     "sampler_append_tokens", "sampler_get_history", "sampler_sample", "sampler_debug_distribution",
     "sampler_record_bytes", "sampler_sample_local", "sampler_merge", "sampler_last_launch_count",
     "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
+    "sampler_resolve_bytes", "sampler_resolve_round", "sampler_resolve_max_rounds",
 ]
 
 
@@ -88,6 +89,9 @@ def _load():
         "sampler_record_bytes": ([P, I32], I64),
         "sampler_sample_local": ([P, P, I64, I32, P, P, P, P], I32),
         "sampler_merge": ([P, P, I32, I32, P, P, P, U64, I32, P, P, P, P, P], I32),
+        "sampler_resolve_bytes": ([P, I32], I64),
+        "sampler_resolve_round": ([P, P, I64, I32, P, P, P, U64, I32, P, I32, I32, P, I32, P, P, P, P, P, P], I32),
+        "sampler_resolve_max_rounds": ([], I32),
         "sampler_last_launch_count": ([P], I32),
         "sampler_version": ([], C.c_char_p),
         "sampler_debug_trace": ([P, P, I32], I32),
@@ -260,6 +264,25 @@ class Sampler:
             int(step) & 0xFFFFFFFFFFFFFFFF, int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]),
             _ptr(out.get("filtered_logprobs")), _ptr(out.get("status")), _stream(stream)))
         return out
+
+    # ------------------------------------------------------------------ NEXT-1 resolve rounds
+    def resolve_bytes(self, B) -> int:
+        return int(_lib.sampler_resolve_bytes(self.h, B))
+
+    @staticmethod
+    def resolve_max_rounds() -> int:
+        return int(_lib.sampler_resolve_max_rounds())
+
+    def resolve_round(self, logits_slice, step, rnd, gathered, world, rank, payload, out, slots=None, params=None,
+                      seeds=None, append=False, active=None, stream=None):
+        """One round of the sharded resolve protocol (include/sampler.h, sampler_resolve_round): ingest the
+        previous round's all-gathered payloads (None at round 0), write this round's payload."""
+        B = logits_slice.shape[0]
+        self._check(_lib.sampler_resolve_round(
+            self.h, _ptr(logits_slice), logits_slice.stride(0), B, _ptr(slots), _ptr(params), _ptr(seeds),
+            int(step) & 0xFFFFFFFFFFFFFFFF, int(rnd), _ptr(gathered), int(world), int(rank), _ptr(payload),
+            int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]), _ptr(out.get("filtered_logprobs")),
+            _ptr(out.get("status")), _ptr(active), _stream(stream)))
 
 
 def params_to_device(params, device=0):

@@ -69,6 +69,21 @@ class _StandInSampler:
         self.merged = (gathered.clone(), world, B, step)
         return {"tokens": torch.zeros(B, dtype=torch.int32)}
 
+    # NEXT-1 resolve rounds: payload = (rank, round) pattern; 3 rounds of work, then no row is active
+    def resolve_bytes(self, B):
+        return 16 * B
+
+    def resolve_round(self, logits_slice, step, rnd, gathered, world, rank, payload, out, slots=None, params=None,
+                      seeds=None, append=False, active=None, stream=None):
+        if rnd > 0:
+            pb = payload.numel()
+            ok = all(torch.equal(gathered[r * pb:(r + 1) * pb], torch.full((pb,), 16 * r + rnd - 1, dtype=torch.uint8))
+                     for r in range(world))
+            self.rounds_ok = getattr(self, "rounds_ok", True) and ok
+        self.last_round = rnd
+        payload.fill_(16 * rank + rnd)
+        active.fill_(max(0, 3 - rnd))
+
     def sample(self, logits_rows, step, slots=None, params=None, seeds=None, append=False, out=None):
         # stand-in result: token = 1000 * rank + local row, logprob = -(token) / 8
         n = logits_rows.shape[0]
@@ -86,6 +101,7 @@ def _worker(rank, world, port, q):
         out = sample_vocab_sharded(s, torch.zeros(B, hi - lo), step=3)
         g, w, b, step = s.merged
         ok = w == world and b == B and step == 3 and "tokens" in out
+        ok = ok and s.rounds_ok and s.last_round == 3  # adaptive stop: 3 exchanges, rank-ordered payloads
         rb = s.record_bytes(B)
         for r in range(world):
             v = torch.arange(rb, dtype=torch.int64)

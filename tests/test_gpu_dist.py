@@ -91,3 +91,38 @@ def test_batch_row_sharded_nccl_world1_matches_oracle(nccl_group):
     assert torch.equal(o["tokens"], o["local"]["tokens"])
     assert_parity(wl, o["local"], oracle_run(wl, 2))
     assert np.isfinite(o["logprobs"].cpu().numpy()).all()
+
+
+def test_vocab_sharded_unbounded_rows_nccl_and_graph(nccl_group):
+    """NEXT-1 over NCCL: c2's top-p-only rows through sample_vocab_sharded (merge -> resolve rounds, each an
+    all_gather_into_tensor), eager (adaptive round count) and captured in a CUDA graph with the fixed
+    round count, both against the oracle."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import resolve_buffers, sample_vocab_sharded
+    wl = make_workload("c2", B=8, V=30000)
+    s = Sampler(wl.V, wl.B, max_history=1024, max_top_k=40, dtype=wl.dtype, vocab_offset=0, vocab_local=wl.V)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    x = device_logits(wl)
+    eager = sample_vocab_sharded(s, x, 6)
+    torch.cuda.synchronize()
+    assert (eager["status"] == 0).all()
+    assert_parity(wl, eager, oracle_run(wl, 6))
+    rb = s.record_bytes(wl.B)
+    rec = torch.empty(rb, dtype=torch.uint8, device="cuda")
+    gathered = torch.empty(rb, dtype=torch.uint8, device="cuda")
+    bufs = resolve_buffers(s, wl.B, 1, x.device)
+    out = s._outs(wl.B, None)
+    kw = dict(rec=rec, gathered=gathered, out=out, resolve_rounds=Sampler.resolve_max_rounds(), resolve_bufs=bufs)
+    sample_vocab_sharded(s, x, 6, **kw)  # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        sample_vocab_sharded(s, x, 6, **kw)
+    out["tokens"].fill_(-7)
+    g.replay()
+    torch.cuda.synchronize()
+    for k in ("tokens", "logprobs", "status"):
+        assert torch.equal(out[k], eager[k]), k

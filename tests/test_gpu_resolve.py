@@ -1,0 +1,155 @@
+"""NEXT-1: vocab-sharded rows whose kept set is not bounded by the exchanged candidates (top-p-only,
+min-p-only, unfiltered, top_k > max_top_k) finished by the resolve rounds (include/sampler.h,
+csrc/resolve.cuh), against the float64 oracle.
+
+G vocab slices run on one GPU in lock step with an in-process all-gather (torch.cat of the rank
+payloads): every rank's round r is launched before the gather of round r, so no kernel ever waits on
+another rank's kernel.  The NCCL path (world size 1) and its CUDA-graph capture are in
+test_gpu_dist.py.
+"""
+import numpy as np
+import pytest
+
+from tests._helpers import assert_parity, oracle_run
+from workloads.synth import RowParams, Workload, device_logits, make_workload, random_params
+
+pytestmark = pytest.mark.gpu
+
+
+def sharded_inprocess(wl, x, G, step, append=False, max_top_k=128, rounds=None, max_history=None):
+    """Returns (per-rank outputs, exchanges, the per-rank samplers)."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import vocab_shard_bounds
+    L = max_history or max(64, max(len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)) + 64)
+    shards, xs, recs = [], [], []
+    for r in range(G):
+        lo, hi = vocab_shard_bounds(wl.V, G, r)
+        sh = Sampler(wl.V, wl.B, max_history=L, max_top_k=max_top_k, dtype=wl.dtype, vocab_offset=lo,
+                     vocab_local=hi - lo)
+        sh.set_params(list(range(wl.B)), wl.params)
+        for b in range(wl.B):
+            if wl.prompts[b] or wl.outputs[b]:
+                sh.set_history(b, wl.prompts[b], wl.outputs[b])
+        xs.append(x[:, lo:hi])
+        rec = torch.empty(sh.record_bytes(wl.B), dtype=torch.uint8, device="cuda")
+        sh.sample_local(xs[-1], rec)
+        recs.append(rec)
+        shards.append(sh)
+    gathered = torch.cat(recs)
+    outs = [sh.merge(gathered, G, wl.B, step, append=append) for sh in shards]
+    pays = [torch.empty(sh.resolve_bytes(wl.B), dtype=torch.uint8, device="cuda") for sh in shards]
+    act = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in shards]
+    for g, sh in enumerate(shards):
+        sh.resolve_round(xs[g], step, 0, None, G, g, pays[g], outs[g], append=append, active=act[g])
+    n = 0
+    while (rounds is None and int(act[0].item()) > 0) or (rounds is not None and n < rounds):
+        gathered = torch.cat(pays)
+        n += 1
+        for g, sh in enumerate(shards):
+            sh.resolve_round(xs[g], step, n, gathered, G, g, pays[g], outs[g], append=append, active=act[g])
+    torch.cuda.synchronize()
+    assert all(int(a.item()) == 0 for a in act)
+    return outs, n, shards
+
+
+def _check_all_ranks(wl, outs, orc):
+    import torch
+    for o in outs[1:]:  # every rank computed the same outputs
+        for k in ("tokens", "logprobs", "filtered_logprobs", "status"):
+            assert torch.equal(o[k], outs[0][k]), k
+    assert_parity(wl, outs[0], orc)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_c2_top_p_only_rows_resolved(G):
+    wl = make_workload("c2", B=12, V=40000)
+    x = device_logits(wl)
+    outs, n, _ = sharded_inprocess(wl, x, G, step=3)
+    assert (outs[0]["status"] == 0).all()
+    assert 3 <= n <= 20, n
+    _check_all_ranks(wl, outs, oracle_run(wl, 3))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_mixed_unbounded_params(dtype):
+    """Every kind of row in one batch: top-p only, min-p only, unfiltered, top_k > max_top_k (alone and
+    with top-p / min-p), and rows the merge decides itself (greedy, top-k 40)."""
+    rng = np.random.default_rng(7)
+    wl = make_workload("c2", B=16, V=24000, dtype=dtype)
+    P = [RowParams(temperature=1.0, top_p=0.9), RowParams(temperature=0.8, min_p=0.02),
+         RowParams(temperature=1.2), RowParams(temperature=0.7, top_k=300),
+         RowParams(temperature=1.0, top_k=1000, top_p=0.8), RowParams(temperature=0.9, top_k=500, min_p=0.1),
+         RowParams(temperature=0.0), RowParams(temperature=0.7, top_k=40, top_p=0.9),
+         RowParams(temperature=1.0, top_p=0.5, min_p=0.05), RowParams(temperature=0.3, top_p=0.99),
+         RowParams(temperature=2.0, top_k=129), RowParams(temperature=1.0, top_p=0.999)]
+    for b in range(wl.B):
+        p = P[b] if b < len(P) else random_params(rng, b, wl.V)
+        p.seed, p.request_id = 100 + b, 7000 + b
+        if b % 2:
+            p.repetition_penalty, p.presence_penalty, p.frequency_penalty = 1.2, 0.3, 0.1
+        wl.params[b] = p
+    x = device_logits(wl)
+    for G in (1, 3, 8):
+        outs, n, _ = sharded_inprocess(wl, x, G, step=5)
+        assert (outs[0]["status"] == 0).all(), outs[0]["status"]
+        _check_all_ranks(wl, outs, oracle_run(wl, 5))
+
+
+def test_ties_and_flat_rows_deep_rounds():
+    """All-equal rows (one value: the search descends into the id bits), a few distinct values, an
+    increasing ramp, -inf-masked rows with fewer than top_k finite logits."""
+    B, V = 8, 20000
+    z = np.zeros((B, V), dtype=np.float32)
+    z[0] = 1.5
+    z[1, ::3] = 2.0
+    z[2] = np.arange(V, dtype=np.float32) * np.float32(1e-4)
+    z[3] = -np.inf
+    z[3, 100:160] = np.linspace(-1, 1, 60, dtype=np.float32)
+    z[4] = (np.arange(V) % 5).astype(np.float32)
+    z[5] = -np.inf
+    z[5, 7] = 0.0
+    z[6] = np.float32(-3.0)
+    z[6, 19999] = 0.0
+    z[7] = np.arange(V, dtype=np.float32)[::-1] * np.float32(-1e-3)
+    params = [RowParams(temperature=1.0, top_p=0.5, seed=b, request_id=b) for b in range(B)]
+    params[1] = RowParams(temperature=1.0, top_k=5000, seed=1, request_id=1)
+    params[3] = RowParams(temperature=1.0, top_k=200, seed=3, request_id=3)
+    params[4] = RowParams(temperature=0.5, top_k=9000, top_p=0.7, seed=4, request_id=4)
+    params[5] = RowParams(temperature=1.0, min_p=0.5, seed=5, request_id=5)
+    params[6] = RowParams(temperature=1.0, seed=6, request_id=6)
+    params[7] = RowParams(temperature=0.01, top_p=0.95, seed=7, request_id=7)
+    wl = Workload("ties", B, V, "f32", z, [[]] * B, [[]] * B, params)
+    x = device_logits(wl)
+    for G in (1, 2, 5):
+        outs, n, _ = sharded_inprocess(wl, x, G, step=2)
+        assert (outs[0]["status"] == 0).all(), outs[0]["status"]
+        _check_all_ranks(wl, outs, oracle_run(wl, 2))
+
+
+def test_resolve_fixed_rounds_and_append():
+    """The fixed round count (graph-capturable) gives the same outputs as the adaptive loop; with
+    append the resolved tokens enter every rank's history (replicated tables)."""
+    import torch
+    wl = make_workload("c2", B=6, V=16000)
+    x = device_logits(wl)
+    from paper_2506_22033_b200 import Sampler
+    ad, n, _ = sharded_inprocess(wl, x, 2, step=1)
+    fx, n2, shards = sharded_inprocess(wl, x, 2, step=1, rounds=Sampler.resolve_max_rounds(), append=True)
+    assert n2 == Sampler.resolve_max_rounds() and n <= n2
+    for k in ("tokens", "logprobs", "status"):
+        assert torch.equal(ad[0][k], fx[0][k]), k
+    toks = fx[0]["tokens"].cpu().tolist()
+    for sh in shards:
+        for b in range(wl.B):
+            assert sh.get_history(b)["output"] == list(wl.outputs[b]) + [toks[b]]
+
+
+def test_full_size_c2_vocab_sharded_sampled_rows():
+    """BASELINE's c2 size (B=64, V=152064) vocab-sharded over 8 slices; sampled rows vs the oracle."""
+    wl = make_workload("c2")
+    x = device_logits(wl)
+    outs, n, _ = sharded_inprocess(wl, x, 8, step=11)
+    assert (outs[0]["status"] == 0).all()
+    rows = list(range(0, 64, 7))
+    _check_all_ranks(wl, [outs[0]], oracle_run(wl, 11, rows=rows))
