@@ -77,9 +77,12 @@ enum {
                                   max_top_k); the sampler_resolve_round rounds below finish it
                                   (DESIGN.md §8 NEXT-1).  Never produced by sampler_sample on an
                                   unsharded handle. */
-  SAMPLER_ROW_INVALID = 4      /* slots_dev[b] outside [0, B_max), or params_dev[b] a parameter set
+  SAMPLER_ROW_INVALID = 4,     /* slots_dev[b] outside [0, B_max), or params_dev[b] a parameter set
                                   that sampler_set_params would reject: checked on the device, the
                                   row gets token -1 and logprob NaN, its slot is not touched */
+  SAMPLER_ROW_EXCHANGE_TIMEOUT = 5 /* sampler_sample_exchange: a peer's record for this row did not
+                                  arrive within the handle's timeout (a rank stopped calling);
+                                  token -1, logprob NaN, no append — the GPU is never hung */
 };
 
 typedef struct {
@@ -264,6 +267,47 @@ int sampler_resolve_round(sampler* h, const void* logits_slice, int64_t ld, int3
 
 /* Exchanges after which every row is resolved (2 x (8 histogram + 1 gather) + kept mass + draw). */
 int32_t sampler_resolve_max_rounds(void);
+
+/* ---- NEXT-2: one-shot peer exchange (NVLink P2P stores + flags, no collective call) ----------
+ * The vocab-sharded step of sampler_sample_local -> all-gather -> sampler_merge as ONE call per
+ * rank with no NCCL launch: phase 1's epilogue stores each row's candidate record straight into
+ * every rank's exchange buffer (P2P stores over NVLink / NVSwitch through IPC-mapped pointers) and
+ * raises a per-(rank, row) flag there (system-scope release); the merge kernel waits for every
+ * rank's flag of its row (acquire) and merges its local copies.  Records are double-buffered by a
+ * per-row sequence number (parity), the TSEM versioned-buffer idea (§5.2): no host
+ * synchronisation and no per-step host argument change, so the whole step replays from one CUDA
+ * graph.  Every rank must make the same sequence of sampler_sample_exchange calls (same B).
+ * Rows the candidates do not bound still get SAMPLER_ROW_UNRESOLVED (finish them with the resolve
+ * rounds above). */
+
+/* SYNC.  Allocate this rank's exchange buffer (2 x world x max_batch x record stride bytes of
+ * records + world x max_batch u32 flags, zeroed) on the handle's device.  ipc_handle_out (host,
+ * nullable, 64 bytes = cudaIpcMemHandle_t) receives the buffer's IPC handle for the peers;
+ * base_out (host, nullable) its device address.  timeout_ms: how long a merge waits for a peer
+ * before reporting SAMPLER_ROW_EXCHANGE_TIMEOUT (0 => 10000).  Errors: EINVAL (world not in
+ * [1,16], rank not in [0,world), already initialised), ENOMEM, ECUDA. */
+int sampler_exchange_init(sampler* h, int32_t world, int32_t rank, uint32_t timeout_ms,
+                          void* ipc_handle_out, void** base_out);
+
+/* SYNC.  Map every peer's buffer from the world x 64 bytes of IPC handles (host, rank order; this
+ * rank's own entry is ignored) with cudaIpcOpenMemHandle (peer access enabled lazily).  The
+ * mappings are closed by sampler_destroy.  Errors: EINVAL, ECUDA (a handle could not be opened). */
+int sampler_exchange_open(sampler* h, const void* ipc_handles);
+
+/* SYNC.  Alternative to sampler_exchange_open for buffers already addressable in this process (several
+ * handles of one process, or mappings the caller made): bases_host[q] = rank q's buffer as returned
+ * by its sampler_exchange_init base_out; bases_host[rank] must be this handle's own. */
+int sampler_exchange_set_peers(sampler* h, void* const* bases_host);
+
+/* ASYNC.  The vocab-sharded step through the peer exchange.  Arguments as sampler_sample_local +
+ * sampler_merge.  phases: 1 = local pass + publish (no outputs), 2 = wait + merge, 3 = both (the
+ * normal call; 1 and 2 let several ranks of ONE process and GPU run in lock step without any kernel
+ * waiting on a kernel queued behind it). */
+int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
+                            const int32_t* slots_dev, const sampling_params* params_dev,
+                            const uint64_t* seeds_dev, uint64_t step, int32_t append_to_history,
+                            int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                            int32_t* row_status_dev, int32_t phases, void* cuda_stream);
 
 /* ---- introspection ------------------------------------------------------------------ */
 

@@ -6,5 +6,5 @@ of include/sampler.h.  See DESIGN.md.
 """
 from .sampler import (  # noqa: F401
     Sampler, SamplingParams, SamplerError, pack_params, params_to_device, version, lib, EXPORTED,
-    ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED, ROW_INVALID, PEN_OPENAI_CTRL, PEN_LINEAR,
+    ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED, ROW_INVALID, ROW_EXCHANGE_TIMEOUT, PEN_OPENAI_CTRL, PEN_LINEAR,
 )

@@ -76,6 +76,35 @@ struct __align__(16) RowInfo {
 };
 constexpr int32_t kRowPending = 100;
 
+// ---- NEXT-2: one-shot peer exchange of the vocab-sharded records (sampler_sample_exchange) ----
+// Every rank owns one exchange buffer: [2 parities][world ranks][B_max rows][rec_stride] records
+// followed by [world][B_max] u32 flags.  Rank q's phase 1 stores row r's record straight into every
+// peer's buffer (NVLink P2P stores through IPC-mapped pointers) at (parity, q, r) and then raises
+// flag (q, r) of every peer to the row's sequence number (release, system scope); a peer's merge
+// waits for flag (q, r) >= its own sequence number for every q (acquire) and reads its local copy.
+// seq[r] counts the exchanges of batch row r on this handle (all ranks make the same calls, so
+// the numbers agree); parity = seq & 1 double-buffers the records (a rank runs at most one step
+// ahead of a peer: its next merge waits for that peer's next phase 1).
+struct ExchPeers {
+  uint8_t* const* bases;  // [world] device pointers (this process' mappings of every rank's buffer)
+  int world, rank;
+  int64_t row_stride;     // rec_stride
+  int64_t rank_pitch;     // B_max * rec_stride
+  int64_t par_pitch;      // world * rank_pitch
+  int64_t flags_off;      // bytes from a base to its flags
+  int nslots;             // B_max
+  uint32_t* seq;          // [B_max] local sequence numbers
+  uint64_t timeout_ns;
+};
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- order-preserving keys ----------------------------------------------------------
 // key(f) is monotone in f (as a float, -0 canonicalised to +0 so that equal values tie);
 // composite = key << 32 | (0xFFFFFFFF - id) orders by (z' desc, id asc) when sorted

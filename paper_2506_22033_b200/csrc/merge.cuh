@@ -530,6 +530,7 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
       e.id = tok;
       e.meta = 2u;
       u[less] = e;
+      pmask_set(hs, slot, tok);  // the id is penalised from the next step on (phase A's presence bitmap)
     }
     hs.tokens[(int64_t)slot * hs.L + np + no] = tok;
     SlotMeta m2 = smeta;
@@ -559,6 +560,7 @@ struct MergeArgs {
   RowOut ro;
   uint64_t* trace;  // debug: per-row phase timestamps (32 per row), nullable
   int pen_mode;
+  ExchPeers xp;     // xp.world > 0: records come from the one-shot peer exchange (NEXT-2)
 };
 constexpr int kMergeKernelSmem = kPool * 8 + 3 * SAMPLER_KCAND_MAX * 8 + kMaxRec * 48 + (kMaxRec + 1) * 4 + 12 + 512;
 
@@ -584,7 +586,41 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
   const int slot = row_slot(m.slots, r, m.hs.nslots, &slot_ok);
   const sampling_params prm = m.params_dev ? m.params_dev[r] : m.params_tab[slot];
   const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
-  block_merge_row(m.records + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step, m.V,
+  const uint8_t* recs = m.records;
+  if (m.xp.world > 0) {  // NEXT-2: wait for every rank's flag of this row, then read the local copies
+    const ExchPeers& x = m.xp;
+    const uint32_t sq = x.seq[r];
+    if (threadIdx.x == 0) {
+      const uint32_t* fl = reinterpret_cast<const uint32_t*>(x.bases[x.rank] + x.flags_off);
+      const uint64_t t0 = gtimer();
+      int timed_out = 0;
+      for (int q = 0; q < x.world && !timed_out; ++q) {
+        while ((int32_t)(ld_acquire_sys(fl + (int64_t)q * x.nslots + r) - sq) < 0) {
+          if (gtimer() - t0 > x.timeout_ns) {
+            timed_out = 1;
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      ms.bs.i[2] = timed_out;
+    }
+    cbar();
+    if (ms.bs.i[2]) {  // a peer never published: report the row, never hang the GPU
+      if (threadIdx.x == 0) {
+        m.ro.tokens[r] = -1;
+        m.ro.logprobs[r] = NAN;
+        if (m.ro.flogprobs) m.ro.flogprobs[r] = NAN;
+        if (m.ro.status) m.ro.status[r] = SAMPLER_ROW_EXCHANGE_TIMEOUT;
+        RowInfo ri{};
+        ri.status = SAMPLER_ROW_EXCHANGE_TIMEOUT;
+        m.ro.info[r] = ri;
+      }
+      return;
+    }
+    recs = x.bases[x.rank] + (int64_t)(sq & 1) * x.par_pitch;
+  }
+  block_merge_row(recs + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step, m.V,
                   m.kcand, 0, nullptr, m.ro, m.append, m.hs, false, !slot_ok || !params_ok(prm, m.pen_mode), ms, tr);
 }
 

@@ -39,6 +39,14 @@ struct sampler {
   int32_t* d_hist = nullptr;
   RowInfo* d_info = nullptr;
   ResState* d_rs = nullptr;     // [max_batch] NEXT-1 resolve rounds (resolve.cuh)
+  // NEXT-2 one-shot peer exchange (common.cuh ExchPeers)
+  uint8_t* d_xbuf = nullptr;     // this rank's exchange buffer (records x 2 parities + flags)
+  uint8_t** d_xbases = nullptr;  // [world] device copy of every rank's mapped base
+  uint32_t* d_xseq = nullptr;    // [max_batch]
+  std::vector<void*> x_opened;   // IPC mappings to close
+  int x_world = 0, x_rank = 0;
+  int64_t x_bytes = 0;
+  uint64_t x_timeout_ns = 0;
   uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
   PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
   RowHand* d_hand = nullptr;    // [max_batch] phase A -> B hand-off
@@ -268,6 +276,10 @@ int sampler_destroy(sampler* h) {
   cudaFree(h->d_hist);
   cudaFree(h->d_info);
   cudaFree(h->d_rs);
+  for (void* p : h->x_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(h->d_xbuf);
+  cudaFree(h->d_xbases);
+  cudaFree(h->d_xseq);
   cudaFree(h->d_trace);
   cudaFree(h->d_gkeys);
   cudaFree(h->d_pmask);
@@ -835,5 +847,130 @@ int sampler_resolve_round(sampler* h, const void* logits_slice, int64_t ld, int3
 }
 
 int32_t sampler_resolve_max_rounds(void) { return kResMaxRounds; }
+
+// ---- NEXT-2: one-shot peer exchange --------------------------------------------------------
+static ExchPeers exch_peers(const sampler* h) {
+  ExchPeers x{};
+  x.bases = h->d_xbases;
+  x.world = h->x_world;
+  x.rank = h->x_rank;
+  x.row_stride = h->rec_stride;
+  x.rank_pitch = h->rec_stride * (int64_t)h->cfg.max_batch;
+  x.par_pitch = x.rank_pitch * h->x_world;
+  x.flags_off = 2 * x.par_pitch;
+  x.nslots = h->cfg.max_batch;
+  x.seq = h->d_xseq;
+  x.timeout_ns = h->x_timeout_ns;
+  return x;
+}
+
+int sampler_exchange_init(sampler* h, int32_t world, int32_t rank, uint32_t timeout_ms, void* ipc_handle_out,
+                          void** base_out) {
+  if (!h) return SAMPLER_EINVAL;
+  if (world < 1 || world > kMaxRec) return fail(h, SAMPLER_EINVAL, "world must be in [1, %d]", kMaxRec);
+  if (rank < 0 || rank >= world) return fail(h, SAMPLER_EINVAL, "rank out of [0, world)");
+  if (h->d_xbuf) return fail(h, SAMPLER_EINVAL, "exchange already initialised on this handle");
+  CK(h, cudaSetDevice(h->cfg.device));
+  const int64_t Bm = h->cfg.max_batch;
+  const int64_t bytes = 2 * (int64_t)world * Bm * h->rec_stride + (int64_t)world * Bm * 4;
+  if (cudaMalloc((void**)&h->d_xbuf, bytes) != cudaSuccess || cudaMalloc((void**)&h->d_xbases, sizeof(void*) * world) != cudaSuccess ||
+      cudaMalloc((void**)&h->d_xseq, sizeof(uint32_t) * Bm) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, SAMPLER_ENOMEM, "exchange buffer allocation failed");
+  }
+  CK(h, cudaMemset(h->d_xbuf, 0, bytes));
+  CK(h, cudaMemset(h->d_xseq, 0, sizeof(uint32_t) * Bm));
+  h->x_world = world;
+  h->x_rank = rank;
+  h->x_bytes = bytes;
+  h->x_timeout_ns = (uint64_t)(timeout_ms ? timeout_ms : 10000) * 1000000ull;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t ih;
+    CK(h, cudaIpcGetMemHandle(&ih, h->d_xbuf));
+    memcpy(ipc_handle_out, &ih, sizeof(ih));
+  }
+  if (base_out) *base_out = h->d_xbuf;
+  return SAMPLER_OK;
+}
+
+static int exch_upload(sampler* h, const std::vector<uint8_t*>& b) {
+  CK(h, cudaMemcpy(h->d_xbases, b.data(), sizeof(void*) * b.size(), cudaMemcpyHostToDevice));
+  return SAMPLER_OK;
+}
+
+int sampler_exchange_open(sampler* h, const void* ipc_handles) {
+  if (!h || !ipc_handles) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (!h->d_xbuf) return fail(h, SAMPLER_EINVAL, "sampler_exchange_init first");
+  CK(h, cudaSetDevice(h->cfg.device));
+  std::vector<uint8_t*> b(h->x_world);
+  for (int q = 0; q < h->x_world; ++q) {
+    if (q == h->x_rank) {
+      b[q] = h->d_xbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, (const uint8_t*)ipc_handles + (size_t)q * sizeof(ih), sizeof(ih));
+    void* p = nullptr;
+    CK(h, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->x_opened.push_back(p);
+    b[q] = (uint8_t*)p;
+  }
+  return exch_upload(h, b);
+}
+
+int sampler_exchange_set_peers(sampler* h, void* const* bases_host) {
+  if (!h || !bases_host) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (!h->d_xbuf) return fail(h, SAMPLER_EINVAL, "sampler_exchange_init first");
+  CK(h, cudaSetDevice(h->cfg.device));
+  std::vector<uint8_t*> b(h->x_world);
+  for (int q = 0; q < h->x_world; ++q) {
+    if (!bases_host[q]) return fail(h, SAMPLER_EINVAL, "NULL peer base");
+    b[q] = (uint8_t*)bases_host[q];
+  }
+  if (b[h->x_rank] != h->d_xbuf) return fail(h, SAMPLER_EINVAL, "bases[rank] must be this handle's own buffer");
+  return exch_upload(h, b);
+}
+
+int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, int32_t B, const int32_t* slots_dev,
+                            const sampling_params* params_dev, const uint64_t* seeds_dev, uint64_t step,
+                            int32_t append, int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                            int32_t* row_status_dev, int32_t phases, void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  if (!h->d_xbuf) return fail(h, SAMPLER_EINVAL, "sampler_exchange_init / open first");
+  if (phases < 1 || phases > 3) return fail(h, SAMPLER_EINVAL, "phases must be 1, 2 or 3");
+  int rc = check_logits(h, logits_slice, ld, B);
+  if (rc) return rc;
+  if ((phases & 2) && (!tokens_dev || !logprobs_dev)) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  CK(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int nk = 0;
+  tmark(h, 0, st);
+  if (phases & 1) {
+    const LaunchPlan lp = plan(h, B);
+    rc = launch_stream(h, stream_args(h, logits_slice, ld, B, slots_dev, params_dev, lp), lp.grid, st);
+    if (rc) return rc;
+    tmark(h, ++nk, st);
+    RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
+    SelectArgs s = select_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, ro, lp);
+    s.mode = 1;
+    s.xp = exch_peers(h);
+    rc = launch_select(h, s, B, st);
+    if (rc) return rc;
+    tmark(h, ++nk, st);
+  }
+  if (phases & 2) {
+    RowOut ro{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
+    MergeArgs m = merge_args(h, slots_dev, params_dev, seeds_dev, step, append, ro);
+    m.xp = exch_peers(h);
+    m.records = h->d_xbuf;
+    m.rank_pitch = m.xp.rank_pitch;
+    m.world = h->x_world;
+    rc = launch_merge(h, m, B, st);
+    if (rc) return rc;
+    tmark(h, ++nk, st);
+  }
+  h->last_launches = nk;
+  return SAMPLER_OK;
+}
 
 }  // extern "C"

@@ -54,6 +54,7 @@ struct SelectArgs {
   RowOut ro;
   uint8_t* out_records;  // mode 1: one candidate record per row
   int64_t out_stride;
+  ExchPeers xp;          // mode 1 with xp.world > 0: records stored into every peer (NEXT-2)
   uint64_t* trace;       // debug: per-row phase timestamps (32 per row), nullable
 };
 
@@ -791,19 +792,38 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
   if (nc > keff) F = ms.top[keff - 1] > F ? ms.top[keff - 1] : F;
 
   if (a.mode == 1) {  // ---- vocab-sharded phase 1: the row's candidate record
-    uint8_t* out = a.out_records + (int64_t)r * a.out_stride;
-    uint64_t* oe = reinterpret_cast<uint64_t*>(out + kRecHdrBytes);
-    for (int i = tid; i < n; i += kBT) oe[i] = ms.top[i];
+    RecHdr h;
+    h.m = M;
+    h.flags = bad ? kRecBad : 0u;
+    h.s = S;
+    h.R = (double)M * rc.c_d;
+    h.n = (uint32_t)n;
+    h.rsv = 0;
+    h.frontier = F;
+    if (a.xp.world == 0) {
+      uint8_t* out = a.out_records + (int64_t)r * a.out_stride;
+      uint64_t* oe = reinterpret_cast<uint64_t*>(out + kRecHdrBytes);
+      for (int i = tid; i < n; i += kBT) oe[i] = ms.top[i];
+      if (tid == 0) *reinterpret_cast<RecHdr*>(out) = h;
+      return;
+    }
+    // NEXT-2: the record goes straight into every peer's exchange buffer (P2P stores), then the
+    // row's flag on every peer is raised (one system-scope release after the CTA barrier)
+    const ExchPeers& x = a.xp;
+    const uint32_t sq = x.seq[r] + 1;
+    const int64_t off = (int64_t)(sq & 1) * x.par_pitch + (int64_t)x.rank * x.rank_pitch + (int64_t)r * x.row_stride;
+    for (int p = 0; p < x.world; ++p) {
+      uint8_t* out = x.bases[p] + off;
+      uint64_t* oe = reinterpret_cast<uint64_t*>(out + kRecHdrBytes);
+      for (int i = tid; i < n; i += kBT) oe[i] = ms.top[i];
+      if (tid == 0) *reinterpret_cast<RecHdr*>(out) = h;
+    }
+    cbar();
     if (tid == 0) {
-      RecHdr h;
-      h.m = M;
-      h.flags = bad ? kRecBad : 0u;
-      h.s = S;
-      h.R = (double)M * rc.c_d;
-      h.n = (uint32_t)n;
-      h.rsv = 0;
-      h.frontier = F;
-      *reinterpret_cast<RecHdr*>(out) = h;
+      __threadfence_system();
+      x.seq[r] = sq;
+      for (int p = 0; p < x.world; ++p)
+        st_release_sys(reinterpret_cast<uint32_t*>(x.bases[p] + x.flags_off) + (int64_t)x.rank * x.nslots + r, sq);
     }
     return;
   }

@@ -55,6 +55,36 @@ def sample_vocab_sharded(sampler: Sampler, logits_slice: torch.Tensor, step: int
     return out
 
 
+def setup_peer_exchange(sampler: Sampler, group=None, timeout_ms=0):
+    """NEXT-2 plumbing: allocate this rank's exchange buffer, all-gather the 64-byte CUDA IPC handles
+    (rank order) over the process group, map every peer's buffer (sampler_exchange_open)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    h, _ = sampler.exchange_init(world, rank, timeout_ms)
+    allh = [None] * world
+    dist.all_gather_object(allh, h, group=group)
+    sampler.exchange_open(b"".join(allh))
+    return allh
+
+
+def sample_vocab_sharded_p2p(sampler: Sampler, logits_slice: torch.Tensor, step: int, group=None, slots=None,
+                             params=None, seeds=None, append=False, out=None, resolve=False, resolve_rounds=None,
+                             resolve_bufs=None):
+    """The vocab-sharded step through the one-shot peer exchange (one library call, no NCCL launch; after
+    setup_peer_exchange).  Rows not bounded by the candidates can be finished by the resolve rounds
+    (resolve=True; those rounds use NCCL all-gathers)."""
+    out = sampler.sample_exchange(logits_slice, step, slots=slots, params=params, seeds=seeds, append=append,
+                                  out=out)
+    if resolve:
+        world = dist.get_world_size(group)
+        if resolve_rounds is None and logits_slice.is_cuda and torch.cuda.is_current_stream_capturing():
+            resolve_rounds = sampler.resolve_max_rounds()
+        resolve_unbounded(sampler, logits_slice, step, out, lambda g, p: dist.all_gather_into_tensor(g, p, group=group),
+                          world, dist.get_rank(group), slots=slots, params=params, seeds=seeds, append=append,
+                          rounds=resolve_rounds, bufs=resolve_bufs)
+    return out
+
+
 def resolve_buffers(sampler: Sampler, B: int, world: int, device):
     """(payload, gathered, active) buffers for resolve_unbounded."""
     nb = sampler.resolve_bytes(B)

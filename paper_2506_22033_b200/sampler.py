@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsampler_b200.so")
 SAMPLER_OK, SAMPLER_EINVAL, SAMPLER_ENOMEM, SAMPLER_ECUDA, SAMPLER_ERANGE, SAMPLER_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 SAMPLER_F32, SAMPLER_BF16 = 0, 2
 PEN_OPENAI_CTRL, PEN_LINEAR = 0, 1
-ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED, ROW_INVALID = 0, 1, 2, 3, 4
+ROW_OK, ROW_NONFINITE, ROW_ALL_NEG_INF, ROW_UNRESOLVED, ROW_INVALID, ROW_EXCHANGE_TIMEOUT = 0, 1, 2, 3, 4, 5
 
 EXPORTED = [
     "sampler_create", "sampler_destroy", "sampler_last_error", "sampler_set_params", "sampler_set_history",
@@ -26,6 +26,7 @@ EXPORTED = [
     "sampler_record_bytes", "sampler_sample_local", "sampler_merge", "sampler_last_launch_count",
     "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
     "sampler_resolve_bytes", "sampler_resolve_round", "sampler_resolve_max_rounds",
+    "sampler_exchange_init", "sampler_exchange_open", "sampler_exchange_set_peers", "sampler_sample_exchange",
 ]
 
 
@@ -92,6 +93,10 @@ def _load():
         "sampler_resolve_bytes": ([P, I32], I64),
         "sampler_resolve_round": ([P, P, I64, I32, P, P, P, U64, I32, P, I32, I32, P, I32, P, P, P, P, P, P], I32),
         "sampler_resolve_max_rounds": ([], I32),
+        "sampler_exchange_init": ([P, I32, I32, C.c_uint32, P, P], I32),
+        "sampler_exchange_open": ([P, P], I32),
+        "sampler_exchange_set_peers": ([P, P], I32),
+        "sampler_sample_exchange": ([P, P, I64, I32, P, P, P, U64, I32, P, P, P, P, I32, P], I32),
         "sampler_last_launch_count": ([P], I32),
         "sampler_version": ([], C.c_char_p),
         "sampler_debug_trace": ([P, P, I32], I32),
@@ -283,6 +288,32 @@ class Sampler:
             int(step) & 0xFFFFFFFFFFFFFFFF, int(rnd), _ptr(gathered), int(world), int(rank), _ptr(payload),
             int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]), _ptr(out.get("filtered_logprobs")),
             _ptr(out.get("status")), _ptr(active), _stream(stream)))
+
+    # ------------------------------------------------------------------ NEXT-2 one-shot peer exchange
+    def exchange_init(self, world, rank, timeout_ms=0):
+        """Returns (64-byte IPC handle as bytes, device base address)."""
+        hbuf = (C.c_uint8 * 64)()
+        base = C.c_void_p()
+        self._check(_lib.sampler_exchange_init(self.h, int(world), int(rank), int(timeout_ms), hbuf, C.byref(base)))
+        return bytes(hbuf), int(base.value or 0)
+
+    def exchange_open(self, handles: bytes):
+        buf = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+        self._check(_lib.sampler_exchange_open(self.h, buf))
+
+    def exchange_set_peers(self, bases):
+        arr = (C.c_void_p * len(bases))(*bases)
+        self._check(_lib.sampler_exchange_set_peers(self.h, arr))
+
+    def sample_exchange(self, logits_slice, step, slots=None, params=None, seeds=None, append=False, out=None,
+                        phases=3, stream=None):
+        B = logits_slice.shape[0]
+        out = self._outs(B, out)
+        self._check(_lib.sampler_sample_exchange(
+            self.h, _ptr(logits_slice), logits_slice.stride(0), B, _ptr(slots), _ptr(params), _ptr(seeds),
+            int(step) & 0xFFFFFFFFFFFFFFFF, int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]),
+            _ptr(out.get("filtered_logprobs")), _ptr(out.get("status")), int(phases), _stream(stream)))
+        return out
 
 
 def params_to_device(params, device=0):

@@ -17,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2506_22033_b200.distributed import (batch_row_bounds, sample_batch_sharded, sample_vocab_sharded,
-                                               vocab_shard_bounds)
+                                               setup_peer_exchange, vocab_shard_bounds)
 
 
 def _free_port():
@@ -69,6 +69,13 @@ class _StandInSampler:
         self.merged = (gathered.clone(), world, B, step)
         return {"tokens": torch.zeros(B, dtype=torch.int32)}
 
+    # NEXT-2: exchange buffer handles (64 bytes, rank-specific) and the peer mapping call
+    def exchange_init(self, world, rank, timeout_ms=0):
+        return bytes([rank + 1]) * 64, 0x1000 * (rank + 1)
+
+    def exchange_open(self, handles):
+        self.opened = handles
+
     # NEXT-1 resolve rounds: payload = (rank, round) pattern; 3 rounds of work, then no row is active
     def resolve_bytes(self, B):
         return 16 * B
@@ -106,6 +113,9 @@ def _worker(rank, world, port, q):
         for r in range(world):
             v = torch.arange(rb, dtype=torch.int64)
             ok = ok and torch.equal(g[r * rb:(r + 1) * rb], ((v + 31 * r + 7) % 251).to(torch.uint8))
+        # NEXT-2: every rank maps every rank's exchange buffer from the handles, in rank order
+        setup_peer_exchange(s)
+        ok = ok and s.opened == b"".join(bytes([r + 1]) * 64 for r in range(world))
         # batch-row sharding of one global batch of 7 rows: every rank ends with the whole result
         Bg = 7
         blo, bhi = batch_row_bounds(Bg, world, rank)

@@ -126,3 +126,86 @@ def test_vocab_sharded_unbounded_rows_nccl_and_graph(nccl_group):
     torch.cuda.synchronize()
     for k in ("tokens", "logprobs", "status"):
         assert torch.equal(out[k], eager[k]), k
+
+
+def test_peer_exchange_nccl_world1_graph_replays(nccl_group):
+    """NEXT-2 on a real process group: setup_peer_exchange (handle all-gather) + sample_vocab_sharded_p2p,
+    the step captured ONCE in a CUDA graph and replayed for several decode steps (per-row sequence numbers
+    and record parities advance on the device): every replay equals the unsharded sampler's step."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import sample_vocab_sharded_p2p, setup_peer_exchange
+    wl = make_workload("c3", B=16, V=12000)
+    x = device_logits(wl)
+    full = make_sampler(wl)
+    s = Sampler(wl.V, wl.B, max_history=1024, max_top_k=40, dtype=wl.dtype, vocab_offset=0, vocab_local=wl.V)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    setup_peer_exchange(s)
+    eager = sample_vocab_sharded_p2p(s, x, 0, append=True)
+    ref = full.sample(x, 0, append=True)
+    torch.cuda.synchronize()
+    assert torch.equal(eager["tokens"], ref["tokens"])
+    assert_parity(wl, eager, oracle_run(wl, 0))
+    out = s._outs(wl.B, None)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        sample_vocab_sharded_p2p(s, x, 5, out=out, append=True)
+    for _ in range(3):
+        g.replay()
+        ref = full.sample(x, 5, append=True)
+        torch.cuda.synchronize()
+        assert (out["status"] == 0).all()
+        assert torch.equal(out["tokens"], ref["tokens"])
+
+
+def _ipc_worker(rank, port, q):
+    """One of two processes on the SAME GPU: CUDA IPC mapping of the other's exchange buffer (gloo for
+    the handle exchange and the barriers).  Publish, barrier, merge: no kernel waits on the other process."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2506_22033_b200 import Sampler
+        from paper_2506_22033_b200.distributed import setup_peer_exchange, vocab_shard_bounds
+        wl = make_workload("c3", B=8, V=16000)
+        x = device_logits(wl)
+        lo, hi = vocab_shard_bounds(wl.V, 2, rank)
+        s = Sampler(wl.V, wl.B, max_history=1024, dtype=wl.dtype, vocab_offset=lo, vocab_local=hi - lo)
+        s.set_params(list(range(wl.B)), wl.params)
+        for b in range(wl.B):
+            s.set_history(b, wl.prompts[b], wl.outputs[b])
+        setup_peer_exchange(s)
+        ok = True
+        for step in range(3):
+            s.sample_exchange(x[:, lo:hi], step, phases=1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            o = s.sample_exchange(x[:, lo:hi], step, phases=2)
+            torch.cuda.synchronize()
+            dist.barrier()
+            full = make_sampler(wl)
+            ref = full.sample(x, step)
+            torch.cuda.synchronize()
+            ok = ok and bool((o["status"] == 0).all()) and torch.equal(o["tokens"], ref["tokens"])
+        q.put((rank, ok))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_ipc_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res

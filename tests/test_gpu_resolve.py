@@ -153,3 +153,68 @@ def test_full_size_c2_vocab_sharded_sampled_rows():
     assert (outs[0]["status"] == 0).all()
     rows = list(range(0, 64, 7))
     _check_all_ranks(wl, [outs[0]], oracle_run(wl, 11, rows=rows))
+
+
+# ---------------------------------------------------------------- NEXT-2: one-shot peer exchange
+def _exchange_shards(wl, G, timeout_ms=0, max_top_k=128):
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import vocab_shard_bounds
+    L = max(64, max(len(p) + len(o) for p, o in zip(wl.prompts, wl.outputs)) + 64)
+    shards, bounds = [], []
+    for g in range(G):
+        lo, hi = vocab_shard_bounds(wl.V, G, g)
+        sh = Sampler(wl.V, wl.B, max_history=L, max_top_k=max_top_k, dtype=wl.dtype, vocab_offset=lo,
+                     vocab_local=hi - lo)
+        sh.set_params(list(range(wl.B)), wl.params)
+        for b in range(wl.B):
+            if wl.prompts[b] or wl.outputs[b]:
+                sh.set_history(b, wl.prompts[b], wl.outputs[b])
+        shards.append(sh)
+        bounds.append((lo, hi))
+    bases = [sh.exchange_init(G, g, timeout_ms)[1] for g, sh in enumerate(shards)]
+    for sh in shards:
+        sh.exchange_set_peers(bases)
+    return shards, bounds
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_peer_exchange_inprocess_decode_steps(G):
+    """G ranks of one process on one GPU in lock step (every rank's publish before any rank's merge):
+    records stored into every rank's buffer by phase 1, flags, double-buffered parities over several
+    decode steps with append — tokens equal the unsharded sampler's at every step, step 0 vs the oracle."""
+    import torch
+    from tests._helpers import make_sampler
+    wl = make_workload("c3", B=24, V=30000)
+    x = device_logits(wl)
+    full = make_sampler(wl)
+    shards, bounds = _exchange_shards(wl, G)
+    for step in range(4):
+        ref = full.sample(x, step, append=True)
+        for g, sh in enumerate(shards):
+            sh.sample_exchange(x[:, bounds[g][0]:bounds[g][1]], step, append=True, phases=1)
+        outs = [sh.sample_exchange(x[:, bounds[g][0]:bounds[g][1]], step, append=True, phases=2)
+                for g, sh in enumerate(shards)]
+        torch.cuda.synchronize()
+        for o in outs:
+            assert (o["status"] == 0).all()
+            assert torch.equal(o["tokens"], ref["tokens"])
+            assert torch.allclose(o["logprobs"], ref["logprobs"], rtol=1e-5, atol=1e-6)
+        if step == 0:
+            assert_parity(wl, outs[0], oracle_run(wl, 0))
+    for sh in shards:  # replicated histories stayed in step with the unsharded handle
+        for b in (0, wl.B - 1):
+            assert sh.get_history(b)["output"] == full.get_history(b)["output"]
+
+
+def test_peer_exchange_timeout_reports_rows():
+    """A merge whose peer never publishes reports SAMPLER_ROW_EXCHANGE_TIMEOUT after the timeout instead of
+    hanging the GPU."""
+    import torch
+    from paper_2506_22033_b200 import ROW_EXCHANGE_TIMEOUT
+    wl = make_workload("c3", B=4, V=8000)
+    x = device_logits(wl)
+    shards, bounds = _exchange_shards(wl, 2, timeout_ms=50)
+    shards[0].sample_exchange(x[:, bounds[0][0]:bounds[0][1]], 0, phases=1)   # rank 1 never publishes
+    o = shards[0].sample_exchange(x[:, bounds[0][0]:bounds[0][1]], 0, phases=2)
+    torch.cuda.synchronize()
+    assert (o["status"] == ROW_EXCHANGE_TIMEOUT).all() and (o["tokens"] == -1).all()
