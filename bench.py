@@ -7,7 +7,9 @@ logprobs -> history append), BASELINE.json metric:
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard rows|split|vocab]
       --shard rows  (default) every rank samples its own batch of the config (replicas, weak scaling)
       --shard split one global batch split by rows across the ranks (batch-row sharding, strong)
-      --shard vocab one global batch split by vocabulary (TP lm_head style; strong)
+      --shard vocab one global batch split by vocabulary (TP lm_head style; strong); also at
+                    N=1 (world-1 process group) to time the sharded step's own overheads
+      --exchange p2p|nccl  vocab mode: one-shot peer exchange (default) or an NCCL all-gather
     python bench.py --impl reference ...      # the float64 CPU oracle as the reference arm
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on
@@ -46,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--batch", type=int, default=None, help="override B (c5 latency sweep)")
     ap.add_argument("--shard", default="rows", choices=["rows", "split", "vocab"])
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="--shard vocab: one-shot P2P record stores + flags (NEXT-2) or an NCCL all-gather")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -283,9 +287,14 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or a.shard == "vocab":
+        if world == 1:  # world-1 group: the vocab-sharded code path on one GPU
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
-    vocab_mode = world > 1 and a.shard == "vocab"
+    vocab_mode = a.shard == "vocab"
     split_mode = world > 1 and a.shard == "split"
 
     wls = [make_workload(a.config, B=a.batch, seed_offset=i + (0 if (vocab_mode or split_mode) else 17 * rank))
@@ -343,21 +352,36 @@ def main():
     rb = s.record_bytes(B)
     rec = torch.empty(rb, dtype=torch.uint8, device=dev)
     gathered = torch.empty(world * rb, dtype=torch.uint8, device=dev)
+    # vocab sharding: rows not bounded by the candidates need the resolve rounds (NEXT-1)
+    need_resolve = vocab_mode and any(p.temperature >= 1e-5 and not (1 <= p.top_k <= kc) for p in wl.params)
+    if vocab_mode:
+        from paper_2506_22033_b200.distributed import (resolve_buffers, sample_vocab_sharded,
+                                                       sample_vocab_sharded_p2p, setup_peer_exchange)
+        rbufs = resolve_buffers(s, B, world, dev)
+        if a.exchange == "p2p":
+            setup_peer_exchange(s)
+
+    def vocab_step(x, i, sl, append):
+        if a.exchange == "p2p":
+            return sample_vocab_sharded_p2p(s, x, i, slots=sl, append=append, out=out, resolve=need_resolve,
+                                            resolve_bufs=rbufs)
+        return sample_vocab_sharded(s, x, i, slots=sl, append=append, rec=rec, gathered=gathered, out=out,
+                                    resolve=need_resolve, resolve_bufs=rbufs)
 
     def one(i):
         x = xs[i % NBUF]
         sl = slot_sets[i % nset]
         if vocab_mode:
-            s.sample_local(x, rec, slots=sl)
-            dist.all_gather_into_tensor(gathered, rec)
-            s.merge(gathered, world, B, i, slots=sl, append=True, out=out)
+            vocab_step(x, i, sl, True)
         else:
             s.sample(x, i, slots=sl, append=True, out=out)
 
     launches_per_step = None
     one(0)
     torch.cuda.synchronize()
-    launches_per_step = s.last_launch_count() + (1 if vocab_mode else 0)
+    launches_per_step = s.last_launch_count() + (2 if vocab_mode and a.exchange == "nccl" else 0)  # + local pass
+    if need_resolve:  # merge + resolve kernels (fixed round count under graphs)
+        launches_per_step += 1 + s.resolve_max_rounds()
 
     use_graph = not a.no_graph  # (vocab sharding: the NCCL all-gather is captured in the graph too)
     graphs = {}
@@ -445,7 +469,10 @@ def main():
     #      The step with the library's event marks is captured in a CUDA graph and replayed, so
     #      the marks bracket each kernel's device execution (no host launch gap inside them).
     kt = None
-    if not vocab_mode:
+    knames = ["stream_kernel", "select_rows_kernel", "exact_kernel"]
+    if vocab_mode and a.exchange == "p2p" and not need_resolve:  # one library call: all 3 kernels marked
+        knames = ["stream_kernel", "select_rows_kernel", "merge_rows_kernel"]
+    if not vocab_mode or knames[2] == "merge_rows_kernel":
         nk = 40
         s.set_timing(True)
         gt = torch.cuda.CUDAGraph()
@@ -472,9 +499,7 @@ def main():
     for i in range(ne):
         dbuf.copy_(hosts[i % 2], non_blocking=True)
         if vocab_mode:
-            s.sample_local(dbuf, rec)
-            dist.all_gather_into_tensor(gathered, rec)
-            o = s.merge(gathered, world, B, 10**9 + i, out=out)
+            o = vocab_step(dbuf, 10**9 + i, None, False)
         else:
             o = s.sample(dbuf, 10**9 + i, out=out)
         res_h[0].copy_(o["tokens"], non_blocking=True)
@@ -505,7 +530,8 @@ def main():
         "scaling": "strong" if (vocab_mode or split_mode) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": a.config, "B": B, "V": V, "logits_dtype": wl.dtype,
-                   "parallelism": (f"vocab{world}" if vocab_mode else (f"split{world}" if split_mode else
+                   "parallelism": (f"vocab{world}-{a.exchange}" + ("+resolve" if need_resolve else "")
+                                   if vocab_mode else (f"split{world}" if split_mode else
                                    (f"rows{world}" if world > 1 else "1gpu"))),
                    "record_bytes_per_row": rb // B,
                    "l2": f"{NBUF} rotating logits buffers ({NBUF * B * (hi - lo) * esize / 1e6:.0f} MB >= 2x L2 126 MB)",
@@ -515,14 +541,14 @@ def main():
                    "graph": use_graph},
         "gbs": step_gbs,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": load_traffic(a.config, ["stream_kernel", "select_rows_kernel", "exact_kernel"][kdom] if kt
+                     "frac": achieved / peak, "traffic": load_traffic(a.config, knames[kdom] if kt
                                                        else "stream_kernel"),
                      "peak_source": peak_src,
-                     "kernel": ["stream_kernel", "select_rows_kernel", "exact_kernel"][kdom] if kt else "step",
+                     "kernel": knames[kdom] if kt else "step",
                      "algorithmic_bytes_per_launch": algo,
                      "kernel_time_s": kern_s,
                      "kernel_times_us": ({n: kt[i] * 1e3 for i, n in
-                                          enumerate(["stream_kernel", "select_rows_kernel", "exact_kernel"][:len(kt)])}
+                                          enumerate(knames[:len(kt)])}
                                          if kt else None),
                      "step_gbs": step_gbs, "step_frac": step_gbs / peak},
         "clocks": clocks,

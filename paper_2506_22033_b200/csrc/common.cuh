@@ -93,15 +93,19 @@ struct ExchPeers {
   int64_t par_pitch;      // world * rank_pitch
   int64_t flags_off;      // bytes from a base to its flags
   int nslots;             // B_max
-  uint32_t* seq;          // [B_max] local sequence numbers
+  uint32_t* seq;          // [B_max] local sequence numbers of phase 1 (publish)
+  uint32_t* mseq;         // [B_max] local sequence numbers of the merge (the same count)
   uint64_t timeout_ns;
 };
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// flag store / load: system scope across GPUs (NVLink peers), GPU scope when every rank is this GPU
+__device__ __forceinline__ void st_release_flag(uint32_t* p, uint32_t v, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_acquire_flag(const uint32_t* p, bool sys) {
   uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 

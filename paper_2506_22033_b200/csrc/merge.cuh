@@ -588,14 +588,17 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
   const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
   const uint8_t* recs = m.records;
   if (m.xp.world > 0) {  // NEXT-2: wait for every rank's flag of this row, then read the local copies
+    // launched with programmatic dependent launch: no grid wait, the flags order everything this row
+    // reads (the publishing CTA of this rank stored its record, RowInfo and flag last)
     const ExchPeers& x = m.xp;
-    const uint32_t sq = x.seq[r];
+    const uint32_t sq = x.mseq[r] + 1;
     if (threadIdx.x == 0) {
+      x.mseq[r] = sq;
       const uint32_t* fl = reinterpret_cast<const uint32_t*>(x.bases[x.rank] + x.flags_off);
       const uint64_t t0 = gtimer();
       int timed_out = 0;
       for (int q = 0; q < x.world && !timed_out; ++q) {
-        while ((int32_t)(ld_acquire_sys(fl + (int64_t)q * x.nslots + r) - sq) < 0) {
+        while ((int32_t)(ld_acquire_flag(fl + (int64_t)q * x.nslots + r, x.world > 1) - sq) < 0) {
           if (gtimer() - t0 > x.timeout_ns) {
             timed_out = 1;
             break;

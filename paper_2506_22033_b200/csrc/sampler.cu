@@ -42,7 +42,7 @@ struct sampler {
   // NEXT-2 one-shot peer exchange (common.cuh ExchPeers)
   uint8_t* d_xbuf = nullptr;     // this rank's exchange buffer (records x 2 parities + flags)
   uint8_t** d_xbases = nullptr;  // [world] device copy of every rank's mapped base
-  uint32_t* d_xseq = nullptr;    // [max_batch]
+  uint32_t* d_xseq = nullptr;    // [2][max_batch] publish / merge sequence numbers
   std::vector<void*> x_opened;   // IPC mappings to close
   int x_world = 0, x_rank = 0;
   int64_t x_bytes = 0;
@@ -609,8 +609,24 @@ static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_par
 }
 
 static int launch_merge(sampler* h, const MergeArgs& m, int B, cudaStream_t st) {
-  merge_rows_kernel<<<B, kBT, kMergeKernelSmem, st>>>(m);
-  CK(h, cudaGetLastError());
+  if (m.xp.world == 0) {
+    merge_rows_kernel<<<B, kBT, kMergeKernelSmem, st>>>(m);
+    CK(h, cudaGetLastError());
+    return SAMPLER_OK;
+  }
+  // peer exchange: programmatic dependent launch after phase 1 (its CTAs trigger at their start, so
+  // every phase-1 CTA is resident before a merge CTA spins on a flag)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(kBT);
+  cfg.dynamicSmemBytes = kMergeKernelSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(h, cudaLaunchKernelEx(&cfg, merge_rows_kernel, m));
   return SAMPLER_OK;
 }
 
@@ -860,6 +876,7 @@ static ExchPeers exch_peers(const sampler* h) {
   x.flags_off = 2 * x.par_pitch;
   x.nslots = h->cfg.max_batch;
   x.seq = h->d_xseq;
+  x.mseq = h->d_xseq + h->cfg.max_batch;
   x.timeout_ns = h->x_timeout_ns;
   return x;
 }
@@ -874,12 +891,12 @@ int sampler_exchange_init(sampler* h, int32_t world, int32_t rank, uint32_t time
   const int64_t Bm = h->cfg.max_batch;
   const int64_t bytes = 2 * (int64_t)world * Bm * h->rec_stride + (int64_t)world * Bm * 4;
   if (cudaMalloc((void**)&h->d_xbuf, bytes) != cudaSuccess || cudaMalloc((void**)&h->d_xbases, sizeof(void*) * world) != cudaSuccess ||
-      cudaMalloc((void**)&h->d_xseq, sizeof(uint32_t) * Bm) != cudaSuccess) {
+      cudaMalloc((void**)&h->d_xseq, 2 * sizeof(uint32_t) * Bm) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, SAMPLER_ENOMEM, "exchange buffer allocation failed");
   }
   CK(h, cudaMemset(h->d_xbuf, 0, bytes));
-  CK(h, cudaMemset(h->d_xseq, 0, sizeof(uint32_t) * Bm));
+  CK(h, cudaMemset(h->d_xseq, 0, 2 * sizeof(uint32_t) * Bm));
   h->x_world = world;
   h->x_rank = rank;
   h->x_bytes = bytes;

@@ -819,11 +819,11 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       if (tid == 0) *reinterpret_cast<RecHdr*>(out) = h;
     }
     cbar();
-    if (tid == 0) {
-      __threadfence_system();
+    if (tid == 0) {  // release (system scope) after the CTA barrier: orders every thread's record stores
       x.seq[r] = sq;
       for (int p = 0; p < x.world; ++p)
-        st_release_sys(reinterpret_cast<uint32_t*>(x.bases[p] + x.flags_off) + (int64_t)x.rank * x.nslots + r, sq);
+        st_release_flag(reinterpret_cast<uint32_t*>(x.bases[p] + x.flags_off) + (int64_t)x.rank * x.nslots + r, sq,
+                        x.world > 1);
     }
     return;
   }
