@@ -165,6 +165,12 @@ int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_
                         int32_t* prompt_out, int32_t* output_out, int32_t* n_unique,
                         int32_t* uniq_ids, int32_t* uniq_counts, int32_t* uniq_in_prompt);
 
+/* SYNC.  The slot's status bits in *flags: SAMPLER_SLOT_OVERFLOW (bit 0) = an in-kernel append
+ * found the history at L_max and dropped the token (sticky until sampler_set_history).
+ * Errors: EINVAL (NULL), ERANGE (slot out of range). */
+enum { SAMPLER_SLOT_OVERFLOW = 1 };
+int sampler_get_slot_flags(sampler* h, int32_t slot, int32_t* flags);
+
 /* ---- sampling ----------------------------------------------------------------------- */
 
 /* ASYNC.  Sample one token for each of B rows of logits (unsharded handle:
@@ -176,7 +182,7 @@ int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_
  *  step        Philox counter words 0-1 (decode step)
  *  append_to_history  nonzero => append each sampled token to its slot; rows
  *              with a non-OK status append nothing.  Overflowing L_max sets the slot's
- *              overflow bit (visible via sampler_get_history) and appends nothing.
+ *              overflow bit (SAMPLER_SLOT_OVERFLOW, read with sampler_get_slot_flags) and appends nothing.
  *  tokens_dev  dev int32[B] out; logprobs_dev dev float[B] out = log softmax(z'/tau_eff)[tok]
  *              (full vocabulary, before filtering; R12)
  *  filtered_logprobs_dev  dev float[B] out, nullable: log of the token's probability in the

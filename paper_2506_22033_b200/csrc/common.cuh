@@ -179,9 +179,19 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
     __nanosleep(ns);
   }
 }
+#ifndef SMP_L2POL
+#define SMP_L2POL 0
+#endif
+// L2 policy of phase A's logits copies: 0 evict_first (default), 1 evict_normal, 2 evict_last
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
+#if SMP_L2POL == 1
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#elif SMP_L2POL == 2
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 // global -> shared bulk copy without an L2 cache hint

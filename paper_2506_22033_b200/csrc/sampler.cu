@@ -442,8 +442,17 @@ int sampler_get_history(sampler* h, int32_t slot, int32_t* n_prompt, int32_t* n_
     if (uniq_counts) uniq_counts[i] = (int32_t)(u[i].meta >> 1);
     if (uniq_in_prompt) uniq_in_prompt[i] = (int32_t)(u[i].meta & 1u);
   }
-  // overflow flag is reported through the sign of n_output? keep a separate path:
-  if (sm.flags & 1) h->err = "history overflow occurred on this slot";
+  return SAMPLER_OK;
+}
+
+int sampler_get_slot_flags(sampler* h, int32_t slot, int32_t* flags) {
+  if (!h || !flags) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (slot < 0 || slot >= h->cfg.max_batch) return fail(h, SAMPLER_ERANGE, "slot out of range");
+  CK(h, cudaSetDevice(h->cfg.device));
+  CK(h, cudaDeviceSynchronize());
+  SlotMeta sm;
+  CK(h, cudaMemcpy(&sm, h->d_meta + slot, sizeof(sm), cudaMemcpyDeviceToHost));
+  *flags = sm.flags;
   return SAMPLER_OK;
 }
 
@@ -467,13 +476,18 @@ struct LaunchPlan {
 
 // Phase A geometry (stream.cuh): equal contiguous spans of the padded step space, one persistent
 // CTA per SM; a span is >= one tile (16 steps) and covers at most kMaxSeg - 2 whole rows.
+#ifndef SMP_MINSPAN
+#define SMP_MINSPAN kTileSteps
+#endif
 static LaunchPlan plan(const sampler* h, int32_t B) {
   LaunchPlan p;
   p.spr = (int)(h->Vq / kStepVec);
   p.nsteps = (int64_t)B * p.spr;
   const int64_t nctas = (int64_t)h->sm_count * kStreamCtasPerSm;
   int64_t span = (p.nsteps + nctas - 1) / nctas;
-  span = std::max<int64_t>(span, kTileSteps);
+  span = std::max<int64_t>(span, SMP_MINSPAN);
+  // phase B merges at most kBT partial records per row (kCW per CTA touching the row): <= 9 CTAs
+  span = std::max<int64_t>(span, (p.spr + kBT / kCW - 2) / (kBT / kCW - 1));
   span = std::min<int64_t>(span, (int64_t)(kMaxSeg - 2) * p.spr);
   p.span = (int)span;
   p.grid = (int)((p.nsteps + span - 1) / span);

@@ -27,6 +27,7 @@ EXPORTED = [
     "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
     "sampler_resolve_bytes", "sampler_resolve_round", "sampler_resolve_max_rounds",
     "sampler_exchange_init", "sampler_exchange_open", "sampler_exchange_set_peers", "sampler_sample_exchange",
+    "sampler_get_slot_flags",
 ]
 
 
@@ -95,6 +96,7 @@ def _load():
         "sampler_resolve_max_rounds": ([], I32),
         "sampler_exchange_init": ([P, I32, I32, C.c_uint32, P, P], I32),
         "sampler_exchange_open": ([P, P], I32),
+        "sampler_get_slot_flags": ([P, I32, P], I32),
         "sampler_exchange_set_peers": ([P, P], I32),
         "sampler_sample_exchange": ([P, P, I64, I32, P, P, P, U64, I32, P, P, P, P, I32, P], I32),
         "sampler_last_launch_count": ([P], I32),
@@ -205,6 +207,12 @@ class Sampler:
         n, m, k = np_.value, no.value, nu.value
         return dict(prompt=pr[:n].tolist(), output=out[:m].tolist(), uniq_ids=ids[:k].tolist(),
                     uniq_counts=cnt[:k].tolist(), uniq_in_prompt=inp[:k].tolist())
+
+    def slot_flags(self, slot) -> int:
+        """Bit 0 (SLOT_OVERFLOW): an append found the slot's history full and dropped the token."""
+        f = C.c_int32()
+        self._check(_lib.sampler_get_slot_flags(self.h, int(slot), C.byref(f)))
+        return int(f.value)
 
     def last_launch_count(self) -> int:
         return int(_lib.sampler_last_launch_count(self.h))

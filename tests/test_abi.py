@@ -100,3 +100,25 @@ def test_error_paths_before_launch():
         s.append_tokens([1], [7])
     assert e.value.code == SAMPLER_ERANGE
     assert s.get_history(1)["output"] == [6]
+
+
+@pytest.mark.gpu
+def test_in_kernel_append_overflow_sets_slot_flag():
+    """An in-kernel append into a full history drops the token and sets SAMPLER_SLOT_OVERFLOW, readable
+    with sampler_get_slot_flags; set_history clears it."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    s = Sampler(1000, 2, max_history=8, dtype="bf16")
+    s.set_history(0, [1, 2, 3], [4, 5, 6, 7])   # 7 of 8
+    s.set_history(1, [1], [])
+    x = torch.randn((2, 1000), device="cuda").to(torch.bfloat16)
+    o1 = s.sample(x, 0, append=True)
+    torch.cuda.synchronize()
+    assert s.slot_flags(0) == 0 and len(s.get_history(0)["output"]) == 5
+    s.sample(x, 1, append=True)
+    torch.cuda.synchronize()
+    assert s.slot_flags(0) & 1 and len(s.get_history(0)["output"]) == 5   # dropped, flagged
+    assert s.slot_flags(1) == 0 and len(s.get_history(1)["output"]) == 2
+    assert int(o1["tokens"][0].item()) == s.get_history(0)["output"][-1]
+    s.set_history(0, [1], [])
+    assert s.slot_flags(0) == 0
