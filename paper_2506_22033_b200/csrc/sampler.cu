@@ -476,6 +476,9 @@ struct LaunchPlan {
 
 // Phase A geometry (stream.cuh): equal contiguous spans of the padded step space, one persistent
 // CTA per SM; a span is >= one tile (16 steps) and covers at most kMaxSeg - 2 whole rows.
+#ifndef SMP_EXG_MIN
+#define SMP_EXG_MIN 1  // smallest cluster size of the exact kernel
+#endif
 #ifndef SMP_MINSPAN
 #define SMP_MINSPAN kTileSteps
 #endif
@@ -670,7 +673,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     // bf16: one CTA per SM (the value-key histogram), chunks of <= 65535 elements
     const bool bf = h->cfg.logits_dtype == SAMPLER_BF16;
     const int per_sm = bf ? 1 : 2;
-    int G = 1;
+    int G = SMP_EXG_MIN;
     while (G < 8 && (int64_t)B * G * 2 <= (int64_t)per_sm * h->sm_count) G *= 2;
     while (bf && G < 8 && ((int64_t)h->cfg.vocab_local + G - 1) / G > kKhMaxChunk - 127) G *= 2;
     ExactArgs e{};
