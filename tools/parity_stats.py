@@ -52,6 +52,8 @@ def main():
     ap.add_argument("--rows", type=int, default=100000)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "parity_r02.json"))
     ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--sharded", type=int, default=0,
+                    help="G > 0: the vocab-sharded path (G slices in one process: local pass, merge, resolve rounds)")
     a = ap.parse_args()
     import torch
     global _JOB
@@ -59,7 +61,8 @@ def main():
     # rows per config: equal shares; each (workload draw, step) call samples a whole batch
     share = a.rows // len(cfgs) + 1
     cores = len(os.sched_getaffinity(0))
-    summary = {"rows": 0, "flagged": 0, "flagged6": 0, "mismatch": 0, "unflagged_mismatch": 0,
+    summary = {"path": f"vocab-sharded G={a.sharded} (merge + resolve rounds)" if a.sharded else "sampler_sample",
+               "rows": 0, "flagged": 0, "flagged6": 0, "mismatch": 0, "unflagged_mismatch": 0,
                "prob_violations": 0, "status_mismatch": 0, "per_config": {}, "cores": cores,
                "band": {"excuse": FLAG_EPS_GPU, "north_star": FLAG_EPS}, "tolerance": {"rel": REL, "abs": ABS}}
     t0 = time.time()
@@ -70,13 +73,17 @@ def main():
         draw = 0
         while st["rows"] < share:
             wl = make_workload(cfg, seed_offset=100 + draw, run=draw)
-            s = make_sampler(wl)
+            s = make_sampler(wl) if not a.sharded else None
             x = device_logits(wl)
             steps = max(1, min(8, -(-(share - st["rows"]) // wl.B)))
             _JOB = wl
             with ctx.Pool(cores) as pool:
                 for step in range(steps):
-                    out = s.sample(x, step)
+                    if a.sharded:
+                        from tests.test_gpu_resolve import sharded_inprocess
+                        out = sharded_inprocess(wl, x, a.sharded, step)[0][0]
+                    else:
+                        out = s.sample(x, step)
                     torch.cuda.synchronize()
                     tok = out["tokens"].cpu().numpy()
                     lp = out["logprobs"].cpu().numpy().astype(np.float64)

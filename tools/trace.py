@@ -20,7 +20,7 @@ from workloads.synth import make_workload
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
-    wl = make_workload(cfg)
+    wl = make_workload(cfg, B=int(os.environ["TRACE_B"]) if os.environ.get("TRACE_B") else None)
     s = Sampler(wl.V, wl.B, max_history=2048, max_top_k=128, dtype=wl.dtype)
     s.set_params(list(range(wl.B)), wl.params)
     for b in range(wl.B):
