@@ -686,7 +686,8 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
     int n = (int)ex_ld32(ex_map(ctl + 20, 0));
     ex_csync();
   EXPROF(6);
-    if (n > kGat) {  // too large: one more level inside bucket b0
+    int sbl = -1;  // the level-1 sub-bucket (level 1)
+    if (n > kGat && b0 < kNB0 - 1) {  // too large: one more level inside bucket b0 (not the far tail)
       level = 1;
       histogram(ybase, scale, kNB1);
       ex_csync();
@@ -737,6 +738,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
       ex_bar();
       int sb = ctl[0];
       if (sb == 0x7FFFFFFF) sb = kNB1 - 1;
+      sbl = sb;
       ex_bar();
       if (tid == sb / (kNB1 / kExThreads)) {
         double rr = mb;
@@ -761,7 +763,114 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
       ex_csync();
   EXPROF(8);
     }
-    n = min(n, kGat);  // (beyond: a pathological tie mass; the first kGat are kept)
+    if (n > kGat) {
+      // near-ties: more than kGat elements in the level-1 sub-bucket (1/65536 octave of weight) or
+      // in the far-tail bucket.  Radix rounds over the composite (z' desc, id asc) of the set's
+      // elements: per round a 256-bin histogram of the next 8 bits (counts, masses relative to the
+      // set's top weight in 2^-40 fixed point: the level's arithmetic), cluster totals, the bin
+      // reaching the target; until it holds <= kGat elements, gathered and walked exactly below
+      const bool lv1 = level == 1;
+      const double yt = lv1 ? ybase + (double)sbl / scale : (double)b0 / 64.0;  // the set's top
+      const double wtop = ex_exp2(-yt);
+      auto member = [&](double y) -> bool {
+        if (lv1) {
+          const double q = (y - ybase) * scale;
+          return q >= 0.0 && q < (double)kNB1 && (int)q == sbl;
+        }
+        return y * 64.0 >= (double)(kNB0 - 1);  // (level 0: the far-tail bucket b0 = kNB0 - 1)
+      };
+      auto relfix = [&](double y) -> uint64_t {
+        const double rel = lv1 ? exp2_neg_small((y - yt) * kLn2) : ex_exp2(-(y - yt));
+        return (uint64_t)(rel * kFix40 + 0.5);
+      };
+      uint32_t* tc2 = reinterpret_cast<uint32_t*>(gat);            // [256] cluster totals (scratch)
+      uint64_t* tm2 = gat + 128;                                   // [256]
+      if (tid == 0) {
+        cu[4] = 0;          // klo
+        cu[5] = ~0ull;      // khi
+        cu[6] = 0;          // count above khi (in the sub-bucket)
+        cu[7] = 0;          // fixed mass above khi
+        ctl[26] = 56;       // shift
+        ctl[27] = 0;        // done
+      }
+      ex_bar();
+      for (;;) {
+        const uint64_t klo = cu[4], khi = cu[5];
+        const int sh = ctl[26];
+        for (int i = tid; i < 256; i += kExThreads) {
+          hcnt[i] = 0;
+          hmass[i] = 0;
+        }
+        ex_csync();  // (every CTA's histogram is clear before any CTA adds to its own)
+        for_each([&](float z, int l) {
+          const double y = ycoord(z);
+          if (!member(y)) return;
+          const uint64_t c = make_comp(z, a.voff + l);
+          if (c < klo || c > khi) return;
+          const int bin = (int)((khi - c) >> sh);
+          atomicAdd(&hcnt[bin], 1u);
+          smem_add_u64(&hmass[bin], relfix(y));
+        });
+        ex_csync();
+        for (int j = tid; j < 256; j += kExThreads) {
+          uint32_t cj;
+          uint64_t mj;
+          tot_bucket(j, &cj, &mj);
+          tc2[j] = cj;
+          tm2[j] = mj;
+        }
+        ex_csync();  // (every remote histogram has been read)
+        if (tid == 0) {
+          uint64_t cb2 = cu[6], mb2 = cu[7];
+          int js = -1, jl = -1;
+          for (int j = 0; j < 256; ++j) {
+            if (tc2[j] == 0) continue;
+            jl = j;
+            const bool hit = (mode == 0) ? (cb2 + tc2[j] >= need)
+                                         : (before + (double)(mb2 + tm2[j]) * (1.0 / kFix40) * wtop >= target);
+            if (hit) {
+              js = j;
+              break;
+            }
+            cb2 += tc2[j];
+            mb2 += tm2[j];
+          }
+          if (js < 0) {  // (rounding shortfall: the last non-empty bin)
+            js = jl;
+            cb2 -= tc2[jl];
+            mb2 -= tm2[jl];
+          }
+          const uint64_t nhi = khi - ((uint64_t)js << sh);
+          const uint64_t span = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
+          cu[4] = (nhi - klo > span) ? nhi - span : klo;
+          cu[5] = nhi;
+          cu[6] = cb2;
+          cu[7] = mb2;
+          ctl[27] = (tc2[js] <= (uint32_t)kGat || sh == 0) ? 1 : 0;
+          ctl[26] = sh - 8;
+        }
+        ex_bar();
+        if (ctl[27]) break;
+      }
+      // the elements of the final interval into the leader's buffer
+      const uint64_t klo = cu[4], khi = cu[5];
+      if (tid == 0) ctl[20] = 0;
+      ex_csync();
+      const uint32_t cnt_addr = ex_map(ctl + 20, 0);
+      for_each([&](float z, int l) {
+        if (!member(ycoord(z))) return;
+        const uint64_t c = make_comp(z, a.voff + l);
+        if (c < klo || c > khi) return;
+        const uint32_t at = ex_atom_add(cnt_addr, 1u);
+        if (at < (uint32_t)kGat) ex_st64(ex_map(gat + at, 0), c);
+      });
+      ex_csync();
+      n = (int)ex_ld32(ex_map(ctl + 20, 0));
+      if (mode == 0) need -= cu[6];                       // (count from the interval's start)
+      before += (double)cu[7] * (1.0 / kFix40) * wtop;    // (the walk's mass from the interval's start)
+      ex_csync();
+    }
+    n = min(n, kGat);  // (the refinement above leaves at most kGat)
     uint64_t pick = 0;
     double pm = before;
     if (rank == 0) {

@@ -434,3 +434,75 @@ def test_very_long_histories_full_vocab(n_hist):
         ids = sorted(set(wl.prompts[b]) | set(wl.outputs[b]))
         assert h["uniq_ids"] == ids
 
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_temperature_edges_and_subnormal_logits(dtype):
+    """tau at the greedy boundary (binary32 9.99e-6 < 1e-5 <= 1e-5: R5), very small tau (a rebase of the lane
+    reference at almost every group, weights underflowing to 0 past the max), very large tau, and rows of
+    subnormal / signed-zero logits; tokens, logprobs and the whole filtered distribution q vs the oracle."""
+    B, V = 12, 5000
+    rng = np.random.default_rng(99)
+    z = rng.normal(0, 2, size=(B, V)).astype(np.float32)
+    z[6] = (rng.integers(-50, 50, size=V) * np.float32(1e-41)).astype(np.float32)   # subnormals
+    z[7] = np.float32(0.0)
+    z[7, ::2] = np.float32(-0.0)
+    z[7, 17] = np.float32(1e-45)                                                  # smallest subnormal wins
+    z[8] = np.where(rng.random(V) < 0.5, np.float32(-1e-44), np.float32(3e-39))
+    z[9] = np.float32(-np.inf)
+    z[9, 4000:4003] = np.float32([1e-40, -2e-40, 5e-41])
+    if dtype == "bf16":
+        from workloads.synth import f32_to_bf16_bits
+        raw = f32_to_bf16_bits(z)
+    else:
+        raw = z
+    taus = [9.99e-6, 1e-5, 1.0001e-5, 1e-4, 0.01, 100.0, 1.0, 1.0, 0.5, 1.0, 2e-5, 50.0]
+    params = [RowParams(temperature=t, top_p=0.9 if b % 3 == 0 else 1.0, top_k=20 if b % 3 == 1 else 0,
+                        seed=b, request_id=b) for b, t in enumerate(taus)]
+    wl = Workload("tau", B, V, dtype, raw, [[]] * B, [[]] * B, params)
+    orc = oracle_run(wl, step=4, want_q=True)
+    s, out = _run(wl, step=4, q=True)
+    assert_parity(wl, out, orc, q=out["q"])
+    s, out = _run(wl, step=4)
+    assert_parity(wl, out, oracle_run(wl, 4))
+
+
+def test_q_full_vocab_for_exact_kernel_rows():
+    """The whole filtered distribution q at BASELINE's full vocabulary for top-p-only rows (the exact
+    cluster kernel: float64 bucket masses, boundary walk) and a min-p-only row, vs the oracle's q."""
+    wl = make_workload("c2", B=3)
+    wl.params[2] = RowParams(temperature=0.8, min_p=0.01, seed=5, request_id=5)
+    orc = oracle_run(wl, step=3, want_q=True)
+    s, out = _run(wl, step=3, q=True)
+    assert_parity(wl, out, orc, q=out["q"])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_exact_kernel_near_tie_floods(dtype):
+    """Rows whose boundary (sub-)bucket holds far more than the exact kernel's 4096-entry gather buffer:
+    all-equal rows (top-p-only, top-k 3000 > K_cand, min-p), a two-valued row and a ramp of values
+    closer than 1/65536 octave of weight — resolved by the composite radix rounds, vs the oracle's q."""
+    B, V = 7, 60000
+    z = np.full((B, V), 0.75, dtype=np.float32)
+    z[6] = -np.arange(V, dtype=np.float32) * np.float32(0.02)   # top_k's cutoff deep in the far-tail bucket
+    z[3, ::2] = np.float32(0.5)
+    z[4] = (np.float32(1.0) + np.arange(V, dtype=np.float32) * np.float32(2 ** -23)).astype(np.float32)
+    z[5, 1000:] = np.float32(-np.inf)
+    if dtype == "bf16":
+        from workloads.synth import f32_to_bf16_bits
+        raw = f32_to_bf16_bits(z)
+    else:
+        raw = z
+    params = [RowParams(temperature=1.0, top_p=0.5, seed=1, request_id=1),
+              RowParams(temperature=0.7, top_k=3000, seed=2, request_id=2),
+              RowParams(temperature=1.0, top_k=5000, top_p=0.3, seed=3, request_id=3),
+              RowParams(temperature=1.0, top_p=0.9, seed=4, request_id=4),
+              RowParams(temperature=1.0, top_p=0.77, seed=5, request_id=5),
+              RowParams(temperature=1.0, top_p=0.6, seed=6, request_id=6),
+              RowParams(temperature=1.0, top_k=5000, seed=7, request_id=7)]
+    wl = Workload("ties", B, V, dtype, raw, [[]] * B, [[]] * B, params)
+    orc = oracle_run(wl, step=1, want_q=True)
+    s, out = _run(wl, step=1, q=True)
+    assert_parity(wl, out, orc, q=out["q"])
+    s, out = _run(wl, step=1)
+    assert_parity(wl, out, oracle_run(wl, 1))
