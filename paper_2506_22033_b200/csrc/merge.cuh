@@ -466,8 +466,10 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
     const bool has = lane < nrec;
     const RecHdr hd = has ? ms.hdr[lane] : RecHdr{};
     const float M = warp_max(has ? hd.m : -INFINITY);
-    const double RM = (double)M * rc.c_d;
-    const double term = (has && hd.s != 0.0) ? hd.s * exp2(hd.R - RM) : 0.0;
+    // R - RM with RM rounded first (no FMA contraction): contracted, the difference of two equal
+    // products would be the product's rounding residual — ~1e22 for |M| ~ 1e38 — and S overflow
+    const double RM = __dmul_rn((double)M, rc.c_d);
+    const double term = (has && hd.s != 0.0) ? hd.s * exp2(__dsub_rn(hd.R, RM)) : 0.0;
     const double S = warp_sum_d(term);
     const uint64_t F = warp_max_u64(has ? hd.frontier : 0ull);
     const unsigned fl = __reduce_or_sync(kFull, has ? hd.flags : 0u);

@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     h.m = M;
     h.flags = bad ? kRecBad : 0u;
     h.s = S;
-    h.R = (double)M * rc.c_d;
+    h.R = __dmul_rn((double)M, rc.c_d);  // (rounded product: the merge subtracts the same rounded product)
     h.n = (uint32_t)n;
     h.rsv = 0;
     h.frontier = F;

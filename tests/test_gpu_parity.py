@@ -506,3 +506,41 @@ def test_exact_kernel_near_tie_floods(dtype):
     assert_parity(wl, out, orc, q=out["q"])
     s, out = _run(wl, step=1)
     assert_parity(wl, out, oracle_run(wl, 1))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_extreme_magnitudes_and_param_edges(dtype):
+    """Logits near the binary32 / bf16 range limits (differences overflow to inf in binary32, weights
+    underflow to 0 in float64), huge temperatures, min_p = 1, top_p at the smallest float, top_k = V - 1."""
+    B, V = 10, 7000
+    rng = np.random.default_rng(5)
+    z = rng.normal(0, 3, size=(B, V)).astype(np.float32)
+    z[0, 10] = np.float32(3e38)
+    z[0, 20] = np.float32(-3e38)
+    z[1] = (rng.normal(0, 1, size=V) * 1e30).astype(np.float32)
+    z[2, ::3] = np.float32(-3e38)
+    z[3] = np.float32(1e20)
+    z[3, 5::7] = np.float32(1e20 * (1 + 2 ** -6))
+    z[4, :] = np.float32(-1e35)
+    z[4, 6999] = np.float32(-9e34)
+    if dtype == "bf16":
+        from workloads.synth import f32_to_bf16_bits
+        raw = f32_to_bf16_bits(z)
+    else:
+        raw = z
+    params = [RowParams(temperature=1.0, top_p=0.9, seed=0, request_id=0),
+              RowParams(temperature=1e30, top_k=300, seed=1, request_id=1),
+              RowParams(temperature=2.0, min_p=0.5, seed=2, request_id=2),
+              RowParams(temperature=1e19, top_p=0.5, seed=3, request_id=3),
+              RowParams(temperature=1e33, seed=4, request_id=4),
+              RowParams(temperature=0.9, min_p=1.0, seed=5, request_id=5),
+              RowParams(temperature=1.0, top_p=float(np.float32(1e-38)), seed=6, request_id=6),
+              RowParams(temperature=0.6, top_k=V - 1, seed=7, request_id=7),
+              RowParams(temperature=3e38, top_k=V - 1, top_p=0.999, seed=8, request_id=8),
+              RowParams(temperature=1.0, top_k=1, min_p=0.9, seed=9, request_id=9)]
+    wl = Workload("extreme", B, V, dtype, raw, [[]] * B, [[]] * B, params)
+    orc = oracle_run(wl, step=6, want_q=True)
+    s, out = _run(wl, step=6, q=True)
+    assert_parity(wl, out, orc, q=out["q"])
+    s, out = _run(wl, step=6)
+    assert_parity(wl, out, oracle_run(wl, 6))

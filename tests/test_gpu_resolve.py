@@ -218,3 +218,38 @@ def test_peer_exchange_timeout_reports_rows():
     o = shards[0].sample_exchange(x[:, bounds[0][0]:bounds[0][1]], 0, phases=2)
     torch.cuda.synchronize()
     assert (o["status"] == ROW_EXCHANGE_TIMEOUT).all() and (o["tokens"] == -1).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_sharded_edge_rows(dtype):
+    """The vocab-sharded path (merge + resolve rounds) on the edge rows of the unsharded suite: subnormal /
+    signed-zero logits, values near the binary32 limit, huge temperatures, all-equal rows, min_p = 1."""
+    B, V = 8, 9000
+    rng = np.random.default_rng(17)
+    z = rng.normal(0, 2, size=(B, V)).astype(np.float32)
+    z[0] = (rng.integers(-50, 50, size=V) * np.float32(1e-41)).astype(np.float32)
+    z[1] = np.float32(0.0)
+    z[1, ::2] = np.float32(-0.0)
+    z[2, 10] = np.float32(3e38)
+    z[3] = (rng.normal(0, 1, size=V) * 1e30).astype(np.float32)
+    z[4] = np.float32(0.75)
+    z[5, ::2] = np.float32(0.5)
+    if dtype == "bf16":
+        from workloads.synth import f32_to_bf16_bits
+        raw = f32_to_bf16_bits(z)
+    else:
+        raw = z
+    params = [RowParams(temperature=1.0, top_p=0.9, seed=0, request_id=0),
+              RowParams(temperature=1.0, top_p=0.3, seed=1, request_id=1),
+              RowParams(temperature=1.0, top_p=0.9, seed=2, request_id=2),
+              RowParams(temperature=1e30, top_k=300, seed=3, request_id=3),
+              RowParams(temperature=1.0, top_k=2000, top_p=0.4, seed=4, request_id=4),
+              RowParams(temperature=0.9, min_p=1.0, seed=5, request_id=5),
+              RowParams(temperature=1e33, seed=6, request_id=6),
+              RowParams(temperature=0.5, top_k=V - 1, min_p=0.2, seed=7, request_id=7)]
+    wl = Workload("edge", B, V, dtype, raw, [[]] * B, [[]] * B, params)
+    x = device_logits(wl)
+    for G in (2, 3):
+        outs, n, _ = sharded_inprocess(wl, x, G, step=3)
+        assert (outs[0]["status"] == 0).all(), outs[0]["status"]
+        _check_all_ranks(wl, outs, oracle_run(wl, 3))
