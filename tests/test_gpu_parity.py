@@ -544,3 +544,37 @@ def test_extreme_magnitudes_and_param_edges(dtype):
     assert_parity(wl, out, orc, q=out["q"])
     s, out = _run(wl, step=6)
     assert_parity(wl, out, oracle_run(wl, 6))
+
+
+@pytest.mark.parametrize("cfg,dtype,V", [("c2", "f32", None), ("c4", "f32", None), ("c3", "f32", None),
+                                         ("c2", "bf16", 262144), ("c4", "bf16", 256000)])
+def test_dtype_and_vocabulary_variants(cfg, dtype, V):
+    """Binary32 logits at the configs' full vocabularies (the exact kernel's per-element path for the
+    unbounded rows) and 256K-class vocabularies in bf16 (more CTAs per row in the exact kernel)."""
+    wl = make_workload(cfg, B=8, V=V, dtype=dtype)
+    s, out = _run(wl, step=2)
+    assert_parity(wl, out, oracle_run(wl, 2))
+
+
+def test_history_append_through_exact_kernel_rows():
+    """Decode steps of top-p-only rows (appended by the exact cluster kernel) and mixed c4 rows, against
+    the oracle replaying the grown histories; the incremental tables equal a recount."""
+    import torch
+    for cfg, B in (("c2", 6), ("c4", 9)):
+        wl = make_workload(cfg, B=B)
+        s = make_sampler(wl, max_history=2400)
+        x = device_logits(wl)
+        outputs = [list(o) for o in wl.outputs]
+        for step in range(4):
+            out = s.sample(x, step, append=True)
+            torch.cuda.synchronize()
+            cur = Workload(wl.name, wl.B, wl.V, wl.dtype, wl.raw, wl.prompts, [list(o) for o in outputs], wl.params)
+            assert_parity(cur, out, oracle_run(cur, step))
+            for b, t in enumerate(out["tokens"].cpu().tolist()):
+                outputs[b].append(int(t))
+        for b in range(wl.B):
+            h = s.get_history(b)
+            assert h["output"] == outputs[b]
+            ids = sorted(set(wl.prompts[b]) | set(outputs[b]))
+            assert h["uniq_ids"] == ids
+            assert h["uniq_counts"] == [outputs[b].count(i) for i in ids]
