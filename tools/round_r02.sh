@@ -16,6 +16,14 @@ done
 for b in 1 2 4 8 16 32; do
   timeout 300 python bench.py --config c5 --batch $b --steps 500 --warmup 20 --no-cpu-baseline --e2e-steps 5 > $O/bench_c5_b$b.json 2> $O/bench_c5_b$b.err
 done
+# vocab-sharded step at world 1 (one-shot peer exchange vs NCCL all-gather; c2 with the resolve rounds)
+for ex in p2p nccl; do
+  timeout 300 python bench.py --shard vocab --exchange $ex --steps 400 --warmup 10 --no-cpu-baseline --e2e-steps 5 > $O/bench_c3_vocab1_$ex.json 2> $O/bench_c3_vocab1_$ex.err
+done
+timeout 300 python bench.py --shard vocab --config c2 --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 3 > $O/bench_c2_vocab1_p2p.json 2> $O/bench_c2_vocab1_p2p.err
+# parity statistics (unsharded >= 1e5 rows; vocab-sharded G = 4)
+[ -n "$PARITY" ] && timeout 1500 python tools/parity_stats.py --rows 100000 --out $O/parity.json > $O/parity.log 2>&1
+[ -n "$PARITY" ] && timeout 900 python tools/parity_stats.py --rows 40000 --sharded 4 --out $O/parity_sharded4.json > $O/parity_sharded4.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches_c3.csv \
   python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-graph --e2e-steps 0 > $O/ncu_c3.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches_c2.csv \

@@ -29,7 +29,8 @@ def last_json(path):
 
 
 lines = [f"# round {rnd} ({src}, one B200 box, graph-replayed bench.py lines; rotation >= 2x L2 for every config)"]
-order = ["c3", "c1", "c2", "c4"] + [f"c5_b{b}" for b in (1, 2, 4, 8, 16, 32)]
+order = ["c3", "c1", "c2", "c4"] + [f"c5_b{b}" for b in (1, 2, 4, 8, 16, 32)] + \
+    ["c3_vocab1_p2p", "c3_vocab1_nccl", "c2_vocab1_p2p"]
 for name in order:
     f = os.path.join(src, f"bench_{name}.json")
     if not os.path.exists(f):
@@ -37,15 +38,16 @@ for name in order:
     d = last_json(f)
     open(os.path.join(P, f"bench_{rnd}_{name}.json"), "w").write(json.dumps(d) + "\n")
     ro = d["roofline"]
-    kt = {k: round(v, 1) for k, v in ro["kernel_times_us"].items()}
-    lines.append(f"{d['config']['workload']:4s} B={d['config']['B']:<5d} step_us={d['ms_per_step'] * 1e3:8.2f} "
+    kt = {k: round(v, 1) for k, v in (ro.get("kernel_times_us") or {}).items()}
+    lines.append(f"{d['config']['workload']:4s} {d['config']['parallelism']:22s} B={d['config']['B']:<5d} step_us={d['ms_per_step'] * 1e3:8.2f} "
                  f"raw_launch_us={d.get('ms_per_step_raw_launch', float('nan')) * 1e3:8.2f} rows/s={d['value']:.3g} "
                  f"dominant={ro['kernel']} frac={ro['frac']:.3f} kernels_us={kt} e2e_rows/s={d['e2e']['value']:.3g} "
                  f"sm_mhz={d['clocks']['sm_mhz']} reasons={d['clocks']['reasons']}")
 open(os.path.join(P, f"configs_{rnd}.txt"), "w").write("\n".join(lines) + "\n")
 if os.path.exists(os.path.join(src, "bench_ref.json")):
     open(os.path.join(P, f"bench_ref_{rnd}_c3.json"), "w").write(json.dumps(last_json(os.path.join(src, "bench_ref.json"))) + "\n")
-for f, dst in (("smi.txt", f"box_{rnd}.txt"), ("clocks.csv", f"clocks_{rnd}.csv")):
+for f, dst in (("smi.txt", f"box_{rnd}.txt"), ("clocks.csv", f"clocks_{rnd}.csv"), ("parity.json", f"parity_{rnd}.json"),
+               ("parity_sharded4.json", f"parity_{rnd}_sharded4.json")):
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(P, dst))
 for cfg in ("c3", "c2"):
