@@ -149,6 +149,36 @@ __device__ __forceinline__ float res_zp(const ResRow& r, const HistState& hs, in
 }
 __device__ __forceinline__ double res_w(float z, const ResRow& r) { return exp(((double)z - r.M) / r.tau); }
 
+// z' of the elements of local vector v (16 bytes: 8 bf16 / 4 f32), in id order: fn(z', local id);
+// penalised ids through the vector's bits of the slot's presence bitmap, then the sorted table
+template <typename T, typename Fn>
+__device__ __forceinline__ void res_vec(const ResRow& r, const HistState& hs, int v, int vloc, int pen_mode, Fn&& fn) {
+  constexpr int VEC = Dec<T>::N;
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(r.rowp) + v);
+  uint32_t pb = 0;
+  if (r.nu) {
+    const int k = v / 128, d = v % 128;
+    pb = (__ldg(r.pm + k * 32 + (d & 31)) >> ((d >> 5) * VEC)) & ((1u << VEC) - 1u);
+  }
+#pragma unroll
+  for (int t = 0; t < VEC; ++t) {
+    const int le = v * VEC + t;
+    if (le >= vloc) break;
+    float z = Dec<T>::elem(u, t);
+    if ((pb >> t) & 1u) {
+      const int32_t id = hs.voff + le;
+      int lo = 0, hi = r.nu;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (r.uniq[mid].id < id) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < r.nu && r.uniq[lo].id == id) z = apply_penalty(z, r.uniq[lo].meta, r.prm, pen_mode);
+    }
+    fn(z, le);
+  }
+}
+
 struct ResSmem {
   ResState st;
   ResRow row;
@@ -234,6 +264,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
   }
   const ResRow& R = sm.row;
   const int vloc = a.hs.vloc;
+  const int nvec = (vloc + Dec<T>::N - 1) / Dec<T>::N;  // 16-byte vectors of the slice (ld * esize % 16 == 0)
 
   // ================================================================ ingest the last exchange
   if (a.round > 0) {
@@ -408,16 +439,16 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     __syncthreads();
     const uint64_t klo = st.klo, khi = st.khi;
     const int sh = st.shift;
-    for (int le = tid; le < vloc; le += kResThreads) {
-      const float z = res_zp<T>(R, a.hs, le, a.pen_mode);
-      const uint64_t c = make_comp(z, a.hs.voff + le);
-      if (c < klo || c > khi) continue;
-      const double w = res_w(z, R);
-      if (!(w > 0.0)) continue;
-      const int j = (int)((khi - c) >> sh);
-      atomicAdd(&sm.cnt[j], 1ull);
-      atom_add128(&sm.mlo[j], &sm.mhi[j], wfix(w));
-    }
+    for (int v = tid; v < nvec; v += kResThreads)
+      res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
+        const uint64_t c = make_comp(z, a.hs.voff + le);
+        if (c < klo || c > khi) return;
+        const double w = res_w(z, R);
+        if (!(w > 0.0)) return;
+        const int j = (int)((khi - c) >> sh);
+        atomicAdd(&sm.cnt[j], 1ull);
+        atom_add128(&sm.mlo[j], &sm.mhi[j], wfix(w));
+      });
     __syncthreads();
     for (int j = tid; j < kResBins; j += kResThreads) {
       reinterpret_cast<uint32_t*>(ob)[j] = (uint32_t)sm.cnt[j];
@@ -432,14 +463,14 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     if (tid == 0) sm.nent = 0;
     __syncthreads();
     const uint64_t klo = st.klo, khi = st.khi;
-    for (int le = tid; le < vloc; le += kResThreads) {
-      const float z = res_zp<T>(R, a.hs, le, a.pen_mode);
-      const uint64_t c = make_comp(z, a.hs.voff + le);
-      if (c < klo || c > khi) continue;
-      if (!(res_w(z, R) > 0.0)) continue;
-      const int i = atomicAdd(&sm.nent, 1);
-      if (i < kResCap) ob[i] = c;
-    }
+    for (int v = tid; v < nvec; v += kResThreads)
+      res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
+        const uint64_t c = make_comp(z, a.hs.voff + le);
+        if (c < klo || c > khi) return;
+        if (!(res_w(z, R) > 0.0)) return;
+        const int i = atomicAdd(&sm.nent, 1);
+        if (i < kResCap) ob[i] = c;
+      });
     __syncthreads();
     if (tid == 0) {
       oh->kind = RK_GATHER;
@@ -449,14 +480,14 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     u128 acc = 0;
     unsigned long long kc = 0;
     const uint64_t cut = st.cut;
-    for (int le = tid; le < vloc; le += kResThreads) {
-      const float z = res_zp<T>(R, a.hs, le, a.pen_mode);
-      if (make_comp(z, a.hs.voff + le) < cut) continue;
-      const double w = res_w(z, R);
-      if (!(w > 0.0) || w < R.minp) continue;
-      acc += wfix(w);
-      kc += 1;
-    }
+    for (int v = tid; v < nvec; v += kResThreads)
+      res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
+        if (make_comp(z, a.hs.voff + le) < cut) return;
+        const double w = res_w(z, R);
+        if (!(w > 0.0) || w < R.minp) return;
+        acc += wfix(w);
+        kc += 1;
+      });
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       acc += shfl_down128(acc, o);
@@ -486,21 +517,21 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
       if (tid == 0) oh->kind = RK_NONE;
     } else {
       // the owner: kept mass per contiguous chunk (ascending id), chunk prefix, one thread re-walks
-      const int ch = (vloc + kResThreads - 1) / kResThreads;
-      const int b0 = tid * ch, b1 = min(vloc, b0 + ch);
+      const int ch = (nvec + kResThreads - 1) / kResThreads;  // vectors per thread, id order
+      const int b0 = tid * ch, b1 = min(nvec, b0 + ch);
       const uint64_t cut = st.cut;
       u128 acc = 0;
       uint32_t kc = 0;
       int lastle = -1;
-      for (int le = b0; le < b1; ++le) {
-        const float z = res_zp<T>(R, a.hs, le, a.pen_mode);
-        if (make_comp(z, a.hs.voff + le) < cut) continue;
-        const double w = res_w(z, R);
-        if (!(w > 0.0) || w < R.minp) continue;
-        acc += wfix(w);
-        kc += 1;
-        lastle = le;
-      }
+      for (int v = b0; v < b1; ++v)
+        res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
+          if (make_comp(z, a.hs.voff + le) < cut) return;
+          const double w = res_w(z, R);
+          if (!(w > 0.0) || w < R.minp) return;
+          acc += wfix(w);
+          kc += 1;
+          lastle = le;
+        });
       sm.tlo[tid] = (uint64_t)acc;
       sm.thi[tid] = (uint64_t)(acc >> 64);
       sm.tcnt[tid] = kc;
@@ -524,17 +555,16 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
         const u128 p0 = mk128(sm.tlo[tid], sm.thi[tid]);
         if (to_d(p0) <= st.target && to_d(p0 + acc) > st.target) {
           u128 cum = p0;
-          for (int le = b0; le < b1; ++le) {
-            const float z = res_zp<T>(R, a.hs, le, a.pen_mode);
-            if (make_comp(z, a.hs.voff + le) < cut) continue;
-            const double w = res_w(z, R);
-            if (!(w > 0.0) || w < R.minp) continue;
-            cum += wfix(w);
-            if (to_d(cum) > st.target) {
-              sm.pick_le = le;
-              break;
-            }
-          }
+          int pick = -1;
+          for (int v = b0; v < b1 && pick < 0; ++v)
+            res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
+              if (pick >= 0 || make_comp(z, a.hs.voff + le) < cut) return;
+              const double w = res_w(z, R);
+              if (!(w > 0.0) || w < R.minp) return;
+              cum += wfix(w);
+              if (to_d(cum) > st.target) pick = le;
+            });
+          sm.pick_le = pick;
         }
       }
       __syncthreads();

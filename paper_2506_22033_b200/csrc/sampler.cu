@@ -498,6 +498,15 @@ static LaunchPlan plan(const sampler* h, int32_t B) {
   return p;
 }
 
+// small batches: phase A's grid leaves at least B SMs free, so phase B's CTAs are resident while it
+// streams and build the penalty hand-off in their prologue (off phase A's critical path)
+#ifndef SMP_PEN_IN_B_MAXB
+#define SMP_PEN_IN_B_MAXB 32
+#endif
+static int pen_in_b(const sampler* h, int32_t B, const LaunchPlan& lp) {
+  return (B <= SMP_PEN_IN_B_MAXB && lp.grid + B <= h->sm_count) ? 1 : 0;
+}
+
 static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_t B, const int32_t* slots,
                               const sampling_params* params_dev, const LaunchPlan& lp) {
   StreamArgs a{};
@@ -522,6 +531,7 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.pent = h->d_pent;
   a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
+  a.pen_in_b = pen_in_b(h, B, lp);
   return a;
 }
 
@@ -571,6 +581,7 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.mode = 0;
   s.append = append;
   s.pending_ok = 1;
+  s.pen_in_b = pen_in_b(h, B, lp);
   s.hs = hist_state(h);
   s.parts = h->d_parts;
   s.hand = h->d_hand;

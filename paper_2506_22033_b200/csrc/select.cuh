@@ -55,6 +55,7 @@ struct SelectArgs {
   uint8_t* out_records;  // mode 1: one candidate record per row
   int64_t out_stride;
   ExchPeers xp;          // mode 1 with xp.world > 0: records stored into every peer (NEXT-2)
+  int pen_in_b;          // small batches: the row's hand-off is built here, before the grid wait
   uint64_t* trace;       // debug: per-row phase timestamps (32 per row), nullable
 };
 
@@ -404,6 +405,56 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
     ctl[1] = 0;
     ctl[2] = 0;
     ctl[5] = 0;
+  }
+  if (a.pen_in_b) {
+    // small batches (phase A leaves SMs free, so this prologue overlaps it): the row's hand-off —
+    // slot, meta, params and every history entry's exact penalised logit — from the
+    // inputs alone (the last step's appends completed before phase A started)
+    bool slot_ok;
+    const int slot = row_slot(a.slots, r, a.hs.nslots, &slot_ok);
+    const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
+    const SlotMeta sm0 = a.hs.meta[slot];
+    if (tid == 0) {
+      RowHand h;
+      h.slot = slot;
+      h.pad[0] = slot_ok ? 0 : 1;
+      h.pad[1] = h.pad[2] = 0;
+      h.meta = sm0;
+      h.prm = prm;
+      const_cast<RowHand*>(a.hand)[r] = h;
+    }
+    const UniqEntry* ut = a.hs.uniq + (int64_t)slot * a.hs.L;
+    const uint8_t* rp = reinterpret_cast<const uint8_t*>(a.logits) + (int64_t)r * a.ld * ESZ;
+    PenEnt* pe = const_cast<PenEnt*>(a.pent) + (int64_t)r * a.hs.L;
+#pragma unroll 1
+    for (int e0 = 0; e0 < sm0.n_uniq; e0 += 4 * kBT) {
+      UniqEntry ue[4];
+      float raw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * kBT + tid;
+        if (e < sm0.n_uniq) ue[q] = ut[e];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * kBT + tid;
+        const int le = e < sm0.n_uniq ? ue[q].id - a.voff : -1;
+        raw[q] = (le >= 0 && le < a.vloc) ? Dec<T>::load1(rp, le) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * kBT + tid;
+        if (e >= sm0.n_uniq) continue;
+        const int le = ue[q].id - a.voff;
+        PenEnt x;
+        x.id = ue[q].id;
+        x.meta = ue[q].meta;
+        x.zp = (le >= 0 && le < a.vloc) ? apply_penalty(raw[q], ue[q].meta, prm, a.pen_mode) : 0.f;
+        x.pad = 0;
+        pe[e] = x;
+      }
+    }
+    cbar();
   }
   griddep_wait();  // phase A's hand-off, partial records and keys are visible from here on
   griddep_launch();  // the next step's phase A may be scheduled as these CTAs retire (it waits)

@@ -96,6 +96,7 @@ struct StreamArgs {
   PenEnt* pent;        // [B][L]
   uint16_t* gkeys;     // [B][gk_stride(Vq)]: group keys | step keys
   uint64_t* trace;     // debug: per-CTA start / end timestamps (globaltimer ns, 64 per CTA), nullable
+  int pen_in_b;        // small batches: phase B builds the hand-off in its prologue (this pass skips it)
 };
 
 // ---- packed binary32 pairs (sm_100a FADD2 / FMUL2) ----------------------------------
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
     UniqEntry* pbuf = reinterpret_cast<UniqEntry*>(smem + kSOffPen);
     uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + kSOffPenBar);
     uint32_t pphase[2] = {0u, 0u};
-    for (int64_t r = rfirst; r * a.spr < s0 + nspan; ++r) {
+    for (int64_t r = rfirst; !a.pen_in_b && r * a.spr < s0 + nspan; ++r) {
       bool slot_ok;
       const int slot = row_slot(a.slots, (int)r, a.hs.nslots, &slot_ok);
       const sampling_params prm = a.params_dev ? a.params_dev[r] : a.params_tab[slot];
