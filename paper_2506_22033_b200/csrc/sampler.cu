@@ -476,6 +476,12 @@ struct LaunchPlan {
 
 // Phase A geometry (stream.cuh): equal contiguous spans of the padded step space, one persistent
 // CTA per SM; a span is >= one tile (16 steps) and covers at most kMaxSeg - 2 whole rows.
+#ifndef SMP_PEN_IN_B_MAXB
+#define SMP_PEN_IN_B_MAXB 32
+#endif
+#ifndef SMP_PEN_IN_B_RESERVE
+#define SMP_PEN_IN_B_RESERVE 1
+#endif
 #ifndef SMP_EXG_MIN
 #define SMP_EXG_MIN 1  // smallest cluster size of the exact kernel
 #endif
@@ -486,7 +492,11 @@ static LaunchPlan plan(const sampler* h, int32_t B) {
   LaunchPlan p;
   p.spr = (int)(h->Vq / kStepVec);
   p.nsteps = (int64_t)B * p.spr;
-  const int64_t nctas = (int64_t)h->sm_count * kStreamCtasPerSm;
+  int64_t nctas = (int64_t)h->sm_count * kStreamCtasPerSm;
+#if SMP_PEN_IN_B_RESERVE
+  // small batches: leave B SMs to phase B (its prologue then overlaps this pass; see pen_in_b)
+  if (B <= SMP_PEN_IN_B_MAXB && (int64_t)B * 4 <= nctas) nctas -= B;
+#endif
   int64_t span = (p.nsteps + nctas - 1) / nctas;
   span = std::max<int64_t>(span, SMP_MINSPAN);
   // phase B merges at most kBT partial records per row (kCW per CTA touching the row): <= 9 CTAs
@@ -500,9 +510,7 @@ static LaunchPlan plan(const sampler* h, int32_t B) {
 
 // small batches: phase A's grid leaves at least B SMs free, so phase B's CTAs are resident while it
 // streams and build the penalty hand-off in their prologue (off phase A's critical path)
-#ifndef SMP_PEN_IN_B_MAXB
-#define SMP_PEN_IN_B_MAXB 32
-#endif
+
 static int pen_in_b(const sampler* h, int32_t B, const LaunchPlan& lp) {
   return (B <= SMP_PEN_IN_B_MAXB && lp.grid + B <= h->sm_count) ? 1 : 0;
 }
