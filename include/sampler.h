@@ -315,6 +315,16 @@ int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, in
                             int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
                             int32_t* row_status_dev, int32_t phases, void* cuda_stream);
 
+/* ---- per-step parameters on the device (CUDA-graph replays of a decode loop) ----------------
+ * The TSEM idea of versioned per-step inputs (§5.2): with step_dev != NULL (device
+ * uint64, 8-byte aligned, owned by the caller and alive while calls use it), every later sample /
+ * merge / sample_exchange / resolve_round call reads the Philox step (R11) from *step_dev
+ * when its kernels run and ignores its host `step` argument.  A decode step captured once in a CUDA
+ * graph then samples a new step per replay when the caller advances *step_dev (for instance with an
+ * increment captured in the same graph).  NULL restores the host argument.  No synchronisation.
+ * Errors: EINVAL (NULL handle, misaligned pointer). */
+int sampler_set_step_source(sampler* h, const uint64_t* step_dev);
+
 /* ---- introspection ------------------------------------------------------------------ */
 
 /* Number of kernel launches the last sample / sample_local / merge / debug call enqueued. */

@@ -48,6 +48,7 @@ struct ExactArgs {
   const sampling_params* params_tab;
   const uint64_t* seeds;
   uint64_t step;
+  const uint64_t* step_dev;  // nullable: the decode step read on the device (sampler_set_step_source)
   int append;
   int pen_mode;
   HistState hs;
@@ -1168,7 +1169,7 @@ __global__ void __launch_bounds__(kExThreads, 1) exact_kernel(const __grid_const
   EXPROF(13);
   EXSTOP(13);
   const uint64_t seed = a.seeds ? a.seeds[r] : prm.seed;
-  const double u = philox_uniform(seed, prm.request_id, a.step);
+  const double u = philox_uniform(seed, prm.request_id, a.step_dev ? *a.step_dev : a.step);
   if (rank == 0 && tid == 0) {
     double W = 0.0;
     for (int g = 0; g < a.G; ++g) W += tots[g];

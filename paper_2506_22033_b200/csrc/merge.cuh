@@ -557,6 +557,7 @@ struct MergeArgs {
   const sampling_params* params_tab;
   const uint64_t* seeds;
   uint64_t step;
+  const uint64_t* step_dev;  // nullable: the decode step read on the device
   int append;
   HistState hs;
   RowOut ro;
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
     }
     recs = x.bases[x.rank] + (int64_t)(sq & 1) * x.par_pitch;
   }
-  block_merge_row(recs + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step, m.V,
+  block_merge_row(recs + (int64_t)r * m.rec_stride, m.rank_pitch, m.world, r, slot, prm, seed, m.step_dev ? *m.step_dev : m.step, m.V,
                   m.kcand, 0, nullptr, m.ro, m.append, m.hs, false, !slot_ok || !params_ok(prm, m.pen_mode), ms, tr);
 }
 

@@ -82,6 +82,7 @@ struct ResolveArgs {
   const sampling_params* params_tab;
   const uint64_t* seeds;
   uint64_t step;
+  const uint64_t* step_dev;  // nullable: the decode step read on the device
   int append;
   HistState hs;
   RowOut ro;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
         }
         st.W = to_d(tot);
         const uint64_t seed = a.seeds ? a.seeds[row] : prm.seed;
-        st.target = philox_uniform(seed, prm.request_id, a.step) * st.W;
+        st.target = philox_uniform(seed, prm.request_id, a.step_dev ? *a.step_dev : a.step) * st.W;
         u128 pre = 0;
         int owner = -1, lastr = 0;
         for (int r = 0; r < a.world; ++r) {

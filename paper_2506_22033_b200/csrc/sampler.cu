@@ -39,6 +39,7 @@ struct sampler {
   int32_t* d_hist = nullptr;
   RowInfo* d_info = nullptr;
   ResState* d_rs = nullptr;     // [max_batch] NEXT-1 resolve rounds (resolve.cuh)
+  const uint64_t* d_step_src = nullptr;  // sampler_set_step_source: the decode step read on the device
   // NEXT-2 one-shot peer exchange (common.cuh ExchPeers)
   uint8_t* d_xbuf = nullptr;     // this rank's exchange buffer (records x 2 parities + flags)
   uint8_t** d_xbases = nullptr;  // [world] device copy of every rank's mapped base
@@ -584,6 +585,7 @@ static SelectArgs select_args(sampler* h, const void* logits, int64_t ld, int32_
   s.params_tab = h->d_params;
   s.seeds = seeds;
   s.step = step;
+  s.step_dev = h->d_step_src;
   s.kcand = h->cfg.max_top_k;
   s.pen_mode = h->cfg.penalty_mode;
   s.mode = 0;
@@ -636,6 +638,7 @@ static MergeArgs merge_args(sampler* h, const int32_t* slots, const sampling_par
   m.params_tab = h->d_params;
   m.seeds = seeds;
   m.step = step;
+  m.step_dev = h->d_step_src;
   m.append = append;
   m.hs = hist_state(h);
   m.ro = ro;
@@ -709,6 +712,7 @@ static int do_sample(sampler* h, const void* logits, int64_t ld, int32_t B, cons
     e.params_tab = h->d_params;
     e.seeds = seeds_dev;
     e.step = step;
+    e.step_dev = h->d_step_src;
     e.append = append;
     e.pen_mode = h->cfg.penalty_mode;
     e.hs = a.hs;
@@ -879,6 +883,7 @@ int sampler_resolve_round(sampler* h, const void* logits_slice, int64_t ld, int3
   a.params_tab = h->d_params;
   a.seeds = seeds_dev;
   a.step = step;
+  a.step_dev = h->d_step_src;
   a.append = append_to_history;
   a.hs = hist_state(h);
   a.ro = RowOut{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
@@ -1023,6 +1028,13 @@ int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, in
     tmark(h, ++nk, st);
   }
   h->last_launches = nk;
+  return SAMPLER_OK;
+}
+
+int sampler_set_step_source(sampler* h, const uint64_t* step_dev) {
+  if (!h) return SAMPLER_EINVAL;
+  if (step_dev && ((uintptr_t)step_dev) % 8) return fail(h, SAMPLER_EINVAL, "step_dev must be 8-byte aligned");
+  h->d_step_src = step_dev;
   return SAMPLER_OK;
 }
 

@@ -45,6 +45,7 @@ struct SelectArgs {
   const sampling_params* params_tab;
   const uint64_t* seeds;
   uint64_t step;
+  const uint64_t* step_dev;  // nullable: the decode step read on the device
   int kcand, pen_mode, mode, append, pending_ok;
   HistState hs;
   const PartRec* parts;    // phase A partial records [B][rpr][kCW]
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       ms.bs.i[w] = (int)fw;
     }
     if (w == kBW - 2 && lane == 0) {  // the draw's uniform, off the critical path
-      const double uu = philox_uniform(seed, prm.request_id, a.step);
+      const double uu = philox_uniform(seed, prm.request_id, a.step_dev ? *a.step_dev : a.step);
       *reinterpret_cast<double*>(ctl + 14) = uu;
     }
     if (w == kBW - 1 && nsv >= keff && nsv <= kBT) {

@@ -27,7 +27,7 @@ EXPORTED = [
     "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
     "sampler_resolve_bytes", "sampler_resolve_round", "sampler_resolve_max_rounds",
     "sampler_exchange_init", "sampler_exchange_open", "sampler_exchange_set_peers", "sampler_sample_exchange",
-    "sampler_get_slot_flags",
+    "sampler_get_slot_flags", "sampler_set_step_source",
 ]
 
 
@@ -97,6 +97,7 @@ def _load():
         "sampler_exchange_init": ([P, I32, I32, C.c_uint32, P, P], I32),
         "sampler_exchange_open": ([P, P], I32),
         "sampler_get_slot_flags": ([P, I32, P], I32),
+        "sampler_set_step_source": ([P, P], I32),
         "sampler_exchange_set_peers": ([P, P], I32),
         "sampler_sample_exchange": ([P, P, I64, I32, P, P, P, U64, I32, P, P, P, P, I32, P], I32),
         "sampler_last_launch_count": ([P], I32),
@@ -213,6 +214,12 @@ class Sampler:
         f = C.c_int32()
         self._check(_lib.sampler_get_slot_flags(self.h, int(slot), C.byref(f)))
         return int(f.value)
+
+    def set_step_source(self, step_dev=None):
+        """step_dev: a device int64 tensor of one element (or None): later calls read the Philox step from
+        it on the device (CUDA-graph replays of a decode loop advance it), ignoring their `step` argument."""
+        self._step_src = step_dev  # (kept alive with the handle)
+        self._check(_lib.sampler_set_step_source(self.h, _ptr(step_dev)))
 
     def last_launch_count(self) -> int:
         return int(_lib.sampler_last_launch_count(self.h))

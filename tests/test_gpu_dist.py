@@ -149,12 +149,15 @@ def test_peer_exchange_nccl_world1_graph_replays(nccl_group):
     assert torch.equal(eager["tokens"], ref["tokens"])
     assert_parity(wl, eager, oracle_run(wl, 0))
     out = s._outs(wl.B, None)
+    step = torch.tensor([5], dtype=torch.int64, device="cuda")
+    s.set_step_source(step)  # the whole decode step in one graph: the Philox step advances per replay
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=torch.cuda.Stream()):
-        sample_vocab_sharded_p2p(s, x, 5, out=out, append=True)
-    for _ in range(3):
+        sample_vocab_sharded_p2p(s, x, 0, out=out, append=True)
+        step.add_(1)
+    for i in range(3):
         g.replay()
-        ref = full.sample(x, 5, append=True)
+        ref = full.sample(x, 5 + i, append=True)
         torch.cuda.synchronize()
         assert (out["status"] == 0).all()
         assert torch.equal(out["tokens"], ref["tokens"])

@@ -578,3 +578,37 @@ def test_history_append_through_exact_kernel_rows():
             ids = sorted(set(wl.prompts[b]) | set(outputs[b]))
             assert h["uniq_ids"] == ids
             assert h["uniq_counts"] == [outputs[b].count(i) for i in ids]
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c2"])
+def test_graph_replays_advance_a_device_step(cfg):
+    """A decode step captured ONCE (sample with in-kernel append + the step increment) and replayed: with
+    sampler_set_step_source every replay draws with the next Philox step (TSEM-style versioned per-step
+    input) and equals eager sampling with host steps, append included (c2: exact-kernel rows)."""
+    import torch
+    wl = make_workload(cfg, B=8, V=20000)
+    x = device_logits(wl)
+    ref = make_sampler(wl, max_history=1024)
+    s = make_sampler(wl, max_history=1024)
+    step = torch.tensor([100], dtype=torch.int64, device="cuda")
+    s.set_step_source(step)
+    out = s._outs(wl.B, None)
+    s.sample(x, 0, out=out)  # warm-up (no append)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        s.sample(x, 0, out=out, append=True)
+        step.add_(1)
+    toks = []
+    for i in range(4):
+        g.replay()
+        r = ref.sample(x, 100 + i, append=True)
+        torch.cuda.synchronize()
+        assert torch.equal(out["tokens"], r["tokens"]), i
+        assert torch.allclose(out["logprobs"], r["logprobs"], rtol=1e-6, atol=1e-7)
+        toks.append(out["tokens"].clone())
+    assert any(not torch.equal(toks[0], t) for t in toks[1:])  # the draws moved with the step
+    assert int(step.item()) == 104
+    for b in range(wl.B):
+        assert s.get_history(b)["output"] == ref.get_history(b)["output"]
+    s.set_step_source(None)
