@@ -315,6 +315,19 @@ int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, in
                             int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
                             int32_t* row_status_dev, int32_t phases, void* cuda_stream);
 
+/* ASYNC.  One resolve round (sampler_resolve_round, NEXT-1) through the peer exchange instead of a
+ * caller all-gather: the previous round's payloads are read from this rank's exchange buffer once
+ * every rank's flag for the row has arrived (bounded wait: SAMPLER_ROW_EXCHANGE_TIMEOUT), and this
+ * round's payload is stored into every rank's buffer with the row's flag raised.  Rounds 0, 1, 2, ...
+ * follow sampler_sample_exchange (or sampler_merge) on every rank, exactly as with
+ * sampler_resolve_round but with no collective call in between; the round count rule is the same. */
+int sampler_resolve_round_exchange(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
+                                   const int32_t* slots_dev, const sampling_params* params_dev,
+                                   const uint64_t* seeds_dev, uint64_t step, int32_t round,
+                                   int32_t append_to_history, int32_t* tokens_dev, float* logprobs_dev,
+                                   float* filtered_logprobs_dev, int32_t* row_status_dev,
+                                   int32_t* active_dev, void* cuda_stream);
+
 /* ---- per-step parameters on the device (CUDA-graph replays of a decode loop) ----------------
  * The TSEM idea of versioned per-step inputs (§5.2): with step_dev != NULL (device
  * uint64, 8-byte aligned, owned by the caller and alive while calls use it), every later sample /

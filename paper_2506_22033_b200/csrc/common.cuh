@@ -96,6 +96,7 @@ struct ExchPeers {
   uint32_t* seq;          // [B_max] local sequence numbers of phase 1 (publish)
   uint32_t* mseq;         // [B_max] local sequence numbers of the merge (the same count)
   uint64_t timeout_ns;
+  int64_t region_off;     // bytes from a base to this region (records: 0; resolve payloads: after them)
 };
 // flag store / load: system scope across GPUs (NVLink peers), GPU scope when every rank is this GPU
 __device__ __forceinline__ void st_release_flag(uint32_t* p, uint32_t v, bool sys) {

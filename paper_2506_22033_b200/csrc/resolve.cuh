@@ -44,6 +44,7 @@ constexpr int kResBodyWords = kResBins / 2 + 2 * kResBins;      // counts (u32) 
 constexpr int kResCap = kResBodyWords - 2;                      // composites per gather payload
 constexpr int64_t kResRowBytes = 16 + 8 * (int64_t)kResBodyWords;
 constexpr int kResMaxRounds = 20;                               // 2 x (8 hist + 1 gather) + TOT + RES
+static_assert(kResRowBytes % 16 == 0, "payload rows are copied as 16-byte vectors");
 
 enum { RPH_DONE = 0, RPH_K = 1, RPH_P = 2, RPH_TOT = 3, RPH_RES = 4 };
 enum { RK_NONE = 0, RK_HIST = 1, RK_GATHER = 2, RK_TOT = 3, RK_RES = 4 };
@@ -90,6 +91,7 @@ struct ResolveArgs {
   ResState* rs;         // [B]
   int32_t* active;      // rows still unresolved after this round (nullable)
   int pen_mode;
+  ExchPeers rx;         // rx.world > 0: payloads through the one-shot peer exchange (NEXT-2), not gathered
 };
 
 __device__ __forceinline__ double to_d(u128 x) {
@@ -191,12 +193,18 @@ struct ResSmem {
   int32_t tlast[kResThreads];
   int nent;
   int pick_le;
+  const uint8_t* gbase;  // previous round's payloads (see res_rank_row)
+  int64_t gpitch;
+  uint8_t* outp;         // this round's payload of the row
+  int timed_out;
   double pick_w;
   float pick_z;
 };
 
-__device__ __forceinline__ const uint8_t* res_rank_row(const ResolveArgs& a, int r, int row) {
-  return a.gathered + ((int64_t)r * a.B + row) * kResRowBytes;
+// the previous round's payload of rank r for `row`: the caller's gathered buffer, or this rank's
+// exchange region (parity of the previous publish) — g / pitch are set per CTA in the prologue
+__device__ __forceinline__ const uint8_t* res_rank_row(const uint8_t* g, int64_t pitch, int r, int row) {
+  return g + (int64_t)r * pitch + (int64_t)row * kResRowBytes;
 }
 
 // Start the P search over the domain { c >= lo } (W1 = the domain's mass, taken at the first ingest).
@@ -255,11 +263,49 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     r.minp = (double)prm.min_p;
     r.prm = prm;
   }
+  if (tid == 0) {
+    sm.timed_out = 0;
+    const ExchPeers& x = a.rx;
+    if (x.world == 0) {
+      sm.gbase = a.gathered;
+      sm.gpitch = (int64_t)a.B * kResRowBytes;
+      sm.outp = a.payload + (int64_t)row * kResRowBytes;
+    } else {
+      // peer exchange: every rank published the previous round's payload of this row with sequence
+      // number rq = x.seq[row] into every rank's region (parity rq & 1); wait for all of them
+      const uint32_t rq = x.seq[row];
+      uint8_t* own = x.bases[x.rank] + x.region_off;
+      if (a.round > 0 && st.phase != RPH_DONE) {
+        const uint32_t* fl = reinterpret_cast<const uint32_t*>(own + x.flags_off);
+        const uint64_t t0 = gtimer();
+        for (int q = 0; q < x.world && !sm.timed_out; ++q)
+          while ((int32_t)(ld_acquire_flag(fl + (int64_t)q * x.nslots + row, x.world > 1) - rq) < 0) {
+            if (gtimer() - t0 > x.timeout_ns) {
+              sm.timed_out = 1;
+              break;
+            }
+            __nanosleep(64);
+          }
+      }
+      sm.gbase = own + (int64_t)(rq & 1) * x.par_pitch;
+      sm.gpitch = x.rank_pitch;
+      sm.outp = own + (int64_t)((rq + 1) & 1) * x.par_pitch + (int64_t)x.rank * x.rank_pitch +
+                (int64_t)row * kResRowBytes;
+    }
+    if (sm.timed_out) {  // a peer stopped: report the row, never hang the GPU
+      a.ro.tokens[row] = -1;
+      a.ro.logprobs[row] = NAN;
+      if (a.ro.flogprobs) a.ro.flogprobs[row] = NAN;
+      if (a.ro.status) a.ro.status[row] = SAMPLER_ROW_EXCHANGE_TIMEOUT;
+      st.phase = RPH_DONE;
+      a.rs[row] = st;
+    }
+  }
   __syncthreads();
   if (st.phase == RPH_DONE) {
     if (tid == 0) {
       if (a.round == 0) a.rs[row] = st;
-      reinterpret_cast<ResHdr*>(a.payload + (int64_t)row * kResRowBytes)->kind = RK_NONE;
+      if (a.rx.world == 0) reinterpret_cast<ResHdr*>(sm.outp)->kind = RK_NONE;
     }
     return;
   }
@@ -275,7 +321,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
         unsigned long long c = 0;
         u128 m = 0;
         for (int r = 0; r < a.world; ++r) {
-          const uint8_t* p = res_rank_row(a, r, row) + 16;
+          const uint8_t* p = res_rank_row(sm.gbase, sm.gpitch, r, row) + 16;
           c += reinterpret_cast<const uint32_t*>(p)[tid];
           const uint64_t* mp = reinterpret_cast<const uint64_t*>(p + 4 * kResBins);
           m += mk128(mp[2 * tid], mp[2 * tid + 1]);
@@ -334,7 +380,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
       if (tid == 0) {
         int n = 0;
         for (int r = 0; r < a.world; ++r) {
-          const uint8_t* p = res_rank_row(a, r, row);
+          const uint8_t* p = res_rank_row(sm.gbase, sm.gpitch, r, row);
           const int nr = (int)reinterpret_cast<const ResHdr*>(p)->n;
           const uint64_t* e = reinterpret_cast<const uint64_t*>(p + 16);
           for (int i = 0; i < nr && n < kResCap; ++i) sm.ent[n++] = e[i];
@@ -380,7 +426,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
       if (tid == 0) {
         u128 tot = 0;
         for (int r = 0; r < a.world; ++r) {
-          const uint64_t* b = reinterpret_cast<const uint64_t*>(res_rank_row(a, r, row) + 16);
+          const uint64_t* b = reinterpret_cast<const uint64_t*>(res_rank_row(sm.gbase, sm.gpitch, r, row) + 16);
           tot += mk128(b[0], b[1]);
         }
         st.W = to_d(tot);
@@ -389,7 +435,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
         u128 pre = 0;
         int owner = -1, lastr = 0;
         for (int r = 0; r < a.world; ++r) {
-          const uint64_t* b = reinterpret_cast<const uint64_t*>(res_rank_row(a, r, row) + 16);
+          const uint64_t* b = reinterpret_cast<const uint64_t*>(res_rank_row(sm.gbase, sm.gpitch, r, row) + 16);
           const u128 tr = mk128(b[0], b[1]);
           if (b[2] > 0) lastr = r;
           if (to_d(pre + tr) > st.target) {
@@ -411,7 +457,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
       __syncthreads();
     } else if (ph == RPH_RES) {
       if (tid == 0) {
-        const uint8_t* p = res_rank_row(a, st.owner, row);
+        const uint8_t* p = res_rank_row(sm.gbase, sm.gpitch, st.owner, row);
         const ResHdr hd = *reinterpret_cast<const ResHdr*>(p);
         const uint64_t* b = reinterpret_cast<const uint64_t*>(p + 16);
         int32_t tok = -1;
@@ -431,7 +477,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
   }
 
   // ================================================================ this round's payload
-  uint8_t* out = a.payload + (int64_t)row * kResRowBytes;
+  uint8_t* out = sm.outp;
   ResHdr* oh = reinterpret_cast<ResHdr*>(out);
   uint64_t* ob = reinterpret_cast<uint64_t*>(out + 16);
   const int ph = st.phase;
@@ -585,6 +631,28 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     }
   } else if (tid == 0) {
     oh->kind = RK_NONE;
+  }
+  if (a.rx.world > 0 && st.phase != RPH_DONE) {
+    // publish: the payload (written into this rank's own region above) copied into every peer's
+    // region, then the row's flag raised everywhere (release after the CTA barrier)
+    const ExchPeers& x = a.rx;
+    __syncthreads();
+    const int64_t off = out - x.bases[x.rank];
+    constexpr int kN16 = (int)(kResRowBytes / 16);
+    for (int p = 0; p < x.world; ++p) {
+      if (p == x.rank) continue;
+      uint4* dst = reinterpret_cast<uint4*>(x.bases[p] + off);
+      const uint4* src = reinterpret_cast<const uint4*>(out);
+      for (int i = tid; i < kN16; i += kResThreads) dst[i] = src[i];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t sq = x.seq[row] + 1;
+      x.seq[row] = sq;
+      for (int p = 0; p < x.world; ++p)
+        st_release_flag(reinterpret_cast<uint32_t*>(x.bases[p] + x.region_off + x.flags_off) + (int64_t)x.rank * x.nslots + row,
+                        sq, x.world > 1);
+    }
   }
   if (tid == 0) {
     a.rs[row] = st;

@@ -43,10 +43,11 @@ struct sampler {
   // NEXT-2 one-shot peer exchange (common.cuh ExchPeers)
   uint8_t* d_xbuf = nullptr;     // this rank's exchange buffer (records x 2 parities + flags)
   uint8_t** d_xbases = nullptr;  // [world] device copy of every rank's mapped base
-  uint32_t* d_xseq = nullptr;    // [2][max_batch] publish / merge sequence numbers
+  uint32_t* d_xseq = nullptr;    // [3][max_batch] publish / merge / resolve sequence numbers
   std::vector<void*> x_opened;   // IPC mappings to close
   int x_world = 0, x_rank = 0;
   int64_t x_bytes = 0;
+  int64_t x_res_off = 0;         // the resolve payload region inside the exchange buffer
   uint64_t x_timeout_ns = 0;
   uint32_t* d_pmask = nullptr;  // [max_batch][spr * 32] penalty presence bitmaps (HistState)
   PartRec* d_parts = nullptr;   // [max_batch][rpr_max][kCW] phase-A partial records
@@ -930,14 +931,19 @@ int sampler_exchange_init(sampler* h, int32_t world, int32_t rank, uint32_t time
   if (h->d_xbuf) return fail(h, SAMPLER_EINVAL, "exchange already initialised on this handle");
   CK(h, cudaSetDevice(h->cfg.device));
   const int64_t Bm = h->cfg.max_batch;
-  const int64_t bytes = 2 * (int64_t)world * Bm * h->rec_stride + (int64_t)world * Bm * 4;
+  // [records: 2 parities x world x B_max][flags: world x B_max] then, 256-aligned, the same for the
+  // resolve rounds' payloads (NEXT-1 over the peer exchange)
+  const int64_t rec_bytes = 2 * (int64_t)world * Bm * h->rec_stride + (int64_t)world * Bm * 4;
+  const int64_t res_off = (rec_bytes + 255) / 256 * 256;
+  const int64_t bytes = res_off + 2 * (int64_t)world * Bm * kResRowBytes + (int64_t)world * Bm * 4;
+  h->x_res_off = res_off;
   if (cudaMalloc((void**)&h->d_xbuf, bytes) != cudaSuccess || cudaMalloc((void**)&h->d_xbases, sizeof(void*) * world) != cudaSuccess ||
-      cudaMalloc((void**)&h->d_xseq, 2 * sizeof(uint32_t) * Bm) != cudaSuccess) {
+      cudaMalloc((void**)&h->d_xseq, 3 * sizeof(uint32_t) * Bm) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, SAMPLER_ENOMEM, "exchange buffer allocation failed");
   }
   CK(h, cudaMemset(h->d_xbuf, 0, bytes));
-  CK(h, cudaMemset(h->d_xseq, 0, 2 * sizeof(uint32_t) * Bm));
+  CK(h, cudaMemset(h->d_xseq, 0, 3 * sizeof(uint32_t) * Bm));
   h->x_world = world;
   h->x_rank = rank;
   h->x_bytes = bytes;
@@ -1035,6 +1041,67 @@ int sampler_set_step_source(sampler* h, const uint64_t* step_dev) {
   if (!h) return SAMPLER_EINVAL;
   if (step_dev && ((uintptr_t)step_dev) % 8) return fail(h, SAMPLER_EINVAL, "step_dev must be 8-byte aligned");
   h->d_step_src = step_dev;
+  return SAMPLER_OK;
+}
+
+static ExchPeers exch_peers_resolve(const sampler* h) {
+  ExchPeers x = exch_peers(h);
+  x.row_stride = kResRowBytes;
+  x.rank_pitch = kResRowBytes * (int64_t)h->cfg.max_batch;
+  x.par_pitch = x.rank_pitch * h->x_world;
+  x.flags_off = 2 * x.par_pitch;
+  x.region_off = h->x_res_off;
+  x.seq = h->d_xseq + 2 * h->cfg.max_batch;
+  x.mseq = nullptr;
+  return x;
+}
+
+int sampler_resolve_round_exchange(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
+                                   const int32_t* slots_dev, const sampling_params* params_dev,
+                                   const uint64_t* seeds_dev, uint64_t step, int32_t round, int32_t append_to_history,
+                                   int32_t* tokens_dev, float* logprobs_dev, float* filtered_logprobs_dev,
+                                   int32_t* row_status_dev, int32_t* active_dev, void* cuda_stream) {
+  if (!h) return SAMPLER_EINVAL;
+  if (!h->d_xbuf) return fail(h, SAMPLER_EINVAL, "sampler_exchange_init / open first");
+  int rc = check_logits(h, logits_slice, ld, B);
+  if (rc) return rc;
+  if (!tokens_dev || !logprobs_dev) return fail(h, SAMPLER_EINVAL, "NULL argument");
+  if (round < 0) return fail(h, SAMPLER_EINVAL, "round must be >= 0");
+  CK(h, cudaSetDevice(h->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  ResolveArgs a{};
+  a.logits = (const uint8_t*)logits_slice;
+  a.ld = ld;
+  a.esize = (h->cfg.logits_dtype == SAMPLER_BF16) ? 2 : 4;
+  a.B = B;
+  a.V = h->cfg.vocab_size;
+  a.kcand = h->cfg.max_top_k;
+  a.world = h->x_world;
+  a.rank = h->x_rank;
+  a.round = round;
+  a.slots = slots_dev;
+  a.params_dev = params_dev;
+  a.params_tab = h->d_params;
+  a.seeds = seeds_dev;
+  a.step = step;
+  a.step_dev = h->d_step_src;
+  a.append = append_to_history;
+  a.hs = hist_state(h);
+  a.ro = RowOut{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
+  a.info = h->d_info;
+  a.rs = h->d_rs;
+  a.active = active_dev;
+  a.pen_mode = h->cfg.penalty_mode;
+  a.rx = exch_peers_resolve(h);
+  if (active_dev) CK(h, cudaMemsetAsync(active_dev, 0, sizeof(int32_t), st));
+  tmark(h, 0, st);
+  if (h->cfg.logits_dtype == SAMPLER_BF16)
+    resolve_kernel<__nv_bfloat16><<<B, kResThreads, 0, st>>>(a);
+  else
+    resolve_kernel<float><<<B, kResThreads, 0, st>>>(a);
+  CK(h, cudaGetLastError());
+  tmark(h, 1, st);
+  h->last_launches = 1;
   return SAMPLER_OK;
 }
 

@@ -70,18 +70,23 @@ def setup_peer_exchange(sampler: Sampler, group=None, timeout_ms=0):
 def sample_vocab_sharded_p2p(sampler: Sampler, logits_slice: torch.Tensor, step: int, group=None, slots=None,
                              params=None, seeds=None, append=False, out=None, resolve=False, resolve_rounds=None,
                              resolve_bufs=None):
-    """The vocab-sharded step through the one-shot peer exchange (one library call, no NCCL launch; after
-    setup_peer_exchange).  Rows not bounded by the candidates can be finished by the resolve rounds
-    (resolve=True; those rounds use NCCL all-gathers)."""
+    """The vocab-sharded step through the one-shot peer exchange (after setup_peer_exchange): one library call
+    for the candidate step and, with resolve=True, the resolve rounds for rows the candidates do not bound,
+    their payloads also through the peer exchange — no collective call on the data path.  resolve_rounds:
+    None = adaptive (one 4-byte read per round; under graph capture the bound), or a fixed count."""
     out = sampler.sample_exchange(logits_slice, step, slots=slots, params=params, seeds=seeds, append=append,
                                   out=out)
     if resolve:
-        world = dist.get_world_size(group)
         if resolve_rounds is None and logits_slice.is_cuda and torch.cuda.is_current_stream_capturing():
             resolve_rounds = sampler.resolve_max_rounds()
-        resolve_unbounded(sampler, logits_slice, step, out, lambda g, p: dist.all_gather_into_tensor(g, p, group=group),
-                          world, dist.get_rank(group), slots=slots, params=params, seeds=seeds, append=append,
-                          rounds=resolve_rounds, bufs=resolve_bufs)
+        active = resolve_bufs[2] if resolve_bufs is not None else torch.zeros(1, dtype=torch.int32,
+                                                                              device=logits_slice.device)
+        kw = dict(slots=slots, params=params, seeds=seeds, append=append, active=active)
+        sampler.resolve_round_exchange(logits_slice, step, 0, out, **kw)
+        n = 0
+        while (resolve_rounds is None and int(active.item()) > 0) or (resolve_rounds is not None and n < resolve_rounds):
+            n += 1
+            sampler.resolve_round_exchange(logits_slice, step, n, out, **kw)
     return out
 
 

@@ -27,7 +27,7 @@ EXPORTED = [
     "sampler_version", "sampler_debug_trace", "sampler_set_timing", "sampler_kernel_times",
     "sampler_resolve_bytes", "sampler_resolve_round", "sampler_resolve_max_rounds",
     "sampler_exchange_init", "sampler_exchange_open", "sampler_exchange_set_peers", "sampler_sample_exchange",
-    "sampler_get_slot_flags", "sampler_set_step_source",
+    "sampler_get_slot_flags", "sampler_set_step_source", "sampler_resolve_round_exchange",
 ]
 
 
@@ -98,6 +98,7 @@ def _load():
         "sampler_exchange_open": ([P, P], I32),
         "sampler_get_slot_flags": ([P, I32, P], I32),
         "sampler_set_step_source": ([P, P], I32),
+        "sampler_resolve_round_exchange": ([P, P, I64, I32, P, P, P, U64, I32, I32, P, P, P, P, P, P], I32),
         "sampler_exchange_set_peers": ([P, P], I32),
         "sampler_sample_exchange": ([P, P, I64, I32, P, P, P, U64, I32, P, P, P, P, I32, P], I32),
         "sampler_last_launch_count": ([P], I32),
@@ -329,6 +330,15 @@ class Sampler:
             int(step) & 0xFFFFFFFFFFFFFFFF, int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]),
             _ptr(out.get("filtered_logprobs")), _ptr(out.get("status")), int(phases), _stream(stream)))
         return out
+
+    def resolve_round_exchange(self, logits_slice, step, rnd, out, slots=None, params=None, seeds=None, append=False,
+                               active=None, stream=None):
+        """One resolve round through the peer exchange (no collective; after exchange_init / open)."""
+        B = logits_slice.shape[0]
+        self._check(_lib.sampler_resolve_round_exchange(
+            self.h, _ptr(logits_slice), logits_slice.stride(0), B, _ptr(slots), _ptr(params), _ptr(seeds),
+            int(step) & 0xFFFFFFFFFFFFFFFF, int(rnd), int(bool(append)), _ptr(out["tokens"]), _ptr(out["logprobs"]),
+            _ptr(out.get("filtered_logprobs")), _ptr(out.get("status")), _ptr(active), _stream(stream)))
 
 
 def params_to_device(params, device=0):

@@ -212,3 +212,38 @@ def test_peer_exchange_ipc_two_processes_one_gpu():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def test_peer_exchange_with_resolve_rounds_in_one_graph(nccl_group):
+    """The whole sharded decode step with unbounded rows through the peer exchange — candidate step, the
+    fixed resolve round count, the step increment — captured once and replayed, == unsharded eager steps."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import sample_vocab_sharded_p2p, setup_peer_exchange
+    wl = make_workload("c2", B=6, V=20000)
+    x = device_logits(wl)
+    full = make_sampler(wl, max_history=1024)
+    s = Sampler(wl.V, wl.B, max_history=1024, dtype=wl.dtype, vocab_offset=0, vocab_local=wl.V)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    setup_peer_exchange(s)
+    eager = sample_vocab_sharded_p2p(s, x, 0, resolve=True)
+    ref = full.sample(x, 0)
+    torch.cuda.synchronize()
+    assert (eager["status"] == 0).all() and torch.equal(eager["tokens"], ref["tokens"])
+    step = torch.tensor([3], dtype=torch.int64, device="cuda")
+    s.set_step_source(step)
+    out = s._outs(wl.B, None)
+    active = torch.zeros(1, dtype=torch.int32, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        sample_vocab_sharded_p2p(s, x, 0, out=out, append=True, resolve=True,
+                                 resolve_bufs=(None, None, active))
+        step.add_(1)
+    for i in range(3):
+        g.replay()
+        ref = full.sample(x, 3 + i, append=True)
+        torch.cuda.synchronize()
+        assert (out["status"] == 0).all()
+        assert torch.equal(out["tokens"], ref["tokens"]), i

@@ -253,3 +253,41 @@ def test_sharded_edge_rows(dtype):
         outs, n, _ = sharded_inprocess(wl, x, G, step=3)
         assert (outs[0]["status"] == 0).all(), outs[0]["status"]
         _check_all_ranks(wl, outs, oracle_run(wl, 3))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_peer_exchange_resolve_rounds(G):
+    """NEXT-1 + NEXT-2: unbounded rows (c2 top-p-only, mixed) resolved with every payload through the peer
+    exchange (sampler_resolve_round_exchange: flags, parities, no collective), G ranks of one process in lock
+    step over two decode steps with append, vs the oracle replaying the grown histories."""
+    import torch
+    wl = make_workload("c2", B=6, V=24000)
+    wl.params[1] = RowParams(temperature=0.8, min_p=0.02, seed=3, request_id=3)
+    wl.params[2] = RowParams(temperature=0.7, top_k=700, top_p=0.9, seed=4, request_id=4)
+    wl.params[3] = RowParams(temperature=0.0, seed=5, request_id=5)
+    x = device_logits(wl)
+    shards, bounds = _exchange_shards(wl, G)
+    xs = [x[:, lo:hi] for lo, hi in bounds]
+    outputs = [list(o) for o in wl.outputs]
+    for step in range(2):
+        for g, sh in enumerate(shards):
+            sh.sample_exchange(xs[g], step, append=True, phases=1)
+        outs = [sh.sample_exchange(xs[g], step, append=True, phases=2) for g, sh in enumerate(shards)]
+        act = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in shards]
+        r = 0
+        while True:
+            for g, sh in enumerate(shards):
+                sh.resolve_round_exchange(xs[g], step, r, outs[g], append=True, active=act[g])
+            torch.cuda.synchronize()
+            if int(act[0].item()) == 0:
+                break
+            r += 1
+            assert r <= 20
+        cur = Workload(wl.name, wl.B, wl.V, wl.dtype, wl.raw, wl.prompts, [list(o) for o in outputs], wl.params)
+        assert (outs[0]["status"] == 0).all(), outs[0]["status"]
+        _check_all_ranks(cur, outs, oracle_run(cur, step))
+        for b, t in enumerate(outs[0]["tokens"].cpu().tolist()):
+            outputs[b].append(int(t))
+    for sh in shards:
+        for b in range(wl.B):
+            assert sh.get_history(b)["output"] == outputs[b]
