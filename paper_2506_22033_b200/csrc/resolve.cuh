@@ -39,6 +39,7 @@ namespace smp {
 typedef unsigned __int128 u128;
 
 constexpr int kResThreads = 512;
+constexpr int kResW = kResThreads / 32;
 constexpr int kResBins = 256;                                   // 8 bits of the composite per round
 constexpr int kResBodyWords = kResBins / 2 + 2 * kResBins;      // counts (u32) + masses (u128)
 constexpr int kResCap = kResBodyWords - 2;                      // composites per gather payload
@@ -68,6 +69,9 @@ struct __align__(16) ResState {
   double S;
   float M;
   int32_t last;                       // u*W at the very top of the mass: the last kept id wins
+  uint64_t wlo[16], whi[16];          // TOT -> RES: kept mass of each warp's id range (this rank)
+  uint32_t wcnt[16];
+  int32_t wlast[16];
 };
 
 struct ResolveArgs {
@@ -116,6 +120,14 @@ __device__ __forceinline__ void atom_add128(unsigned long long* lo, unsigned lon
   if (old + vl < old) vh += 1;
   if (vh) atomicAdd(hi, vh);
 }
+// 64-bit shared add as two native 32-bit atomics with the carry (integer: order-independent)
+__device__ __forceinline__ void smem_add_u64_32(uint64_t* p, uint64_t v) {
+  uint32_t* p32 = reinterpret_cast<uint32_t*>(p);
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(p32, lo);
+  const uint32_t up = hi + ((uint32_t)(old + lo) < old ? 1u : 0u);
+  if (up) atomicAdd(p32 + 1, up);
+}
 __device__ __forceinline__ u128 shfl_down128(u128 v, int o) {
   const uint64_t lo = __shfl_down_sync(kFull, (uint64_t)v, o);
   const uint64_t hi = __shfl_down_sync(kFull, (uint64_t)(v >> 64), o);
@@ -127,7 +139,7 @@ struct ResRow {  // per-row constants of one round (smem)
   const UniqEntry* uniq;
   const uint32_t* pm;
   int nu, slot;
-  double M, tau, minp;
+  double M, tau, inv_tau, minp;
   sampling_params prm;
 };
 
@@ -150,7 +162,32 @@ __device__ __forceinline__ float res_zp(const ResRow& r, const HistState& hs, in
   if (lo < r.nu && r.uniq[lo].id == id) return apply_penalty(x, r.uniq[lo].meta, r.prm, pen_mode);
   return x;
 }
-__device__ __forceinline__ double res_w(float z, const ResRow& r) { return exp(((double)z - r.M) / r.tau); }
+__device__ __forceinline__ double res_w(float z, const ResRow& r) { return exp(((double)z - r.M) * r.inv_tau); }
+
+// z' of element t of local vector v (loaded as u, its presence bits pb)
+template <typename T>
+__device__ __forceinline__ float res_elem(const ResRow& r, const HistState& hs, const uint4 u, uint32_t pb, int v, int t,
+                                          int pen_mode) {
+  float z = Dec<T>::elem(u, t);
+  if ((pb >> t) & 1u) {
+    const int32_t id = hs.voff + v * Dec<T>::N + t;
+    int lo = 0, hi = r.nu;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (r.uniq[mid].id < id) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < r.nu && r.uniq[lo].id == id) z = apply_penalty(z, r.uniq[lo].meta, r.prm, pen_mode);
+  }
+  return z;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t res_pbits(const ResRow& r, int v) {
+  constexpr int VEC = Dec<T>::N;
+  if (!r.nu) return 0u;
+  const int k = v / 128, d = v % 128;
+  return (__ldg(r.pm + k * 32 + (d & 31)) >> ((d >> 5) * VEC)) & ((1u << VEC) - 1u);
+}
 
 // z' of the elements of local vector v (16 bytes: 8 bf16 / 4 f32), in id order: fn(z', local id);
 // penalised ids through the vector's bits of the slot's presence bitmap, then the sorted table
@@ -186,9 +223,11 @@ struct ResSmem {
   ResState st;
   ResRow row;
   unsigned long long cnt[kResBins], mlo[kResBins], mhi[kResBins];
+  uint32_t hc[kResBins];          // emission: counts (native 32-bit shared atomics)
+  uint64_t hm[3][kResBins];       // emission: masses in three 27-bit pieces (each sum < 2^58)
   uint64_t ent[kResCap], srt[kResCap];
   uint64_t wlo[kResCap], whi[kResCap];
-  uint64_t tlo[kResThreads], thi[kResThreads];
+  uint64_t tlo[kResThreads + 1], thi[kResThreads + 1];
   uint32_t tcnt[kResThreads];
   int32_t tlast[kResThreads];
   int nent;
@@ -260,6 +299,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     r.pm = a.hs.pmask + (int64_t)slot * a.hs.spr * 32;
     r.M = (double)st.M;
     r.tau = (double)decode_row(prm, a.V, a.kcand).tau;
+    r.inv_tau = 1.0 / r.tau;
     r.minp = (double)prm.min_p;
     r.prm = prm;
   }
@@ -481,11 +521,46 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
   ResHdr* oh = reinterpret_cast<ResHdr*>(out);
   uint64_t* ob = reinterpret_cast<uint64_t*>(out + 16);
   const int ph = st.phase;
+  // TOT / RES: warp-contiguous id ranges (coalesced rounds of 32 vectors); vec_kept = the kept mass
+  // of one vector (and, with `before`, the first element whose cumulative mass crosses u*W)
+    const uint64_t cut = st.cut;
+    const int Sw = ((nvec + kResW * 32 - 1) / (kResW * 32)) * 32;
+    const int wv0 = wid * Sw, wv1 = min(nvec, wv0 + Sw);
+    auto vec_kept = [&](int v, u128* m, uint32_t* n, int* lastle, int stop_le_for, const u128* before,
+                        int* pick) {
+      // kept mass of vector v (and, with `before`, the first element whose cumulative crosses u*W)
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(R.rowp) + v);
+      const uint32_t pb = res_pbits<T>(R, v);
+      u128 cum = before ? *before : (u128)0;
+      for (int t = 0; t < Dec<T>::N; ++t) {
+        const int le = v * Dec<T>::N + t;
+        if (le >= vloc) break;
+        const float z = res_elem<T>(R, a.hs, u, pb, v, t, a.pen_mode);
+        if (make_comp(z, a.hs.voff + le) < cut) continue;
+        const double w = res_w(z, R);
+        if (!(w > 0.0) || w < R.minp) continue;
+        const u128 f = wfix(w);
+        *m += f;
+        *n += 1;
+        *lastle = le;
+        if (before) {
+          cum += f;
+          if (*pick < 0 && to_d(cum) > st.target) *pick = le;
+        }
+      }
+      (void)stop_le_for;
+    };
   if ((ph == RPH_K || ph == RPH_P) && st.mode == RK_HIST) {
-    for (int j = tid; j < kResBins; j += kResThreads) sm.cnt[j] = sm.mlo[j] = sm.mhi[j] = 0;
+    for (int j = tid; j < kResBins; j += kResThreads) {
+      sm.hc[j] = 0;
+      sm.hm[0][j] = sm.hm[1][j] = sm.hm[2][j] = 0;
+    }
     __syncthreads();
     const uint64_t klo = st.klo, khi = st.khi;
     const int sh = st.shift;
+    // shared 64-bit atomics are compare-and-swap loops (they spin under the contention of the first
+    // rounds, where most of the row falls into a few bins): counts as native 32-bit atomics, masses
+    // as three 27-bit pieces, each accumulated by two native 32-bit atomics with the carry
     for (int v = tid; v < nvec; v += kResThreads)
       res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
         const uint64_t c = make_comp(z, a.hs.voff + le);
@@ -493,14 +568,19 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
         const double w = res_w(z, R);
         if (!(w > 0.0)) return;
         const int j = (int)((khi - c) >> sh);
-        atomicAdd(&sm.cnt[j], 1ull);
-        atom_add128(&sm.mlo[j], &sm.mhi[j], wfix(w));
+        const u128 f = wfix(w);
+        atomicAdd(&sm.hc[j], 1u);
+        smem_add_u64_32(&sm.hm[0][j], (uint64_t)f & 0x7FFFFFFull);
+        smem_add_u64_32(&sm.hm[1][j], (uint64_t)(f >> 27) & 0x7FFFFFFull);
+        const uint64_t p2 = (uint64_t)(f >> 54);
+        if (p2) smem_add_u64_32(&sm.hm[2][j], p2);
       });
     __syncthreads();
     for (int j = tid; j < kResBins; j += kResThreads) {
-      reinterpret_cast<uint32_t*>(ob)[j] = (uint32_t)sm.cnt[j];
-      ob[kResBins / 2 + 2 * j] = sm.mlo[j];
-      ob[kResBins / 2 + 2 * j + 1] = sm.mhi[j];
+      const u128 m = (u128)sm.hm[0][j] + ((u128)sm.hm[1][j] << 27) + ((u128)sm.hm[2][j] << 54);
+      reinterpret_cast<uint32_t*>(ob)[j] = sm.hc[j];
+      ob[kResBins / 2 + 2 * j] = (uint64_t)m;
+      ob[kResBins / 2 + 2 * j + 1] = (uint64_t)(m >> 64);
     }
     if (tid == 0) {
       oh->kind = RK_HIST;
@@ -525,33 +605,28 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     }
   } else if (ph == RPH_TOT) {
     u128 acc = 0;
-    unsigned long long kc = 0;
-    const uint64_t cut = st.cut;
-    for (int v = tid; v < nvec; v += kResThreads)
-      res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
-        if (make_comp(z, a.hs.voff + le) < cut) return;
-        const double w = res_w(z, R);
-        if (!(w > 0.0) || w < R.minp) return;
-        acc += wfix(w);
-        kc += 1;
-      });
+    uint32_t kc = 0;
+    int lastle = -1;
+    for (int v = wv0 + lane; v < wv1; v += 32) vec_kept(v, &acc, &kc, &lastle, 0, nullptr, nullptr);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       acc += shfl_down128(acc, o);
       kc += __shfl_down_sync(kFull, kc, o);
+      lastle = max(lastle, __shfl_down_sync(kFull, lastle, o));
     }
     if (lane == 0) {
-      sm.tlo[wid] = (uint64_t)acc;
-      sm.thi[wid] = (uint64_t)(acc >> 64);
-      sm.tcnt[wid] = (uint32_t)kc;
+      st.wlo[wid] = (uint64_t)acc;
+      st.whi[wid] = (uint64_t)(acc >> 64);
+      st.wcnt[wid] = kc;
+      st.wlast[wid] = lastle;
     }
     __syncthreads();
     if (tid == 0) {
       u128 t = 0;
       uint64_t n = 0;
-      for (int w = 0; w < kResThreads / 32; ++w) {
-        t += mk128(sm.tlo[w], sm.thi[w]);
-        n += sm.tcnt[w];
+      for (int w = 0; w < kResW; ++w) {
+        t += mk128(st.wlo[w], st.whi[w]);
+        n += st.wcnt[w];
       }
       ob[0] = (uint64_t)t;
       ob[1] = (uint64_t)(t >> 64);
@@ -563,56 +638,71 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     if (st.owner != a.rank) {
       if (tid == 0) oh->kind = RK_NONE;
     } else {
-      // the owner: kept mass per contiguous chunk (ascending id), chunk prefix, one thread re-walks
-      const int ch = (nvec + kResThreads - 1) / kResThreads;  // vectors per thread, id order
-      const int b0 = tid * ch, b1 = min(nvec, b0 + ch);
-      const uint64_t cut = st.cut;
-      u128 acc = 0;
-      uint32_t kc = 0;
-      int lastle = -1;
-      for (int v = b0; v < b1; ++v)
-        res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
-          if (make_comp(z, a.hs.voff + le) < cut) return;
-          const double w = res_w(z, R);
-          if (!(w > 0.0) || w < R.minp) return;
-          acc += wfix(w);
-          kc += 1;
-          lastle = le;
-        });
-      sm.tlo[tid] = (uint64_t)acc;
-      sm.thi[tid] = (uint64_t)(acc >> 64);
-      sm.tcnt[tid] = kc;
-      sm.tlast[tid] = lastle;
-      if (tid == 0) sm.pick_le = -1;
-      __syncthreads();
-      if (tid == 0) {  // exclusive prefix from the mass of the ranks before
-        u128 p = mk128(st.pre_lo, st.pre_hi);
-        int lt = -1;
-        for (int t = 0; t < kResThreads; ++t) {
-          const u128 v = mk128(sm.tlo[t], sm.thi[t]);
-          sm.tlo[t] = (uint64_t)p;
-          sm.thi[t] = (uint64_t)(p >> 64);
-          p += v;
-          if (sm.tcnt[t] > 0) lt = t;
-        }
-        if (st.last && lt >= 0) sm.pick_le = sm.tlast[lt];
+      // the owner: kept mass per warp range (ascending id, coalesced rounds of 32 vectors), the warp
+      // prefix from the mass of the ranks before; the warp holding u*W re-walks its range round by
+      // round (warp scans), the crossing lane walks its vector's elements
+      // (the warp totals of this rank's TOT pass, kept in the row state)
+      if (lane == 0) {
+        sm.tlo[wid] = st.wlo[wid];
+        sm.thi[wid] = st.whi[wid];
+        sm.tcnt[wid] = st.wcnt[wid];
+        sm.tlast[wid] = st.wlast[wid];
+      }
+      if (tid == 0) {
+        sm.pick_le = -1;
+        sm.nent = -1;  // (the crossing warp)
       }
       __syncthreads();
-      if (!st.last && kc > 0) {
-        const u128 p0 = mk128(sm.tlo[tid], sm.thi[tid]);
-        if (to_d(p0) <= st.target && to_d(p0 + acc) > st.target) {
-          u128 cum = p0;
-          int pick = -1;
-          for (int v = b0; v < b1 && pick < 0; ++v)
-            res_vec<T>(R, a.hs, v, vloc, a.pen_mode, [&](float z, int le) {
-              if (pick >= 0 || make_comp(z, a.hs.voff + le) < cut) return;
-              const double w = res_w(z, R);
-              if (!(w > 0.0) || w < R.minp) return;
-              cum += wfix(w);
-              if (to_d(cum) > st.target) pick = le;
-            });
-          sm.pick_le = pick;
+      if (tid == 0) {  // warp prefix from the mass of the ranks before; the crossing warp
+        u128 p = mk128(st.pre_lo, st.pre_hi);
+        int lt = -1;
+        for (int w = 0; w < kResW; ++w) {
+          const u128 v = mk128(sm.tlo[w], sm.thi[w]);
+          if (sm.nent < 0 && !st.last && sm.tcnt[w] > 0 && to_d(p + v) > st.target) {
+            sm.nent = w;
+            sm.tlo[kResW] = (uint64_t)p;
+            sm.thi[kResW] = (uint64_t)(p >> 64);
+          }
+          p += v;
+          if (sm.tcnt[w] > 0) lt = max(lt, sm.tlast[w]);
         }
+        if (st.last || sm.nent < 0) sm.pick_le = lt;  // (u*W at the top of the mass: the last kept id)
+      }
+      __syncthreads();
+      if (wid == sm.nent) {
+        u128 P = mk128(sm.tlo[kResW], sm.thi[kResW]);
+        int found = -1;
+        for (int vb = wv0; vb < wv1 && found < 0; vb += 32) {
+          const int v = vb + lane;
+          u128 m = 0;
+          uint32_t n = 0;
+          int ll = -1;
+          if (v < wv1) vec_kept(v, &m, &n, &ll, 0, nullptr, nullptr);
+          u128 incl = m;  // inclusive warp scan (u128)
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t lo = __shfl_up_sync(kFull, (uint64_t)incl, o);
+            const uint64_t hi = __shfl_up_sync(kFull, (uint64_t)(incl >> 64), o);
+            if (lane >= o) incl += mk128(lo, hi);
+          }
+          const bool cross = n > 0 && to_d(P + incl - m) <= st.target && to_d(P + incl) > st.target;
+          const unsigned bal = __ballot_sync(kFull, cross);
+          if (bal) {
+            int pk = -1;
+            if (lane == __ffs(bal) - 1) {
+              const u128 before = P + incl - m;
+              u128 m2 = 0;
+              uint32_t n2 = 0;
+              int l2 = -1;
+              vec_kept(v, &m2, &n2, &l2, 0, &before, &pk);
+              if (pk < 0) pk = l2;  // (rounding inside the vector: its last kept)
+            }
+            found = __shfl_sync(kFull, pk, __ffs(bal) - 1);
+          }
+          const uint64_t tl = __shfl_sync(kFull, (uint64_t)incl, 31), th = __shfl_sync(kFull, (uint64_t)(incl >> 64), 31);
+          P += mk128(tl, th);
+        }
+        if (lane == 0) sm.pick_le = found >= 0 ? found : sm.tlast[wid];  // (rounding: the warp's last kept)
       }
       __syncthreads();
       if (tid == 0) {
