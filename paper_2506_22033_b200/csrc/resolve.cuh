@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     const uint64_t cut = st.cut;
     const int Sw = ((nvec + kResW * 32 - 1) / (kResW * 32)) * 32;
     const int wv0 = wid * Sw, wv1 = min(nvec, wv0 + Sw);
-    auto vec_kept = [&](int v, u128* m, uint32_t* n, int* lastle, int stop_le_for, const u128* before,
+    auto vec_kept = [&](int v, u128* m, uint32_t* n, int* lastle, const u128* before,
                         int* pick) {
       // kept mass of vector v (and, with `before`, the first element whose cumulative crosses u*W)
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(R.rowp) + v);
@@ -548,7 +548,6 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
           if (*pick < 0 && to_d(cum) > st.target) *pick = le;
         }
       }
-      (void)stop_le_for;
     };
   if ((ph == RPH_K || ph == RPH_P) && st.mode == RK_HIST) {
     for (int j = tid; j < kResBins; j += kResThreads) {
@@ -607,7 +606,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
     u128 acc = 0;
     uint32_t kc = 0;
     int lastle = -1;
-    for (int v = wv0 + lane; v < wv1; v += 32) vec_kept(v, &acc, &kc, &lastle, 0, nullptr, nullptr);
+    for (int v = wv0 + lane; v < wv1; v += 32) vec_kept(v, &acc, &kc, &lastle, nullptr, nullptr);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       acc += shfl_down128(acc, o);
@@ -677,7 +676,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
           u128 m = 0;
           uint32_t n = 0;
           int ll = -1;
-          if (v < wv1) vec_kept(v, &m, &n, &ll, 0, nullptr, nullptr);
+          if (v < wv1) vec_kept(v, &m, &n, &ll, nullptr, nullptr);
           u128 incl = m;  // inclusive warp scan (u128)
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -694,7 +693,7 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
               u128 m2 = 0;
               uint32_t n2 = 0;
               int l2 = -1;
-              vec_kept(v, &m2, &n2, &l2, 0, &before, &pk);
+              vec_kept(v, &m2, &n2, &l2, &before, &pk);
               if (pk < 0) pk = l2;  // (rounding inside the vector: its last kept)
             }
             found = __shfl_sync(kFull, pk, __ffs(bal) - 1);
