@@ -471,7 +471,7 @@ def main():
     kt = None
     knames = ["stream_kernel", "select_rows_kernel", "exact_kernel"]
     if vocab_mode and a.exchange == "p2p" and not need_resolve:  # one library call: all 3 kernels marked
-        knames = ["stream_kernel", "select_rows_kernel", "merge_rows_kernel"]
+        knames = ["stream_kernel", "select_rows_kernel", "merge_rows_kernel"]  # (B <= 2 x SMs: merge fused)
     if not vocab_mode or knames[2] == "merge_rows_kernel":
         nk = 40
         s.set_timing(True)

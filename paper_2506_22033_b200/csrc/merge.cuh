@@ -544,6 +544,28 @@ __device__ __noinline__ void block_merge_row(const uint8_t* recs, int64_t pitch,
 #undef MTR
 }
 
+// NEXT-2: one thread waits until every rank's flag for row r has reached sq (acquire; bounded by the
+// handle's timeout); returns 1 on timeout
+__device__ __noinline__ int exch_wait_row(const ExchPeers& x, int r, uint32_t sq) {
+  const uint32_t* fl = reinterpret_cast<const uint32_t*>(x.bases[x.rank] + x.flags_off);
+  const uint64_t t0 = gtimer();
+  for (int q = 0; q < x.world; ++q)
+    while ((int32_t)(ld_acquire_flag(fl + (int64_t)q * x.nslots + r, x.world > 1) - sq) < 0) {
+      if (gtimer() - t0 > x.timeout_ns) return 1;
+      __nanosleep(64);
+    }
+  return 0;
+}
+__device__ __forceinline__ void exch_timeout_row(const RowOut& ro, int r) {
+  ro.tokens[r] = -1;
+  ro.logprobs[r] = NAN;
+  if (ro.flogprobs) ro.flogprobs[r] = NAN;
+  if (ro.status) ro.status[r] = SAMPLER_ROW_EXCHANGE_TIMEOUT;
+  RowInfo ri{};
+  ri.status = SAMPLER_ROW_EXCHANGE_TIMEOUT;
+  ro.info[r] = ri;
+}
+
 // Sharded phase 2: one CTA per row merges the row's per-rank candidate records (rank order,
 // P:375) into the final sample.
 struct MergeArgs {
@@ -597,31 +619,11 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
     const uint32_t sq = x.mseq[r] + 1;
     if (threadIdx.x == 0) {
       x.mseq[r] = sq;
-      const uint32_t* fl = reinterpret_cast<const uint32_t*>(x.bases[x.rank] + x.flags_off);
-      const uint64_t t0 = gtimer();
-      int timed_out = 0;
-      for (int q = 0; q < x.world && !timed_out; ++q) {
-        while ((int32_t)(ld_acquire_flag(fl + (int64_t)q * x.nslots + r, x.world > 1) - sq) < 0) {
-          if (gtimer() - t0 > x.timeout_ns) {
-            timed_out = 1;
-            break;
-          }
-          __nanosleep(64);
-        }
-      }
-      ms.bs.i[2] = timed_out;
+      ms.bs.i[2] = exch_wait_row(x, r, sq);
     }
     cbar();
     if (ms.bs.i[2]) {  // a peer never published: report the row, never hang the GPU
-      if (threadIdx.x == 0) {
-        m.ro.tokens[r] = -1;
-        m.ro.logprobs[r] = NAN;
-        if (m.ro.flogprobs) m.ro.flogprobs[r] = NAN;
-        if (m.ro.status) m.ro.status[r] = SAMPLER_ROW_EXCHANGE_TIMEOUT;
-        RowInfo ri{};
-        ri.status = SAMPLER_ROW_EXCHANGE_TIMEOUT;
-        m.ro.info[r] = ri;
-      }
+      if (threadIdx.x == 0) exch_timeout_row(m.ro, r);
       return;
     }
     recs = x.bases[x.rank] + (int64_t)(sq & 1) * x.par_pitch;

@@ -1014,15 +1014,23 @@ int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, in
     rc = launch_stream(h, stream_args(h, logits_slice, ld, B, slots_dev, params_dev, lp), lp.grid, st);
     if (rc) return rc;
     tmark(h, ++nk, st);
-    RowOut ro{nullptr, nullptr, nullptr, nullptr, h->d_info};
-    SelectArgs s = select_args(h, logits_slice, ld, B, slots_dev, params_dev, nullptr, 0, 0, ro, lp);
+    // phases == 3: the merge is fused into the selection kernel (each CTA publishes its row's record,
+    // waits for the peers' records of that row and merges them); phases 1 / 2 split it in two launches
+    // (fused only when every row's CTA is resident at once — 2 per SM — so no CTA waits for a peer
+    // row that its own GPU has not scheduled yet)
+    const bool fused = phases == 3 && B <= 2 * h->sm_count;
+    RowOut ro{fused ? tokens_dev : nullptr, fused ? logprobs_dev : nullptr, fused ? filtered_logprobs_dev : nullptr,
+              fused ? row_status_dev : nullptr, h->d_info};
+    SelectArgs s = select_args(h, logits_slice, ld, B, slots_dev, params_dev, seeds_dev, step, fused ? append : 0, ro,
+                               lp);
     s.mode = 1;
     s.xp = exch_peers(h);
+    s.fuse_merge = fused ? 1 : 0;
     rc = launch_select(h, s, B, st);
     if (rc) return rc;
     tmark(h, ++nk, st);
   }
-  if (phases & 2) {
+  if (phases == 2 || (phases == 3 && B > 2 * h->sm_count)) {
     RowOut ro{tokens_dev, logprobs_dev, filtered_logprobs_dev, row_status_dev, h->d_info};
     MergeArgs m = merge_args(h, slots_dev, params_dev, seeds_dev, step, append, ro);
     m.xp = exch_peers(h);

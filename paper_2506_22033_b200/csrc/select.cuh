@@ -56,6 +56,8 @@ struct SelectArgs {
   uint8_t* out_records;  // mode 1: one candidate record per row
   int64_t out_stride;
   ExchPeers xp;          // mode 1 with xp.world > 0: records stored into every peer (NEXT-2)
+  int fuse_merge;        // with xp: this CTA then waits for every rank's record of its row and merges
+                         // them (outputs in ro, append) — the exchange and the merge in one kernel
   int pen_in_b;          // small batches: the row's hand-off is built here, before the grid wait
   uint64_t* trace;       // debug: per-row phase timestamps (32 per row), nullable
 };
@@ -877,6 +879,21 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
         st_release_flag(reinterpret_cast<uint32_t*>(x.bases[p] + x.flags_off) + (int64_t)x.rank * x.nslots + r, sq,
                         x.world > 1);
     }
+    if (!a.fuse_merge) return;
+    // fused: every rank's record of this row (the peers' P2P stores land in this rank's buffer), then
+    // the merge + decision + append of merge.cuh in this CTA (its shared memory is free again)
+    if (tid == 0) {
+      x.mseq[r] = sq;
+      ctl[10] = exch_wait_row(x, r, sq);  // (ctl[10] is the decision's slot, unused in mode 1)
+    }
+    cbar();
+    if (ctl[10]) {
+      if (tid == 0) exch_timeout_row(a.ro, r);
+      return;
+    }
+    const uint8_t* recs = x.bases[x.rank] + (int64_t)(sq & 1) * x.par_pitch + (int64_t)r * x.row_stride;
+    block_merge_row(recs, x.rank_pitch, x.world, r, slot, prm, seed, a.step_dev ? *a.step_dev : a.step, a.V, a.kcand,
+                    0, nullptr, a.ro, a.append, a.hs, false, invalid, ms, nullptr);
     return;
   }
   // ---- decision (whole block, candidate-parallel)
