@@ -204,6 +204,25 @@ __device__ __forceinline__ uint64_t ex_sum_u64(uint64_t v, uint64_t* scr) {
 
 // Descending bitonic sort of buf[0..n) (n <= kGat) by the whole block.
 __device__ void ex_sort_desc(uint64_t* buf, int n) {
+  if (n <= 2 * kExThreads) {
+    // small sets (the usual boundary bucket): rank sort of the distinct composites, one barrier
+    // instead of the bitonic network's log2(N)^2 / 2 (45 at N = 512); in place via registers
+    uint64_t x[2];
+    int rk[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) x[q] = threadIdx.x + q * kExThreads < n ? buf[threadIdx.x + q * kExThreads] : 0ull;
+    for (int j = 0; j < n; ++j) {
+      const uint64_t y = buf[j];
+      rk[0] += y > x[0] ? 1 : 0;
+      rk[1] += y > x[1] ? 1 : 0;
+    }
+    ex_bar();
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (threadIdx.x + q * kExThreads < n) buf[rk[q]] = x[q];
+    ex_bar();
+    return;
+  }
   int N = 1;
   while (N < n) N <<= 1;
   for (int i = n + threadIdx.x; i < N; i += kExThreads) buf[i] = 0;
