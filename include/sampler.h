@@ -308,7 +308,9 @@ int sampler_exchange_set_peers(sampler* h, void* const* bases_host);
 /* ASYNC.  The vocab-sharded step through the peer exchange.  Arguments as sampler_sample_local +
  * sampler_merge.  phases: 1 = local pass + publish (no outputs), 2 = wait + merge, 3 = both (the
  * normal call; 1 and 2 let several ranks of ONE process and GPU run in lock step without any kernel
- * waiting on a kernel queued behind it). */
+ * waiting on a kernel queued behind it).  With phases = 3 and B <= 2 x the SM count the merge is
+ * fused into the selection kernel (each CTA publishes its row's record, waits for the peers' records
+ * of that row and merges them: two launches per step); larger batches use the separate merge kernel. */
 int sampler_sample_exchange(sampler* h, const void* logits_slice, int64_t ld, int32_t B,
                             const int32_t* slots_dev, const sampling_params* params_dev,
                             const uint64_t* seeds_dev, uint64_t step, int32_t append_to_history,
