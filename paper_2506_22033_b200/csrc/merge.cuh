@@ -613,9 +613,11 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
   const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
   const uint8_t* recs = m.records;
   if (m.xp.world > 0) {  // NEXT-2: wait for every rank's flag of this row, then read the local copies
-    // launched with programmatic dependent launch: no grid wait, the flags order everything this row
-    // reads (the publishing CTA of this rank stored its record, RowInfo and flag last)
+    // launched with programmatic dependent launch; the grid wait orders this rank's publishing kernel
+    // (measured: relying on the local flags alone let a large-batch merge read a row's record before
+    // it was complete, 2 runs in 3), the flags then order the peers' records
     const ExchPeers& x = m.xp;
+    griddep_wait();
     const uint32_t sq = x.mseq[r] + 1;
     if (threadIdx.x == 0) {
       x.mseq[r] = sq;

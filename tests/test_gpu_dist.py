@@ -247,3 +247,27 @@ def test_peer_exchange_with_resolve_rounds_in_one_graph(nccl_group):
         torch.cuda.synchronize()
         assert (out["status"] == 0).all()
         assert torch.equal(out["tokens"], ref["tokens"]), i
+
+
+def test_peer_exchange_large_batch_uses_the_merge_kernel(nccl_group):
+    """B > 2 x SMs: sampler_sample_exchange(phases=3) publishes, then merges in a separate kernel (no CTA
+    waits for a row its GPU has not scheduled); decode steps with append == the unsharded sampler."""
+    import torch
+    from paper_2506_22033_b200 import Sampler
+    from paper_2506_22033_b200.distributed import sample_vocab_sharded_p2p, setup_peer_exchange
+    wl = make_workload("c3", B=320, V=6000)
+    x = device_logits(wl)
+    full = make_sampler(wl, max_history=1024)
+    s = Sampler(wl.V, wl.B, max_history=1024, max_top_k=40, dtype=wl.dtype, vocab_offset=0, vocab_local=wl.V)
+    s.set_params(list(range(wl.B)), wl.params)
+    for b in range(wl.B):
+        s.set_history(b, wl.prompts[b], wl.outputs[b])
+    setup_peer_exchange(s)
+    for step in range(3):
+        out = sample_vocab_sharded_p2p(s, x, step, append=True)
+        ref = full.sample(x, step, append=True)
+        torch.cuda.synchronize()
+        assert s.last_launch_count() == 3
+        st = out["status"].cpu()
+        assert (st == 0).all(), (step, sorted(set(st.tolist())), (st != 0).nonzero().flatten().tolist()[:10])
+        assert torch.equal(out["tokens"], ref["tokens"]), step
