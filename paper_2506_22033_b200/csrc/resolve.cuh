@@ -734,6 +734,8 @@ __global__ void __launch_bounds__(kResThreads, 1) resolve_kernel(const __grid_co
       const uint4* src = reinterpret_cast<const uint4*>(out);
       for (int i = tid; i < kN16; i += kResThreads) dst[i] = src[i];
     }
+    if (x.world > 1) __threadfence_system();  // (each storing thread's own writes, before the release)
+    else __threadfence();
     __syncthreads();
     if (tid == 0) {
       const uint32_t sq = x.seq[row] + 1;

@@ -872,6 +872,10 @@ __global__ void __launch_bounds__(kBT, 2) select_rows_kernel(const __grid_consta
       for (int i = tid; i < n; i += kBT) oe[i] = ms.top[i];
       if (tid == 0) *reinterpret_cast<RecHdr*>(out) = h;
     }
+    // every storing thread's own fence (a fence orders only its thread's writes), then the barrier,
+    // then one release of the flags
+    if (x.world > 1) __threadfence_system();
+    else __threadfence();
     cbar();
     if (tid == 0) {  // release (system scope) after the CTA barrier: orders every thread's record stores
       x.seq[r] = sq;
