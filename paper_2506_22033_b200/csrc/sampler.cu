@@ -142,7 +142,8 @@ const char* sampler_version(void) {
   return "paper_2506_22033_b200 sampler: sm_100a (compute_100a); phase A: persistent warp-specialised "
          "stream (1-D bulk-copy ring, penalty presence bitmap, packed bf16 exp-sum, group/step keys); "
          "phase B: per-row step-key bound, group re-read, exact top-k, candidate-parallel decision, "
-         "Philox4x32-10; exact multi-pass fallback";
+         "Philox4x32-10; exact float64 cluster kernel for unbounded rows; vocab-sharded: NCCL or one-shot "
+         "peer exchange (fused merge), distributed resolve rounds";
 }
 
 const char* sampler_last_error(const sampler* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
