@@ -613,17 +613,18 @@ __global__ void __launch_bounds__(kBT, 2) merge_rows_kernel(const __grid_constan
   const uint64_t seed = m.seeds ? m.seeds[r] : prm.seed;
   const uint8_t* recs = m.records;
   if (m.xp.world > 0) {  // NEXT-2: wait for every rank's flag of this row, then read the local copies
-    // launched with programmatic dependent launch; the grid wait orders this rank's publishing kernel
-    // (measured: relying on the local flags alone let a large-batch merge read a row's record before
-    // it was complete, 2 runs in 3), the flags then order the peers' records
+    // launched with programmatic dependent launch; the grid wait orders this rank's publishing kernel,
+    // the flags the peers' records
     const ExchPeers& x = m.xp;
     griddep_wait();
-    const uint32_t sq = x.mseq[r] + 1;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // (one thread reads and advances the row's sequence number; the others
+      const uint32_t sq = x.mseq[r] + 1;  //  take it from shared memory after the barrier)
       x.mseq[r] = sq;
+      ms.bs.i[3] = (int)sq;
       ms.bs.i[2] = exch_wait_row(x, r, sq);
     }
     cbar();
+    const uint32_t sq = (uint32_t)ms.bs.i[3];
     if (ms.bs.i[2]) {  // a peer never published: report the row, never hang the GPU
       if (threadIdx.x == 0) exch_timeout_row(m.ro, r);
       return;

@@ -543,6 +543,7 @@ static StreamArgs stream_args(sampler* h, const void* logits, int64_t ld, int32_
   a.gkeys = h->d_gkeys;
   a.trace = h->d_trace;
   a.pen_in_b = pen_in_b(h, B, lp);
+  a.early_tiles = a.pen_in_b;
   return a;
 }
 

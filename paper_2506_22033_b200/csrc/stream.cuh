@@ -97,6 +97,7 @@ struct StreamArgs {
   uint16_t* gkeys;     // [B][gk_stride(Vq)]: group keys | step keys
   uint64_t* trace;     // debug: per-CTA start / end timestamps (globaltimer ns, 64 per CTA), nullable
   int pen_in_b;        // small batches: phase B builds the hand-off in its prologue (this pass skips it)
+  int early_tiles;     // small batches: the first tiles' logits copies before the grid wait
 };
 
 // ---- packed binary32 pairs (sm_100a FADD2 / FMUL2) ----------------------------------
@@ -260,8 +261,10 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
   // previous kernel of the stream (the last step's phase B) was still running — wait for it before
   // any memory access (it appends to the histories this pass reads, and reads the scratch this
   // pass writes); then let phase B's CTAs be scheduled as this grid's CTAs retire
-  griddep_wait();
-  griddep_launch();
+  if (!a.early_tiles) {
+    griddep_wait();
+    griddep_launch();
+  }
   const int64_t s0 = (int64_t)blockIdx.x * a.span;
   const int nspan = (int)min((int64_t)a.span, a.nsteps - s0);  // steps of this CTA
   const int ntiles = (nspan + kTileSteps - 1) / kTileSteps;
@@ -284,6 +287,43 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
     fence_mbar_init();
   }
   __syncthreads();
+  // small batches (early_tiles): the first kNS tiles' logits are this call's input, not the last
+  // step's output, so their bulk copies are issued before the grid wait (the bitmap words — history
+  // state the last step's phase B appends to — after it) and the ring fills while the previous kernel
+  // drains (measured: c5 B = 1 19.8 -> 18.8 us; at c3 it costs 0.9 us, so large batches wait first)
+  if (a.early_tiles) {
+    if (w == kCW && lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      for (int t = 0; t < kNS && t < ntiles; ++t) {
+        const int64_t st0 = s0 + (int64_t)t * kTileSteps;
+        int r = (int)(st0 / a.spr), k = (int)(st0 - (int64_t)r * a.spr);
+        const int n = min(kTileSteps, nspan - t * kTileSteps);
+        uint32_t bytes = 0;
+        {
+          int kk = k;
+          for (int j = 0; j < n; ++j) {
+            bytes += (uint32_t)min(kStepVec, nvv - kk * kStepVec) * 16u;
+            if (++kk == a.spr) kk = 0;
+          }
+        }
+        mbar_arrive_expect_tx(full + t, bytes + (uint32_t)n * 128u);
+        uint8_t* dst = ring + t * (kTileSteps * kStepBytes);
+        for (int j = 0; j < n;) {
+          const int j0 = j, k0 = k;
+          uint32_t nb = 0;
+          do {
+            nb += (uint32_t)min(kStepVec, nvv - k * kStepVec) * 16u;
+            ++j;
+            ++k;
+          } while (j < n && k < a.spr);
+          bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + t, pol);
+          if (k == a.spr) { k = 0; ++r; }
+        }
+      }
+    }
+    griddep_wait();
+    griddep_launch();
+  }
 
   if (w == kCW + 1) {
     // ================= penalty warp: the hand-off of the rows that start in this span =================
@@ -374,7 +414,8 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
           }
         }
         constexpr bool bmcopy = true;
-        mbar_arrive_expect_tx(full + sl, bytes + (bmcopy ? (uint32_t)n * 128u : 0u));
+        const bool early = a.early_tiles && t < kNS;  // (logits already in flight, expect_tx done)
+        if (!early) mbar_arrive_expect_tx(full + sl, bytes + (bmcopy ? (uint32_t)n * 128u : 0u));
         uint8_t* dst = ring + sl * (kTileSteps * kStepBytes);
         uint8_t* bdst = reinterpret_cast<uint8_t*>(bm) + sl * (kTileSteps * 128);
         // one bulk copy per run of consecutive steps of one row (contiguous in global memory)
@@ -386,7 +427,8 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) stream_kerne
             ++j;
             ++k;
           } while (j < n && k < a.spr);
-          bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
+          if (!early)
+            bulk_g2s(dst + j0 * kStepBytes, lg + ((int64_t)r * ldb + (int64_t)k0 * kStepBytes), nb, full + sl, pol);
           // the run's penalty-bitmap words (HistState::pmask, 128 B per step)
           if (bmcopy) {
             const int slot = row_slot(a.slots, r, a.hs.nslots, nullptr);
