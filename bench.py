@@ -158,12 +158,12 @@ def cpu_model():
 def load_parity():
     """The committed north-star parity statistics (tools/parity_stats.py on a B200): rows, flagged
     fraction at the 1e-9 excuse band and at the literal 1e-6, token mismatches, unflagged ones."""
-    p = os.path.join(ROOT, "profiles", "parity_r02i.json")
+    p = os.path.join(ROOT, "profiles", "parity_r02j.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
     return {k: d.get(k) for k in ("rows", "flag_frac", "flag6_frac", "mismatch_frac", "unflagged_mismatch",
-                                  "prob_violations", "pass")} | {"source": "profiles/parity_r02i.json"}
+                                  "prob_violations", "pass")} | {"source": "profiles/parity_r02j.json"}
 
 
 def cpu_cores():
