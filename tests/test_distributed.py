@@ -109,6 +109,12 @@ def _worker(rank, world, port, q):
         g, w, b, step = s.merged
         ok = w == world and b == B and step == 3 and "tokens" in out
         ok = ok and s.rounds_ok and s.last_round == 3  # adaptive stop: 3 exchanges, rank-ordered payloads
+        # the fixed round count (CUDA-graph mode): exactly `rounds` exchanges whatever the active count
+        from paper_2506_22033_b200.distributed import resolve_unbounded
+        s.rounds_ok = True
+        n = resolve_unbounded(s, torch.zeros(B, hi - lo), 4, {}, lambda g, p: dist.all_gather_into_tensor(g, p),
+                              world, rank, rounds=5)
+        ok = ok and n == 5 and s.last_round == 5
         rb = s.record_bytes(B)
         for r in range(world):
             v = torch.arange(rb, dtype=torch.int64)
